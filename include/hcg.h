@@ -1,0 +1,185 @@
+/*
+ * hcg.h -- C ABI of the B200-native Hypercurves/Multicurves kNN hot path.
+ *
+ * Plain C: no torch, no C++ types, no exceptions cross this boundary.  Every
+ * entry point returns an hcg_status; on failure hcg_last_error() holds a
+ * thread-local message.  The C++ wrapper in hypercurves_b200.hpp maps the codes
+ * back to the reference's exception types (std::invalid_argument for
+ * HCG_EINVAL / HCG_ECAPACITY / HCG_ENONFINITE, std::runtime_error otherwise),
+ * as the reference throws them (curve.cpp:35-59,167; vecio.cpp:15,78,88,116).
+ *
+ * Which reference interface each entry point replaces (paths relative to the
+ * reference root):
+ *   hcg_make_lut       quantize_component over the 256 byte values of a view
+ *                      (proj/src/curve.cpp:166-174; bvecs widening vecio.cpp:50-51)
+ *   hcg_build          hc::MulticurvesIndex(const Dataset&, ProjectionScheme)
+ *                      (proj/include/hypercurves/multicurves.hpp:77; Alg. 1)
+ *   hcg_search         hc::MulticurvesIndex::search(q, SearchParams) batched
+ *                      (multicurves.hpp:81; Alg. 2)
+ *   hcg_keys           hc::curve_encode(kind, project(v, scheme, c))  (curve.cpp:162-164,
+ *                      multicurves.hpp:40)
+ *   hcg_sorted         hc::SubIndex::entries()            (multicurves.hpp:55)
+ *   hcg_windows        hc::SubIndex::rank_of / window     (multicurves.hpp:57-63)
+ *   hcg_candidates     hc::MulticurvesIndex::candidate_union (multicurves.hpp:87-89)
+ *   hcg_brute_force    hc::brute_force_knn                (proj/src/vecio.cpp:115-122)
+ *   hcg_search_packed  per-shard search of hypershard's IHLS stage
+ *   hcg_merge_packed   hypershard aggregate: k-way merge by (distance, id)
+ *
+ *   hcg_miss_bound /   equivalence module: binomial_tail / miss_bound / plan_depth
+ *   hcg_plan_depth
+ *   hcg_gen_rows /     the counter-based synthetic SIFT-like generator of
+ *   hcg_gen_queries    SURVEY.md §8(d) (bench/test data; bit-identical to the oracle)
+ *
+ * Data model.  Descriptors are byte vectors (bvecs).  The reference sees each
+ * byte b through a "view" v(b) (raw: float(b); lifted: 1 + b/256).  The
+ * quantizer only ever sees those 256 values, so the scheme carries the 256
+ * quantized cells (hcg_make_lut computes them with the reference's
+ * float_to_ordinal >> (32 - m) rule) and a distance scale: the reference's
+ * squared distance is exactly sqdist_u32 * dist_scale^2 for affine views with a
+ * power-of-two scale, so search results are bit-exact in both views.
+ *
+ * Pointers.  Every data pointer may be host memory (pageable or pinned) or
+ * device memory of the index's device; the library stages host buffers itself
+ * (cudaMemcpyAsync on `stream`) and synchronises `stream` before returning
+ * whenever an output lives in host memory.  With all-device buffers the calls
+ * are stream-ordered and asynchronous.  `stream` may be NULL (legacy default
+ * stream).
+ *
+ * Threading.  One index lives on one device.  Concurrent searches on one index
+ * from different streams/threads are allowed (search is const);
+ * build and free are exclusive.
+ */
+#ifndef HCG_H
+#define HCG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum hcg_status {
+    HCG_OK = 0,
+    HCG_EINVAL = -1,      /* precondition violated (reference: std::invalid_argument) */
+    HCG_ECAPACITY = -2,   /* key width / k / depth beyond capacity (curve.cpp:43-45)  */
+    HCG_ENONFINITE = -3,  /* NaN/Inf component (curve.cpp:167)                        */
+    HCG_ENOMEM = -4,      /* device allocation failed                                  */
+    HCG_ECUDA = -5,       /* CUDA runtime error                                        */
+    HCG_ENODEV = -6       /* no usable sm_100 device                                   */
+} hcg_status;
+
+typedef enum hcg_curve_kind { HCG_ZORDER = 0, HCG_HILBERT = 1 } hcg_curve_kind;
+
+#define HCG_MAX_KEY_BITS 1024  /* HC_MAX_KEY_BITS, keys.hpp:15-23 */
+#define HCG_MAX_CURVE_DIMS 128 /* dims feeding one curve          */
+#define HCG_MAX_K 256          /* largest k of the warp top-k      */
+#define HCG_MAX_ROW_BYTES 512  /* descriptor length (bytes)        */
+
+/* ProjectionScheme (multicurves.hpp:18-32) plus the view of the bytes. */
+typedef struct hcg_scheme {
+    uint32_t d_full;            /* bytes per descriptor                            */
+    uint32_t curves;            /* number of subindexes                            */
+    uint32_t bits_per_dim;      /* m in [1, 32]                                    */
+    uint32_t curve_kind;        /* hcg_curve_kind                                  */
+    const uint32_t* assign_off; /* curves+1 offsets into assign                    */
+    const uint32_t* assign;     /* assign[assign_off[c] + s] = input dim of slot s */
+    uint32_t cell_lut[256];     /* quantized cell of each byte value (m bits)      */
+    double dist_scale;          /* view scale: distance = sqrt(sqdist) * dist_scale */
+} hcg_scheme;
+
+typedef struct hcg_index hcg_index;
+
+const char* hcg_last_error(void);
+const char* hcg_version(void);
+
+/* Quantized cell of every byte value for the affine view v(b) = offset + b*scale
+ * (computed in f32 exactly like the reference's widened components).  Fails
+ * with HCG_ENONFINITE when a value is not finite and HCG_EINVAL for m outside
+ * [1, 32]. */
+hcg_status hcg_make_lut(float offset, float scale, uint32_t bits_per_dim, uint32_t* lut256);
+
+/* Round-robin assignment, seed 0: dim j -> curve j % curves,
+ * slot j / curves.  assign_off has curves+1 entries, assign has d_full. */
+hcg_status hcg_default_assignment(uint32_t d_full, uint32_t curves, uint32_t* assign_off,
+                                  uint32_t* assign);
+
+/* Build an index over n descriptors (rows: n x d_full bytes).  The id of row s
+ * is id_base + s * id_stride (the dataset's ids 0..n-1 are base 0, stride 1; a
+ * shard of `id mod G` partitioning is base r, stride G).  The index copies the
+ * rows into HBM and owns all device memory. */
+hcg_status hcg_build(const hcg_scheme* scheme, const uint8_t* rows, uint64_t n, uint64_t id_base,
+                     uint64_t id_stride, int device, void* stream, hcg_index** out);
+hcg_status hcg_free(hcg_index* index);
+
+uint64_t hcg_size(const hcg_index* index);
+uint32_t hcg_curves(const hcg_index* index);
+/* 64-bit words of the full key of curve c: ceil(dims_c * m / 64). */
+uint32_t hcg_key_words(const hcg_index* index, uint32_t curve);
+/* Device bytes owned by the index. */
+uint64_t hcg_device_bytes(const hcg_index* index);
+
+/* Batched search: for each of nq queries (nq x d_full bytes) the top-k of the
+ * deduplicated union of every curve's probe-depth window, ordered by
+ * (squared distance, id).  out_ids / out_sqdist are nq x k; entries at or past
+ * out_len[q] are id UINT64_MAX, sqdist UINT32_MAX.  The reference's rooted
+ * distance is sqrt((double)sqdist) * dist_scale. */
+hcg_status hcg_search(const hcg_index* index, const uint8_t* queries, uint32_t nq, uint32_t k,
+                      uint32_t depth, uint64_t* out_ids, uint32_t* out_sqdist, uint32_t* out_len,
+                      void* stream);
+
+/* Per-shard search writing packed (sqdist << 32 | id) u64 per result, nq x k,
+ * padding UINT64_MAX; requires ids < 2^32.  Input to hcg_merge_packed. */
+hcg_status hcg_search_packed(const hcg_index* index, const uint8_t* queries, uint32_t nq,
+                             uint32_t k, uint32_t depth, uint64_t* out_packed, void* stream);
+
+/* k-way merge of `parts` packed lists (parts x nq x k, each sorted ascending)
+ * into the global top-k per query.  device = CUDA device of
+ * the buffers. */
+hcg_status hcg_merge_packed(const uint64_t* packed, uint32_t parts, uint32_t nq, uint32_t k,
+                            uint64_t* out_ids, uint32_t* out_sqdist, uint32_t* out_len, int device,
+                            void* stream);
+
+/* ---- parity taps ---- */
+/* Full-width keys (hcg_key_words words per key, least significant word first,
+ * as ExtendedKey::words) of n arbitrary rows on curve c. */
+hcg_status hcg_keys(const hcg_index* index, const uint8_t* rows, uint64_t n, uint32_t curve,
+                    uint64_t* out_words, void* stream);
+/* Sorted subindex c: ids (n) and, when out_words != NULL, full keys (n x words). */
+hcg_status hcg_sorted(const hcg_index* index, uint32_t curve, uint64_t* out_ids,
+                      uint64_t* out_words, void* stream);
+/* rank_of and window [begin, end) of every (query, curve), nq x curves each. */
+hcg_status hcg_windows(const hcg_index* index, const uint8_t* queries, uint32_t nq, uint32_t depth,
+                       uint64_t* out_rank, uint64_t* out_begin, uint64_t* out_end, void* stream);
+/* Deduplicated candidate ids per query (set semantics, order unspecified):
+ * out_ids is nq x cap, out_count[q] the number of unique candidates.  Fails
+ * with HCG_ECAPACITY when a query has more than cap candidates. */
+hcg_status hcg_candidates(const hcg_index* index, const uint8_t* queries, uint32_t nq,
+                          uint32_t depth, uint64_t* out_ids, uint32_t cap, uint32_t* out_count,
+                          void* stream);
+
+/* Exact kNN over the index's rows (ground truth for recall, vecio.cpp:115-122). */
+hcg_status hcg_brute_force(const hcg_index* index, const uint8_t* queries, uint32_t nq, uint32_t k,
+                           uint64_t* out_ids, uint32_t* out_sqdist, uint32_t* out_len,
+                           void* stream);
+
+/* ---- probe-depth planner (equivalence module, host math) ---- */
+/* P[Bin(trials, p) > phi]. */
+double hcg_binomial_tail(uint32_t trials, double p, uint32_t phi);
+/* 1 - max(0, 1 - Phi * P[Bin(Phi, 1/shards) > phi])^2 clamped to [0,1]
+ * (PAPER.md:895-896). */
+double hcg_miss_bound(uint32_t Phi, uint32_t shards, uint32_t phi);
+/* Smallest phi <= Phi with miss_bound <= target. */
+uint32_t hcg_plan_depth(uint32_t Phi, uint32_t shards, double target);
+
+/* ---- synthetic data; out is a device pointer ---- */
+/* Row i of the output is generator row first + i * stride (128 bytes each). */
+hcg_status hcg_gen_rows(uint64_t first, uint64_t stride, uint64_t count, uint8_t* out_dev,
+                        int device, void* stream);
+hcg_status hcg_gen_queries(uint64_t first, uint64_t count, uint64_t n_db, uint8_t* out_dev,
+                           int device, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HCG_H */

@@ -1,0 +1,118 @@
+"""ctypes binding of the C ABI in include/hcg.h (libhcg.so, built in-tree).
+
+No fallback: if the CUDA library is missing the import fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libhcg.so")
+
+HCG_OK = 0
+HCG_EINVAL = -1
+HCG_ECAPACITY = -2
+HCG_ENONFINITE = -3
+HCG_ENOMEM = -4
+HCG_ECUDA = -5
+HCG_ENODEV = -6
+
+HCG_ZORDER = 0
+HCG_HILBERT = 1
+HCG_MAX_K = 256
+HCG_MAX_KEY_BITS = 1024
+
+# Every symbol include/hcg.h declares (checked by tests/test_abi.py).
+EXPORTS = [
+    "hcg_last_error", "hcg_version", "hcg_make_lut", "hcg_default_assignment", "hcg_build",
+    "hcg_free", "hcg_size", "hcg_curves", "hcg_key_words", "hcg_device_bytes", "hcg_search",
+    "hcg_search_packed", "hcg_merge_packed", "hcg_keys", "hcg_sorted", "hcg_windows",
+    "hcg_candidates", "hcg_brute_force", "hcg_binomial_tail", "hcg_miss_bound",
+    "hcg_plan_depth", "hcg_gen_rows", "hcg_gen_queries",
+]
+
+
+class HcgScheme(C.Structure):
+    _fields_ = [
+        ("d_full", C.c_uint32),
+        ("curves", C.c_uint32),
+        ("bits_per_dim", C.c_uint32),
+        ("curve_kind", C.c_uint32),
+        ("assign_off", C.POINTER(C.c_uint32)),
+        ("assign", C.POINTER(C.c_uint32)),
+        ("cell_lut", C.c_uint32 * 256),
+        ("dist_scale", C.c_double),
+    ]
+
+
+class HcgError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[hcg {code}] {msg}")
+        self.code = code
+
+
+class HcgInvalidArgument(HcgError, ValueError):
+    """Mirrors the reference's std::invalid_argument (curve.cpp:35-59, vecio.cpp:15,78,88,116)."""
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: the CUDA extension must be built "
+            "(python -c 'import __graft_entry__ as g; g.build()'); there is no CPU fallback")
+    L = C.CDLL(LIB_PATH)
+    vp, u8, u32, u64 = C.c_void_p, C.c_uint8, C.c_uint32, C.c_uint64
+    P = C.POINTER
+    L.hcg_last_error.restype = C.c_char_p
+    L.hcg_version.restype = C.c_char_p
+    L.hcg_make_lut.argtypes = [C.c_float, C.c_float, u32, P(u32)]
+    L.hcg_default_assignment.argtypes = [u32, u32, P(u32), P(u32)]
+    L.hcg_build.argtypes = [P(HcgScheme), vp, u64, u64, u64, C.c_int, vp, P(vp)]
+    L.hcg_free.argtypes = [vp]
+    L.hcg_size.restype = u64
+    L.hcg_size.argtypes = [vp]
+    L.hcg_curves.restype = u32
+    L.hcg_curves.argtypes = [vp]
+    L.hcg_key_words.restype = u32
+    L.hcg_key_words.argtypes = [vp, u32]
+    L.hcg_device_bytes.restype = u64
+    L.hcg_device_bytes.argtypes = [vp]
+    L.hcg_search.argtypes = [vp, vp, u32, u32, u32, vp, vp, vp, vp]
+    L.hcg_search_packed.argtypes = [vp, vp, u32, u32, u32, vp, vp]
+    L.hcg_merge_packed.argtypes = [vp, u32, u32, u32, vp, vp, vp, C.c_int, vp]
+    L.hcg_keys.argtypes = [vp, vp, u64, u32, vp, vp]
+    L.hcg_sorted.argtypes = [vp, u32, vp, vp, vp]
+    L.hcg_windows.argtypes = [vp, vp, u32, u32, vp, vp, vp, vp]
+    L.hcg_candidates.argtypes = [vp, vp, u32, u32, vp, u32, vp, vp]
+    L.hcg_brute_force.argtypes = [vp, vp, u32, u32, vp, vp, vp, vp]
+    L.hcg_binomial_tail.restype = C.c_double
+    L.hcg_binomial_tail.argtypes = [u32, C.c_double, u32]
+    L.hcg_miss_bound.restype = C.c_double
+    L.hcg_miss_bound.argtypes = [u32, u32, u32]
+    L.hcg_plan_depth.restype = u32
+    L.hcg_plan_depth.argtypes = [u32, u32, C.c_double]
+    L.hcg_gen_rows.argtypes = [u64, u64, u64, vp, C.c_int, vp]
+    L.hcg_gen_queries.argtypes = [u64, u64, u64, vp, C.c_int, vp]
+    for name in ("hcg_make_lut", "hcg_default_assignment", "hcg_build", "hcg_free", "hcg_search",
+                 "hcg_search_packed", "hcg_merge_packed", "hcg_keys", "hcg_sorted", "hcg_windows",
+                 "hcg_candidates", "hcg_brute_force", "hcg_gen_rows", "hcg_gen_queries"):
+        getattr(L, name).restype = C.c_int
+    del u8
+    _lib = L
+    return L
+
+
+def check(rc: int) -> None:
+    if rc == HCG_OK:
+        return
+    msg = lib().hcg_last_error().decode(errors="replace")
+    if rc in (HCG_EINVAL, HCG_ECAPACITY, HCG_ENONFINITE):
+        raise HcgInvalidArgument(rc, msg)
+    raise HcgError(rc, msg)

@@ -1,0 +1,771 @@
+// api.cu -- host side of the C ABI declared in include/hcg.h.
+//
+// Owns device memory of an index, stages host buffers, validates the
+// reference's preconditions and turns them into status codes (the C++ wrapper
+// turns the codes back into the reference's exceptions).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "hcg_host.hpp"
+#include "hcg_internal.cuh"
+
+struct hcg_index {
+    int device = 0;
+    uint32_t d_full = 0, pitch = 0, C = 0, m = 0, kind = 0;
+    double dist_scale = 1.0;
+    uint64_t n = 0, id_base = 0, id_stride = 1;
+    std::vector<uint32_t> off, assign;
+    uint32_t lut[256] = {};
+    int dmax = 8, wsmax = 1;
+    uint8_t* rows = nullptr;
+    uint32_t* d_lut = nullptr;
+    uint16_t* d_assign = nullptr;
+    std::vector<hcg::CurveDev> curves;
+    hcg::CurveDev* d_curves = nullptr;
+    std::vector<uint64_t*> keys;
+    std::vector<uint32_t*> slots;
+    uint32_t** d_slot_ptrs = nullptr;
+    uint64_t bytes = 0;
+};
+
+namespace hcg {
+
+namespace {
+thread_local std::string g_err;
+}
+
+hcg_status set_error(hcg_status code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+hcg_status check_launch(const char* what) {
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_error(HCG_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    return HCG_OK;
+}
+
+namespace {
+
+#define HCG_TRY_CUDA(call)                                                                          \
+    do {                                                                                            \
+        const cudaError_t e_ = (call);                                                              \
+        if (e_ != cudaSuccess) return set_error(HCG_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+#define HCG_TRY(call)                       \
+    do {                                    \
+        const hcg_status r_ = (call);       \
+        if (r_ != HCG_OK) return r_;        \
+    } while (0)
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+// Stream-ordered scratch, released (stream-ordered) when the call returns.
+struct Scratch {
+    cudaStream_t st;
+    std::vector<void*> ptrs;
+    explicit Scratch(cudaStream_t s) : st(s) {}
+    ~Scratch() {
+        for (void* p : ptrs) cudaFreeAsync(p, st);
+    }
+    template <class T>
+    T* alloc(size_t count) {
+        void* p = nullptr;
+        if (cudaMallocAsync(&p, std::max<size_t>(count, 1) * sizeof(T), st) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        ptrs.push_back(p);
+        return static_cast<T*>(p);
+    }
+};
+
+bool is_device_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+uint32_t round16(uint32_t x) { return (x + 15u) & ~15u; }
+
+// Device copy of nrows x d_full bytes with row pitch `pitch` (zero padded).
+hcg_status stage_rows(Scratch& sc, const uint8_t* src, uint64_t nrows, uint32_t d_full, uint32_t pitch,
+                      const uint8_t** out) {
+    if (nrows == 0) {
+        *out = nullptr;
+        return HCG_OK;
+    }
+    if (pitch == d_full && is_device_ptr(src) && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+        *out = src;
+        return HCG_OK;
+    }
+    uint8_t* d = sc.alloc<uint8_t>(size_t(nrows) * pitch);
+    if (!d) return set_error(HCG_ENOMEM, "query staging buffer");
+    if (pitch != d_full) HCG_TRY_CUDA(cudaMemsetAsync(d, 0, size_t(nrows) * pitch, sc.st));
+    HCG_TRY_CUDA(cudaMemcpy2DAsync(d, pitch, src, d_full, d_full, nrows, cudaMemcpyDefault, sc.st));
+    *out = d;
+    return HCG_OK;
+}
+
+template <class T>
+struct OutBuf {
+    T* user = nullptr;
+    T* dev = nullptr;
+    size_t count = 0;
+    bool host = false;
+};
+
+template <class T>
+hcg_status stage_out(Scratch& sc, T* user, size_t count, OutBuf<T>* o) {
+    o->user = user;
+    o->count = count;
+    o->host = user && !is_device_ptr(user);
+    o->dev = o->host ? sc.alloc<T>(count) : user;
+    if (user && !o->dev) return set_error(HCG_ENOMEM, "output staging buffer");
+    return HCG_OK;
+}
+
+template <class T>
+hcg_status finish_out(Scratch& sc, const OutBuf<T>& o) {
+    if (o.host && o.count)
+        HCG_TRY_CUDA(cudaMemcpyAsync(o.user, o.dev, o.count * sizeof(T), cudaMemcpyDeviceToHost, sc.st));
+    return HCG_OK;
+}
+
+uint32_t ordinal_of(float x) {
+    uint32_t bits;
+    std::memcpy(&bits, &x, 4);
+    return (bits >> 31) ? ~bits : (bits | 0x80000000u);
+}
+
+int pow2_bucket(uint32_t v, int lo, int hi) {
+    int b = lo;
+    while (b < int(v) && b < hi) b <<= 1;
+    return b;
+}
+
+hcg_status check_index(const hcg_index* ix) {
+    if (!ix) return set_error(HCG_EINVAL, "null index");
+    return HCG_OK;
+}
+
+void release(hcg_index* ix) {
+    if (!ix) return;
+    DeviceGuard g(ix->device);
+    cudaFree(ix->rows);
+    cudaFree(ix->d_lut);
+    cudaFree(ix->d_assign);
+    cudaFree(ix->d_curves);
+    cudaFree(ix->d_slot_ptrs);
+    for (auto* p : ix->keys) cudaFree(p);
+    for (auto* p : ix->slots) cudaFree(p);
+    delete ix;
+}
+
+template <class T>
+hcg_status dev_alloc(T** p, size_t count, uint64_t* bytes) {
+    const size_t b = std::max<size_t>(count, 1) * sizeof(T);
+    if (cudaMalloc(reinterpret_cast<void**>(p), b) != cudaSuccess) {
+        cudaGetLastError();
+        return set_error(HCG_ENOMEM, "device allocation of " + std::to_string(b) + " bytes failed");
+    }
+    *bytes += b;
+    return HCG_OK;
+}
+
+hcg_status validate_scheme(const hcg_scheme* s) {
+    if (!s) return set_error(HCG_EINVAL, "null scheme");
+    if (s->d_full < 1 || s->d_full > HCG_MAX_ROW_BYTES)
+        return set_error(HCG_ECAPACITY, "d_full must be in [1, " + std::to_string(HCG_MAX_ROW_BYTES) + "]");
+    if (s->curves < 1 || s->curves > s->d_full) return set_error(HCG_EINVAL, "curves must be in [1, d_full]");
+    if (s->bits_per_dim < 1 || s->bits_per_dim > 32) return set_error(HCG_EINVAL, "bits_per_dim out of range [1,32]");
+    if (s->curve_kind > 1) return set_error(HCG_EINVAL, "unknown curve kind");
+    if (!s->assign_off || !s->assign) return set_error(HCG_EINVAL, "null assignment");
+    if (!(s->dist_scale > 0.0) || !std::isfinite(s->dist_scale)) return set_error(HCG_EINVAL, "dist_scale must be > 0");
+    std::vector<bool> covered(s->d_full, false);
+    for (uint32_t c = 0; c < s->curves; ++c) {
+        if (s->assign_off[c + 1] < s->assign_off[c]) return set_error(HCG_EINVAL, "assignment offsets not monotone");
+        const uint32_t d = s->assign_off[c + 1] - s->assign_off[c];
+        if (d < 1) return set_error(HCG_EINVAL, "curve with no dimensions");
+        if (uint64_t(d) * s->bits_per_dim > HCG_MAX_KEY_BITS)
+            return set_error(HCG_ECAPACITY, "key width " + std::to_string(uint64_t(d) * s->bits_per_dim) +
+                                                " exceeds capacity " + std::to_string(HCG_MAX_KEY_BITS));
+        if (d > HCG_MAX_CURVE_DIMS) return set_error(HCG_ECAPACITY, "more than 128 dimensions on one curve");
+        for (uint32_t i = s->assign_off[c]; i < s->assign_off[c + 1]; ++i) {
+            if (s->assign[i] >= s->d_full) return set_error(HCG_EINVAL, "assignment out of range");
+            covered[s->assign[i]] = true;
+        }
+    }
+    for (bool cv : covered)
+        if (!cv) return set_error(HCG_EINVAL, "input dimension not covered by any curve");
+    const uint64_t lim = s->bits_per_dim == 32 ? (1ull << 32) : (1ull << s->bits_per_dim);
+    for (int b = 0; b < 256; ++b)
+        if (s->cell_lut[b] >= lim) return set_error(HCG_EINVAL, "cell_lut entry exceeds 2^m");
+    return HCG_OK;
+}
+
+hcg_status check_device(int device) {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+        cudaGetLastError();
+        return set_error(HCG_ENODEV, "no CUDA device");
+    }
+    if (device < 0 || device >= count) return set_error(HCG_ENODEV, "device ordinal out of range");
+    int major = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
+    if (major != 10) return set_error(HCG_ENODEV, "this build targets sm_100a (B200) only");
+    return HCG_OK;
+}
+
+// Build curve c: K1 keys, prefix detection, K2 stable radix sort, suffix pack.
+hcg_status build_curve(hcg_index* ix, uint32_t c, cudaStream_t st) {
+    const uint64_t n = ix->n;
+    const uint32_t d = ix->off[c + 1] - ix->off[c];
+    const uint32_t W = (d * ix->m + 63) / 64;
+    CurveDev& cv = ix->curves[c];
+    std::memset(&cv, 0, sizeof(cv));
+    cv.w = W;
+    cv.dims = d;
+    cv.off = ix->off[c];
+    if (n == 0) {
+        cv.ws = 1;
+        return HCG_OK;
+    }
+    Scratch sc(st);
+    uint64_t* keys_soa = sc.alloc<uint64_t>(size_t(W) * n);
+    unsigned long long* or_and = sc.alloc<unsigned long long>(2 * W);
+    if (!keys_soa || !or_and) return set_error(HCG_ENOMEM, "key buffers");
+    HCG_TRY_CUDA(cudaMemsetAsync(or_and, 0, W * 8, st));
+    HCG_TRY_CUDA(cudaMemsetAsync(or_and + W, 0xFF, W * 8, st));
+    HCG_TRY(keygen_rows(ix->rows, n, ix->pitch, ix->d_assign + ix->off[c], int(d), int(ix->m), int(ix->kind),
+                        ix->d_lut, keys_soa, int(W), or_and, ix->dmax, st));
+    std::vector<uint64_t> oa(2 * W);
+    HCG_TRY_CUDA(cudaMemcpyAsync(oa.data(), or_and, 2 * W * 8, cudaMemcpyDeviceToHost, st));
+    HCG_TRY_CUDA(cudaStreamSynchronize(st));
+
+    int hv = 0;
+    for (int w = int(W) - 1; w >= 0; --w) {
+        const uint64_t vary = oa[w] ^ oa[W + w];
+        if (vary) {
+            hv = 64 * w + 63 - __builtin_clzll(vary);
+            break;
+        }
+    }
+    const int hw = hv >> 6, hb = hv & 63;
+    const uint64_t above = hb == 63 ? 0ull : (~0ull << (hb + 1));
+    const uint64_t below = hb == 63 ? ~0ull : ((2ull << hb) - 1);
+    cv.hv = uint32_t(hv);
+    cv.ws = uint32_t(hw + 1);
+    for (uint32_t w = 0; w < W; ++w)
+        cv.prefix[w] = int(w) > hw ? oa[w] : (int(w) == hw ? (oa[w] & above) : 0ull);
+
+    uint64_t* kb = sc.alloc<uint64_t>(n);
+    uint64_t* ka = sc.alloc<uint64_t>(n);
+    uint32_t* va = sc.alloc<uint32_t>(n);
+    uint32_t* vb = nullptr;
+    uint32_t* counts = reinterpret_cast<uint32_t*>(sc.alloc<uint8_t>(radix_counts_bytes(n)));
+    if (!kb || !ka || !va || !counts) return set_error(HCG_ENOMEM, "sort buffers");
+    HCG_TRY(dev_alloc(&vb, n, &ix->bytes));  // becomes (or swaps into) the resident slots array
+    uint32_t* totals = counts + (radix_counts_bytes(n) / 4 - 256);
+    uint32_t* v = vb;
+    uint32_t* v_alt = va;
+    launch_iota(v, n, st);
+    for (uint32_t w = 0; w <= uint32_t(hw); ++w) {
+        uint64_t vary = oa[w] ^ oa[W + w];
+        if (int(w) == hw) vary &= below;
+        uint32_t dmask = 0;
+        for (int s = 0; s < 8; ++s)
+            if ((vary >> (8 * s)) & 0xFF) dmask |= 1u << s;
+        if (!dmask) continue;
+        launch_gather_word(keys_soa + uint64_t(w) * n, v, kb, n, st);
+        uint64_t* k = kb;
+        uint64_t* k_alt = ka;
+        HCG_TRY(radix_sort_pairs(&k, &v, &k_alt, &v_alt, n, dmask, counts, totals, st));
+        kb = k;
+        ka = k_alt;
+    }
+    HCG_TRY(dev_alloc(&ix->keys[c], size_t(n) * cv.ws, &ix->bytes));
+    launch_pack_suffix(keys_soa, v, n, int(cv.ws), below, ix->keys[c], st);
+    HCG_TRY(check_launch("pack suffix"));
+    if (v == vb) {
+        ix->slots[c] = vb;
+    } else {  // result landed in the scratch buffer: copy into the resident array
+        HCG_TRY_CUDA(cudaMemcpyAsync(vb, v, n * 4, cudaMemcpyDeviceToDevice, st));
+        ix->slots[c] = vb;
+    }
+    cv.keys = ix->keys[c];
+    cv.slots = ix->slots[c];
+    HCG_TRY_CUDA(cudaStreamSynchronize(st));
+    return HCG_OK;
+}
+
+hcg_status check_search_args(const hcg_index* ix, uint32_t k, uint32_t depth) {
+    HCG_TRY(check_index(ix));
+    if (k < 1) return set_error(HCG_EINVAL, "k must be >= 1");
+    if (k > HCG_MAX_K) return set_error(HCG_ECAPACITY, "k exceeds HCG_MAX_K");
+    if (depth < 1) return set_error(HCG_EINVAL, "probe_depth must be >= 1");
+    return HCG_OK;
+}
+
+hcg_status locate(const hcg_index* ix, Scratch& sc, const uint8_t* dq, uint32_t nq, uint32_t depth,
+                  uint32_t* begins, uint64_t* ranks) {
+    LocateArgs a{};
+    a.queries = dq;
+    a.nq = nq;
+    a.pitch = ix->pitch;
+    a.curves = ix->d_curves;
+    a.C = ix->C;
+    a.assign = ix->d_assign;
+    a.lut = ix->d_lut;
+    a.m = int(ix->m);
+    a.kind = int(ix->kind);
+    a.n = ix->n;
+    a.depth = depth;
+    a.out_begin = begins;
+    a.out_rank = ranks;
+    return launch_locate(a, ix->dmax, ix->wsmax, sc.st);
+}
+
+RefineArgs refine_args(const hcg_index* ix, const uint8_t* dq, uint32_t nq, uint32_t depth, uint32_t k,
+                       const uint32_t* begins) {
+    RefineArgs a{};
+    a.queries = dq;
+    a.nq = nq;
+    a.pitch = ix->pitch;
+    a.d_full = ix->d_full;
+    a.rows = ix->rows;
+    a.slots = ix->d_slot_ptrs;
+    a.C = ix->C;
+    a.begins = begins;
+    a.take = uint32_t(std::min<uint64_t>(depth, ix->n));
+    a.k = k;
+    a.id_base = ix->id_base;
+    a.id_stride = ix->id_stride;
+    return a;
+}
+
+hcg_status run_refine(const hcg_index* ix, Scratch& sc, const RefineArgs& a) {
+    size_t need = 0;
+    HCG_TRY(launch_refine(a, nullptr, &need, ix->device, sc.st));
+    void* scratch = need ? sc.alloc<uint8_t>(need) : reinterpret_cast<void*>(1);
+    if (!scratch) return set_error(HCG_ENOMEM, "refine scratch");
+    return launch_refine(a, need ? scratch : reinterpret_cast<void*>(1), &need, ix->device, sc.st);
+}
+
+// Copy a host-side vector to a user buffer that may be host or device memory.
+template <class T>
+hcg_status deliver(T* user, const std::vector<T>& v) {
+    if (v.empty()) return HCG_OK;
+    if (is_device_ptr(user)) HCG_TRY_CUDA(cudaMemcpy(user, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+    else std::memcpy(user, v.data(), v.size() * sizeof(T));
+    return HCG_OK;
+}
+
+}  // namespace
+}  // namespace hcg
+
+using namespace hcg;
+
+extern "C" {
+
+const char* hcg_last_error(void) { return g_err.c_str(); }
+const char* hcg_version(void) { return "hcg 0.1 (sm_100a)"; }
+
+hcg_status hcg_make_lut(float offset, float scale, uint32_t m, uint32_t* lut) {
+    if (!lut) return set_error(HCG_EINVAL, "null lut");
+    if (m < 1 || m > 32) return set_error(HCG_EINVAL, "bits_per_dim out of range [1,32]");
+    for (int b = 0; b < 256; ++b) {
+        const float v = offset + float(b) * scale;
+        if (!std::isfinite(v)) return set_error(HCG_ENONFINITE, "non-finite component");
+        lut[b] = uint32_t(uint64_t(ordinal_of(v)) >> (32 - m));
+    }
+    return HCG_OK;
+}
+
+hcg_status hcg_default_assignment(uint32_t d_full, uint32_t curves, uint32_t* off, uint32_t* assign) {
+    if (!off || !assign) return set_error(HCG_EINVAL, "null output");
+    if (curves < 1 || curves > d_full) return set_error(HCG_EINVAL, "curves must be in [1, d_full]");
+    uint32_t pos = 0;
+    for (uint32_t c = 0; c < curves; ++c) {
+        off[c] = pos;
+        for (uint32_t j = c; j < d_full; j += curves) assign[pos++] = j;
+    }
+    off[curves] = pos;
+    return HCG_OK;
+}
+
+hcg_status hcg_build(const hcg_scheme* s, const uint8_t* rows, uint64_t n, uint64_t id_base, uint64_t id_stride,
+                     int device, void* stream, hcg_index** out) {
+    if (!out) return set_error(HCG_EINVAL, "null output handle");
+    *out = nullptr;
+    HCG_TRY(validate_scheme(s));
+    if (id_stride < 1) return set_error(HCG_EINVAL, "id_stride must be >= 1");
+    if (n >= (1ull << 32)) return set_error(HCG_ECAPACITY, "more than 2^32-1 rows in one index");
+    if (n && !rows) return set_error(HCG_EINVAL, "null rows");
+    HCG_TRY(check_device(device));
+    DeviceGuard g(device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+
+    auto* ix = new hcg_index;
+    ix->device = device;
+    ix->d_full = s->d_full;
+    ix->pitch = round16(s->d_full);
+    ix->C = s->curves;
+    ix->m = s->bits_per_dim;
+    ix->kind = s->curve_kind;
+    ix->dist_scale = s->dist_scale;
+    ix->n = n;
+    ix->id_base = id_base;
+    ix->id_stride = id_stride;
+    ix->off.assign(s->assign_off, s->assign_off + s->curves + 1);
+    ix->assign.assign(s->assign, s->assign + ix->off[s->curves]);
+    std::memcpy(ix->lut, s->cell_lut, sizeof(ix->lut));
+    uint32_t maxd = 1;
+    for (uint32_t c = 0; c < ix->C; ++c) maxd = std::max(maxd, ix->off[c + 1] - ix->off[c]);
+    ix->dmax = pow2_bucket(maxd, 8, 128);
+    ix->curves.resize(ix->C);
+    ix->keys.assign(ix->C, nullptr);
+    ix->slots.assign(ix->C, nullptr);
+
+    auto fail = [&](hcg_status rc) {
+        cudaStreamSynchronize(st);
+        release(ix);
+        return rc;
+    };
+    hcg_status rc;
+    if ((rc = dev_alloc(&ix->rows, size_t(n) * ix->pitch, &ix->bytes)) != HCG_OK) return fail(rc);
+    if ((rc = dev_alloc(&ix->d_lut, 256, &ix->bytes)) != HCG_OK) return fail(rc);
+    if ((rc = dev_alloc(&ix->d_assign, ix->assign.size(), &ix->bytes)) != HCG_OK) return fail(rc);
+    std::vector<uint16_t> asg16(ix->assign.begin(), ix->assign.end());
+    if (n) {
+        if (ix->pitch != ix->d_full && cudaMemsetAsync(ix->rows, 0, size_t(n) * ix->pitch, st) != cudaSuccess)
+            return fail(set_error(HCG_ECUDA, "memset rows"));
+        if (cudaMemcpy2DAsync(ix->rows, ix->pitch, rows, ix->d_full, ix->d_full, n, cudaMemcpyDefault, st) !=
+            cudaSuccess)
+            return fail(set_error(HCG_ECUDA, std::string("copy rows: ") + cudaGetErrorString(cudaGetLastError())));
+    }
+    if (cudaMemcpyAsync(ix->d_lut, ix->lut, sizeof(ix->lut), cudaMemcpyHostToDevice, st) != cudaSuccess ||
+        cudaMemcpyAsync(ix->d_assign, asg16.data(), asg16.size() * 2, cudaMemcpyHostToDevice, st) != cudaSuccess)
+        return fail(set_error(HCG_ECUDA, "copy scheme"));
+    for (uint32_t c = 0; c < ix->C; ++c)
+        if ((rc = build_curve(ix, c, st)) != HCG_OK) return fail(rc);
+    uint32_t maxws = 1;
+    for (auto& cv : ix->curves) maxws = std::max(maxws, cv.ws);
+    ix->wsmax = pow2_bucket(maxws, 1, 16);
+    if ((rc = dev_alloc(&ix->d_curves, ix->C, &ix->bytes)) != HCG_OK) return fail(rc);
+    if ((rc = dev_alloc(&ix->d_slot_ptrs, ix->C, &ix->bytes)) != HCG_OK) return fail(rc);
+    if (cudaMemcpyAsync(ix->d_curves, ix->curves.data(), sizeof(CurveDev) * ix->C, cudaMemcpyHostToDevice, st) !=
+            cudaSuccess ||
+        cudaMemcpyAsync(ix->d_slot_ptrs, ix->slots.data(), sizeof(uint32_t*) * ix->C, cudaMemcpyHostToDevice, st) !=
+            cudaSuccess)
+        return fail(set_error(HCG_ECUDA, "copy curve table"));
+    if (cudaStreamSynchronize(st) != cudaSuccess)
+        return fail(set_error(HCG_ECUDA, std::string("build: ") + cudaGetErrorString(cudaGetLastError())));
+    *out = ix;
+    return HCG_OK;
+}
+
+hcg_status hcg_free(hcg_index* ix) {
+    release(ix);
+    return HCG_OK;
+}
+
+uint64_t hcg_size(const hcg_index* ix) { return ix ? ix->n : 0; }
+uint32_t hcg_curves(const hcg_index* ix) { return ix ? ix->C : 0; }
+uint32_t hcg_key_words(const hcg_index* ix, uint32_t c) { return ix && c < ix->C ? ix->curves[c].w : 0; }
+uint64_t hcg_device_bytes(const hcg_index* ix) { return ix ? ix->bytes : 0; }
+
+static hcg_status search_impl(const hcg_index* ix, const uint8_t* queries, uint32_t nq, uint32_t k, uint32_t depth,
+                              uint64_t* out_ids, uint32_t* out_sqdist, uint32_t* out_len, uint64_t* out_packed,
+                              void* stream) {
+    HCG_TRY(check_search_args(ix, k, depth));
+    if (nq == 0) return HCG_OK;
+    if (!queries) return set_error(HCG_EINVAL, "null queries");
+    const bool packed = out_packed != nullptr;
+    if (!packed && (!out_ids || !out_sqdist || !out_len)) return set_error(HCG_EINVAL, "null output");
+    if (packed && ix->n && ix->id_base + (ix->n - 1) * ix->id_stride >= (1ull << 32))
+        return set_error(HCG_ECAPACITY, "packed results need ids < 2^32");
+    DeviceGuard g(ix->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    Scratch sc(st);
+    OutBuf<uint64_t> oi, op;
+    OutBuf<uint32_t> os, ol;
+    const size_t cnt = size_t(nq) * k;
+    if (packed) {
+        HCG_TRY(stage_out(sc, out_packed, cnt, &op));
+    } else {
+        HCG_TRY(stage_out(sc, out_ids, cnt, &oi));
+        HCG_TRY(stage_out(sc, out_sqdist, cnt, &os));
+        HCG_TRY(stage_out(sc, out_len, nq, &ol));
+    }
+    if (ix->n == 0) {  // empty index: every list is empty
+        if (packed) {
+            HCG_TRY_CUDA(cudaMemsetAsync(op.dev, 0xFF, cnt * 8, st));
+        } else {
+            HCG_TRY_CUDA(cudaMemsetAsync(oi.dev, 0xFF, cnt * 8, st));
+            HCG_TRY_CUDA(cudaMemsetAsync(os.dev, 0xFF, cnt * 4, st));
+            HCG_TRY_CUDA(cudaMemsetAsync(ol.dev, 0, size_t(nq) * 4, st));
+        }
+    } else {
+        const uint8_t* dq = nullptr;
+        HCG_TRY(stage_rows(sc, queries, nq, ix->d_full, ix->pitch, &dq));
+        uint32_t* begins = sc.alloc<uint32_t>(size_t(nq) * ix->C);
+        if (!begins) return set_error(HCG_ENOMEM, "window buffer");
+        HCG_TRY(locate(ix, sc, dq, nq, depth, begins, nullptr));
+        RefineArgs a = refine_args(ix, dq, nq, depth, k, begins);
+        if (packed) {
+            a.mode = kOutPacked;
+            a.out_packed = op.dev;
+        } else {
+            a.mode = kOutIds;
+            a.out_ids = oi.dev;
+            a.out_sqdist = os.dev;
+            a.out_len = ol.dev;
+        }
+        HCG_TRY(run_refine(ix, sc, a));
+    }
+    HCG_TRY(finish_out(sc, oi));
+    HCG_TRY(finish_out(sc, os));
+    HCG_TRY(finish_out(sc, ol));
+    HCG_TRY(finish_out(sc, op));
+    if (oi.host || os.host || ol.host || op.host) HCG_TRY_CUDA(cudaStreamSynchronize(st));
+    return HCG_OK;
+}
+
+hcg_status hcg_search(const hcg_index* ix, const uint8_t* queries, uint32_t nq, uint32_t k, uint32_t depth,
+                      uint64_t* out_ids, uint32_t* out_sqdist, uint32_t* out_len, void* stream) {
+    return search_impl(ix, queries, nq, k, depth, out_ids, out_sqdist, out_len, nullptr, stream);
+}
+
+hcg_status hcg_search_packed(const hcg_index* ix, const uint8_t* queries, uint32_t nq, uint32_t k, uint32_t depth,
+                             uint64_t* out_packed, void* stream) {
+    if (!out_packed) return set_error(HCG_EINVAL, "null output");
+    return search_impl(ix, queries, nq, k, depth, nullptr, nullptr, nullptr, out_packed, stream);
+}
+
+hcg_status hcg_merge_packed(const uint64_t* packed, uint32_t parts, uint32_t nq, uint32_t k, uint64_t* out_ids,
+                            uint32_t* out_sqdist, uint32_t* out_len, int device, void* stream) {
+    if (k < 1) return set_error(HCG_EINVAL, "k must be >= 1");
+    if (k > HCG_MAX_K) return set_error(HCG_ECAPACITY, "k exceeds HCG_MAX_K");
+    if (parts < 1) return set_error(HCG_EINVAL, "parts must be >= 1");
+    if (nq == 0) return HCG_OK;
+    if (!packed || !out_ids || !out_sqdist || !out_len) return set_error(HCG_EINVAL, "null buffer");
+    HCG_TRY(check_device(device));
+    DeviceGuard g(device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    Scratch sc(st);
+    const size_t cnt = size_t(nq) * k;
+    const uint64_t* dp = packed;
+    if (!is_device_ptr(packed)) {
+        uint64_t* d = sc.alloc<uint64_t>(cnt * parts);
+        if (!d) return set_error(HCG_ENOMEM, "merge staging");
+        HCG_TRY_CUDA(cudaMemcpyAsync(d, packed, cnt * parts * 8, cudaMemcpyHostToDevice, st));
+        dp = d;
+    }
+    OutBuf<uint64_t> oi;
+    OutBuf<uint32_t> os, ol;
+    HCG_TRY(stage_out(sc, out_ids, cnt, &oi));
+    HCG_TRY(stage_out(sc, out_sqdist, cnt, &os));
+    HCG_TRY(stage_out(sc, out_len, nq, &ol));
+    HCG_TRY(launch_merge(dp, parts, nq, k, oi.dev, os.dev, ol.dev, st));
+    HCG_TRY(finish_out(sc, oi));
+    HCG_TRY(finish_out(sc, os));
+    HCG_TRY(finish_out(sc, ol));
+    if (oi.host || os.host || ol.host) HCG_TRY_CUDA(cudaStreamSynchronize(st));
+    return HCG_OK;
+}
+
+hcg_status hcg_keys(const hcg_index* ix, const uint8_t* rows, uint64_t n, uint32_t curve, uint64_t* out_words,
+                    void* stream) {
+    HCG_TRY(check_index(ix));
+    if (curve >= ix->C) return set_error(HCG_EINVAL, "curve out of range");
+    if (n == 0) return HCG_OK;
+    if (!rows || !out_words) return set_error(HCG_EINVAL, "null buffer");
+    DeviceGuard g(ix->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    Scratch sc(st);
+    const uint8_t* dr = nullptr;
+    HCG_TRY(stage_rows(sc, rows, n, ix->d_full, ix->pitch, &dr));
+    const uint32_t W = ix->curves[curve].w;
+    uint64_t* soa = sc.alloc<uint64_t>(size_t(W) * n);
+    unsigned long long* oa = sc.alloc<unsigned long long>(2 * W);
+    if (!soa || !oa) return set_error(HCG_ENOMEM, "key buffers");
+    const uint32_t d = ix->off[curve + 1] - ix->off[curve];
+    HCG_TRY(keygen_rows(dr, n, ix->pitch, ix->d_assign + ix->off[curve], int(d), int(ix->m), int(ix->kind),
+                        ix->d_lut, soa, int(W), oa, ix->dmax, st));
+    std::vector<uint64_t> h(size_t(W) * n), t(size_t(W) * n);
+    HCG_TRY_CUDA(cudaMemcpyAsync(h.data(), soa, h.size() * 8, cudaMemcpyDeviceToHost, st));
+    HCG_TRY_CUDA(cudaStreamSynchronize(st));
+    for (uint64_t i = 0; i < n; ++i)
+        for (uint32_t w = 0; w < W; ++w) t[i * W + w] = h[uint64_t(w) * n + i];
+    return deliver(out_words, t);
+}
+
+hcg_status hcg_sorted(const hcg_index* ix, uint32_t curve, uint64_t* out_ids, uint64_t* out_words, void* stream) {
+    HCG_TRY(check_index(ix));
+    if (curve >= ix->C) return set_error(HCG_EINVAL, "curve out of range");
+    if (ix->n == 0) return HCG_OK;
+    DeviceGuard g(ix->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    Scratch sc(st);
+    const uint64_t n = ix->n;
+    const CurveDev& cv = ix->curves[curve];
+    if (out_ids) {
+        std::vector<uint32_t> s(n);
+        HCG_TRY_CUDA(cudaMemcpyAsync(s.data(), ix->slots[curve], n * 4, cudaMemcpyDeviceToHost, st));
+        HCG_TRY_CUDA(cudaStreamSynchronize(st));
+        std::vector<uint64_t> ids(n);
+        for (uint64_t i = 0; i < n; ++i) ids[i] = ix->id_base + uint64_t(s[i]) * ix->id_stride;
+        HCG_TRY(deliver(out_ids, ids));
+    }
+    if (out_words) {
+        uint64_t* full = sc.alloc<uint64_t>(size_t(n) * cv.w);
+        if (!full) return set_error(HCG_ENOMEM, "key buffer");
+        launch_expand_keys(ix->keys[curve], n, int(cv.ws), int(cv.w), cv, full, st);
+        HCG_TRY(check_launch("expand keys"));
+        std::vector<uint64_t> h(size_t(n) * cv.w);
+        HCG_TRY_CUDA(cudaMemcpyAsync(h.data(), full, h.size() * 8, cudaMemcpyDeviceToHost, st));
+        HCG_TRY_CUDA(cudaStreamSynchronize(st));
+        HCG_TRY(deliver(out_words, h));
+    }
+    return HCG_OK;
+}
+
+hcg_status hcg_windows(const hcg_index* ix, const uint8_t* queries, uint32_t nq, uint32_t depth, uint64_t* out_rank,
+                       uint64_t* out_begin, uint64_t* out_end, void* stream) {
+    HCG_TRY(check_search_args(ix, 1, depth));
+    if (nq == 0) return HCG_OK;
+    if (!queries || !out_rank || !out_begin || !out_end) return set_error(HCG_EINVAL, "null buffer");
+    const size_t cnt = size_t(nq) * ix->C;
+    std::vector<uint64_t> r(cnt, 0), b(cnt, 0), e(cnt, 0);
+    if (ix->n) {
+        DeviceGuard g(ix->device);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        Scratch sc(st);
+        const uint8_t* dq = nullptr;
+        HCG_TRY(stage_rows(sc, queries, nq, ix->d_full, ix->pitch, &dq));
+        uint32_t* begins = sc.alloc<uint32_t>(cnt);
+        uint64_t* ranks = sc.alloc<uint64_t>(cnt);
+        if (!begins || !ranks) return set_error(HCG_ENOMEM, "window buffers");
+        HCG_TRY(locate(ix, sc, dq, nq, depth, begins, ranks));
+        std::vector<uint32_t> hb(cnt);
+        HCG_TRY_CUDA(cudaMemcpyAsync(hb.data(), begins, cnt * 4, cudaMemcpyDeviceToHost, st));
+        HCG_TRY_CUDA(cudaMemcpyAsync(r.data(), ranks, cnt * 8, cudaMemcpyDeviceToHost, st));
+        HCG_TRY_CUDA(cudaStreamSynchronize(st));
+        const uint64_t take = std::min<uint64_t>(depth, ix->n);
+        for (size_t i = 0; i < cnt; ++i) {
+            b[i] = hb[i];
+            e[i] = hb[i] + take;
+        }
+    }
+    HCG_TRY(deliver(out_rank, r));
+    HCG_TRY(deliver(out_begin, b));
+    return deliver(out_end, e);
+}
+
+hcg_status hcg_candidates(const hcg_index* ix, const uint8_t* queries, uint32_t nq, uint32_t depth, uint64_t* out_ids,
+                          uint32_t cap, uint32_t* out_count, void* stream) {
+    HCG_TRY(check_search_args(ix, 1, depth));
+    if (nq == 0) return HCG_OK;
+    if (!queries || !out_ids || !out_count) return set_error(HCG_EINVAL, "null buffer");
+    DeviceGuard g(ix->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    Scratch sc(st);
+    OutBuf<uint64_t> oi;
+    OutBuf<uint32_t> oc;
+    HCG_TRY(stage_out(sc, out_ids, size_t(nq) * cap, &oi));
+    HCG_TRY(stage_out(sc, out_count, nq, &oc));
+    if (ix->n == 0) {
+        HCG_TRY_CUDA(cudaMemsetAsync(oc.dev, 0, size_t(nq) * 4, st));
+    } else {
+        const uint8_t* dq = nullptr;
+        HCG_TRY(stage_rows(sc, queries, nq, ix->d_full, ix->pitch, &dq));
+        uint32_t* begins = sc.alloc<uint32_t>(size_t(nq) * ix->C);
+        if (!begins) return set_error(HCG_ENOMEM, "window buffer");
+        HCG_TRY(locate(ix, sc, dq, nq, depth, begins, nullptr));
+        RefineArgs a = refine_args(ix, dq, nq, depth, 1, begins);
+        a.mode = kOutCandidates;
+        a.out_ids = oi.dev;
+        a.out_len = oc.dev;
+        a.cap = cap;
+        HCG_TRY(run_refine(ix, sc, a));
+    }
+    HCG_TRY(finish_out(sc, oi));
+    HCG_TRY(finish_out(sc, oc));
+    HCG_TRY_CUDA(cudaStreamSynchronize(st));
+    std::vector<uint32_t> counts(nq);
+    if (oc.host) std::memcpy(counts.data(), out_count, nq * 4);
+    else HCG_TRY_CUDA(cudaMemcpy(counts.data(), out_count, nq * 4, cudaMemcpyDeviceToHost));
+    for (uint32_t c : counts)
+        if (c > cap) return set_error(HCG_ECAPACITY, "candidate set larger than cap");
+    return HCG_OK;
+}
+
+hcg_status hcg_brute_force(const hcg_index* ix, const uint8_t* queries, uint32_t nq, uint32_t k, uint64_t* out_ids,
+                           uint32_t* out_sqdist, uint32_t* out_len, void* stream) {
+    HCG_TRY(check_search_args(ix, k, 1));
+    if (nq == 0) return HCG_OK;
+    if (!queries || !out_ids || !out_sqdist || !out_len) return set_error(HCG_EINVAL, "null buffer");
+    if (ix->n && ix->id_base + (ix->n - 1) * ix->id_stride >= (1ull << 32))
+        return set_error(HCG_ECAPACITY, "brute force needs ids < 2^32");
+    DeviceGuard g(ix->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    Scratch sc(st);
+    OutBuf<uint64_t> oi;
+    OutBuf<uint32_t> os, ol;
+    const size_t cnt = size_t(nq) * k;
+    HCG_TRY(stage_out(sc, out_ids, cnt, &oi));
+    HCG_TRY(stage_out(sc, out_sqdist, cnt, &os));
+    HCG_TRY(stage_out(sc, out_len, nq, &ol));
+    if (ix->n == 0) {
+        HCG_TRY_CUDA(cudaMemsetAsync(oi.dev, 0xFF, cnt * 8, st));
+        HCG_TRY_CUDA(cudaMemsetAsync(os.dev, 0xFF, cnt * 4, st));
+        HCG_TRY_CUDA(cudaMemsetAsync(ol.dev, 0, size_t(nq) * 4, st));
+    } else {
+        const uint8_t* dq = nullptr;
+        HCG_TRY(stage_rows(sc, queries, nq, ix->d_full, ix->pitch, &dq));
+        BruteArgs a{ix->rows, ix->n, ix->pitch, dq, nq, k, ix->id_base, ix->id_stride};
+        uint64_t* part = sc.alloc<uint64_t>(brute_scratch_bytes(a) / 8);
+        if (!part) return set_error(HCG_ENOMEM, "brute-force scratch");
+        HCG_TRY(launch_brute(a, part, oi.dev, os.dev, ol.dev, st));
+    }
+    HCG_TRY(finish_out(sc, oi));
+    HCG_TRY(finish_out(sc, os));
+    HCG_TRY(finish_out(sc, ol));
+    if (oi.host || os.host || ol.host) HCG_TRY_CUDA(cudaStreamSynchronize(st));
+    return HCG_OK;
+}
+
+hcg_status hcg_gen_rows(uint64_t first, uint64_t stride, uint64_t count, uint8_t* out_dev, int device, void* stream) {
+    if (count && !is_device_ptr(out_dev)) return set_error(HCG_EINVAL, "hcg_gen_rows needs a device buffer");
+    HCG_TRY(check_device(device));
+    DeviceGuard g(device);
+    return gen_rows(first, stride, count, out_dev, static_cast<cudaStream_t>(stream));
+}
+
+hcg_status hcg_gen_queries(uint64_t first, uint64_t count, uint64_t n_db, uint8_t* out_dev, int device, void* stream) {
+    if (count && !is_device_ptr(out_dev)) return set_error(HCG_EINVAL, "hcg_gen_queries needs a device buffer");
+    HCG_TRY(check_device(device));
+    DeviceGuard g(device);
+    return gen_queries(first, count, n_db, out_dev, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

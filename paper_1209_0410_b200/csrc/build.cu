@@ -1,0 +1,348 @@
+// build.cu -- index build on the B200: K1 key generation and K2 stable LSD
+// radix sort of each curve's (key, slot) list.
+//
+// Reference behaviour (Alg. 1; multicurves.hpp:47-51,77):
+// every vector is projected onto each curve's subspace, quantized, turned into
+// an extended key, and each curve keeps its (key, id) entries sorted by key
+// then id.  Here the input is already in slot (= id) order, so a STABLE sort
+// by key alone reproduces the (key, id) order exactly.
+//
+// HBM layout produced per curve c:
+//   keys[c]  : n x ws u64, suffix of the key below the curve's common prefix
+//   slots[c] : n u32, row index of each sorted entry
+#include <algorithm>
+#include <vector>
+
+#include "hcg_internal.cuh"
+#include "hcg_host.hpp"
+
+namespace hcg {
+
+// ------------------------------------------------------------------ K1 ----
+template <int DMAX>
+struct KeyWords {
+    static constexpr int value = DMAX / 2 > kMaxKeyWords ? kMaxKeyWords : (DMAX / 2 < 1 ? 1 : DMAX / 2);
+};
+
+// One thread per row: key of curve c (full width, SoA words) plus an OR/AND
+// reduction over all keys that later yields the common prefix.
+template <int DMAX>
+__global__ void __launch_bounds__(256) k_keygen(const uint8_t* __restrict__ rows, uint64_t n,
+                                                uint32_t pitch, const uint16_t* __restrict__ assign_c,
+                                                int d, int m, int kind, const uint32_t* __restrict__ lut_g,
+                                                uint64_t* __restrict__ keys_soa, int W,
+                                                unsigned long long* __restrict__ or_and) {
+    constexpr int WMAX = KeyWords<DMAX>::value;
+    __shared__ uint32_t lut[256];
+    __shared__ uint16_t asg[DMAX];
+    __shared__ uint64_t red_or[8][WMAX];
+    __shared__ uint64_t red_and[8][WMAX];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    lut[tid] = lut_g[tid];
+    if (tid < DMAX) asg[tid] = tid < d ? assign_c[tid] : 0;
+    __syncthreads();
+
+    const uint64_t i = uint64_t(blockIdx.x) * 256 + tid;
+    const bool valid = i < n;
+    uint64_t key[WMAX];
+    if (valid) {
+        uint32_t x[DMAX];
+        const uint8_t* row = rows + i * pitch;
+#pragma unroll
+        for (int s = 0; s < DMAX; ++s) x[s] = s < d ? lut[__ldg(row + asg[s])] : 0u;
+        make_key<DMAX, WMAX>(x, d, m, kind, key);
+#pragma unroll
+        for (int w = 0; w < WMAX; ++w)
+            if (w < W) keys_soa[uint64_t(w) * n + i] = key[w];
+    }
+#pragma unroll
+    for (int w = 0; w < WMAX; ++w) {
+        uint64_t o = valid ? key[w] : 0ull;
+        uint64_t a = valid ? key[w] : ~0ull;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            o |= __shfl_xor_sync(kFull, o, off);
+            a &= __shfl_xor_sync(kFull, a, off);
+        }
+        if (lane == 0) {
+            red_or[warp][w] = o;
+            red_and[warp][w] = a;
+        }
+    }
+    __syncthreads();
+    if (tid < W && tid < WMAX) {
+        uint64_t o = 0, a = ~0ull;
+        for (int k = 0; k < 8; ++k) {
+            o |= red_or[k][tid];
+            a &= red_and[k][tid];
+        }
+        atomicOr(or_and + tid, (unsigned long long)o);
+        atomicAnd(or_and + W + tid, (unsigned long long)a);
+    }
+}
+
+// ------------------------------------------------------------------ K2 ----
+constexpr int kSortThreads = 256;
+constexpr int kSortIpt = 8;
+constexpr int kSortTile = kSortThreads * kSortIpt;  // 2048
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// Exclusive scan of one value per thread over a 256-thread block.
+__device__ __forceinline__ uint32_t block_excl_scan256(uint32_t v, uint32_t* wsum) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t inc = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t t = __shfl_up_sync(kFull, inc, off);
+        if (lane >= off) inc += t;
+    }
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t s = lane < 8 ? wsum[lane] : 0;
+#pragma unroll
+        for (int off = 1; off < 8; off <<= 1) {
+            const uint32_t t = __shfl_up_sync(kFull, s, off);
+            if (lane >= off) s += t;
+        }
+        if (lane < 8) wsum[lane] = s;  // inclusive warp totals
+    }
+    __syncthreads();
+    const uint32_t before = warp ? wsum[warp - 1] : 0;
+    const uint32_t r = before + inc - v;
+    __syncthreads();
+    return r;
+}
+
+__global__ void __launch_bounds__(kSortThreads) k_upsweep(const uint64_t* __restrict__ keys, uint64_t n,
+                                                          int shift, uint32_t* __restrict__ counts,
+                                                          uint32_t tiles) {
+    __shared__ uint32_t h[8][256];
+    const int tid = threadIdx.x, warp = tid >> 5;
+    for (int i = tid; i < 8 * 256; i += kSortThreads) (&h[0][0])[i] = 0;
+    __syncthreads();
+    const uint64_t base = uint64_t(blockIdx.x) * kSortTile;
+#pragma unroll
+    for (int t = 0; t < kSortIpt; ++t) {
+        const uint64_t idx = base + uint64_t(t) * kSortThreads + tid;
+        if (idx < n) atomicAdd(&h[warp][(keys[idx] >> shift) & 255], 1u);
+    }
+    __syncthreads();
+    uint32_t s = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) s += h[w][tid];
+    counts[uint64_t(tid) * tiles + blockIdx.x] = s;
+}
+
+// One block per digit: exclusive scan of that digit's per-tile counts.
+__global__ void __launch_bounds__(1024) k_scan_rows(uint32_t* __restrict__ counts, uint32_t tiles,
+                                                    uint32_t* __restrict__ totals) {
+    __shared__ uint32_t wsum[32];
+    uint32_t* row = counts + uint64_t(blockIdx.x) * tiles;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    uint32_t carry = 0;
+    for (uint32_t base = 0; base < tiles; base += 1024) {
+        const uint32_t v = base + tid < tiles ? row[base + tid] : 0;
+        uint32_t inc = v;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const uint32_t t = __shfl_up_sync(kFull, inc, off);
+            if (lane >= off) inc += t;
+        }
+        if (lane == 31) wsum[warp] = inc;
+        __syncthreads();
+        if (warp == 0) {
+            uint32_t s = wsum[lane];
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const uint32_t t = __shfl_up_sync(kFull, s, off);
+                if (lane >= off) s += t;
+            }
+            wsum[lane] = s;
+        }
+        __syncthreads();
+        const uint32_t excl = (warp ? wsum[warp - 1] : 0) + inc - v;
+        if (base + tid < tiles) row[base + tid] = carry + excl;
+        carry += wsum[31];
+        __syncthreads();
+    }
+    if (tid == 0) totals[blockIdx.x] = carry;
+}
+
+// Stable scatter of one tile.  Warp w owns elements [w*256, w*256+256) of the
+// tile and walks them in 8 coalesced rounds, so (warp, round, lane) is the
+// original order; ranks come from per-warp digit counters and match_any.
+// The tile is re-ordered in shared memory first so the global writes leave in
+// per-digit runs.
+__global__ void __launch_bounds__(kSortThreads) k_downsweep(
+    const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin, uint64_t* __restrict__ kout,
+    uint32_t* __restrict__ vout, uint64_t n, int shift, const uint32_t* __restrict__ counts,
+    const uint32_t* __restrict__ totals, uint32_t tiles) {
+    __shared__ uint32_t whist[8][256];
+    __shared__ uint32_t tile_off[256];
+    __shared__ uint32_t gbase[256];
+    __shared__ uint32_t wsum[8];
+    __shared__ uint64_t skeys[kSortTile];
+    __shared__ uint32_t svals[kSortTile];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int i = tid; i < 8 * 256; i += kSortThreads) (&whist[0][0])[i] = 0;
+    const uint32_t gex = block_excl_scan256(totals[tid], wsum);
+    gbase[tid] = gex + counts[uint64_t(tid) * tiles + blockIdx.x];
+
+    const uint64_t base = uint64_t(blockIdx.x) * kSortTile;
+    const uint64_t wbase = base + uint64_t(warp) * (32 * kSortIpt);
+    uint64_t k[kSortIpt];
+    uint32_t v[kSortIpt], dg[kSortIpt], lr[kSortIpt];
+#pragma unroll
+    for (int t = 0; t < kSortIpt; ++t) {
+        const uint64_t idx = wbase + uint64_t(t) * 32 + lane;
+        const bool ok = idx < n;
+        k[t] = ok ? kin[idx] : 0ull;
+        v[t] = ok ? vin[idx] : 0u;
+        dg[t] = ok ? uint32_t((k[t] >> shift) & 255) : 256u;
+    }
+    const unsigned lt = lanemask_lt();
+#pragma unroll
+    for (int t = 0; t < kSortIpt; ++t) {
+        const unsigned peers = __match_any_sync(kFull, dg[t]);
+        const uint32_t rank = __popc(peers & lt);
+        const uint32_t b = dg[t] < 256 ? whist[warp][dg[t]] : 0u;
+        __syncwarp();
+        if (dg[t] < 256 && rank == 0) whist[warp][dg[t]] = b + __popc(peers);
+        __syncwarp();
+        lr[t] = b + rank;
+    }
+    __syncthreads();
+    uint32_t run = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+        const uint32_t c = whist[w][tid];
+        whist[w][tid] = run;
+        run += c;
+    }
+    tile_off[tid] = block_excl_scan256(run, wsum);
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < kSortIpt; ++t) {
+        if (dg[t] < 256) {
+            const uint32_t li = tile_off[dg[t]] + whist[warp][dg[t]] + lr[t];
+            skeys[li] = k[t];
+            svals[li] = v[t];
+        }
+    }
+    __syncthreads();
+    const uint32_t tile_n = uint32_t(min(uint64_t(kSortTile), n - base));
+    for (uint32_t i = tid; i < tile_n; i += kSortThreads) {
+        const uint64_t key = skeys[i];
+        const uint32_t d = uint32_t((key >> shift) & 255);
+        const uint64_t g = uint64_t(gbase[d]) + (i - tile_off[d]);
+        kout[g] = key;
+        vout[g] = svals[i];
+    }
+}
+
+__global__ void k_iota(uint32_t* v, uint64_t n) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) v[i] = uint32_t(i);
+}
+
+__global__ void k_gather_word(const uint64_t* __restrict__ src, const uint32_t* __restrict__ perm,
+                              uint64_t* __restrict__ dst, uint64_t n) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = src[perm[i]];
+}
+
+// Sorted suffix keys, AoS (ws words per entry), bits above hv cleared.
+__global__ void k_pack_suffix(const uint64_t* __restrict__ keys_soa, const uint32_t* __restrict__ perm,
+                              uint64_t n, int ws, uint64_t top_mask, uint64_t* __restrict__ out) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t s = perm[i];
+    for (int w = 0; w < ws; ++w) {
+        uint64_t v = keys_soa[uint64_t(w) * n + s];
+        if (w == ws - 1) v &= top_mask;
+        out[i * ws + w] = v;
+    }
+}
+
+// Re-expand sorted suffix keys to full-width keys (parity tap).
+__global__ void k_expand_keys(const uint64_t* __restrict__ suffix, uint64_t n, int ws, int w_full,
+                              CurveDev cv, uint64_t* __restrict__ out) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    for (int w = 0; w < w_full; ++w) out[i * w_full + w] = cv.prefix[w] | (w < ws ? suffix[i * ws + w] : 0ull);
+}
+
+// ---------------------------------------------------------------- host ----
+namespace {
+inline unsigned blocks_for(uint64_t n, unsigned t) { return unsigned((n + t - 1) / t); }
+
+template <int DMAX>
+void launch_keygen(const uint8_t* rows, uint64_t n, uint32_t pitch, const uint16_t* assign_c, int d, int m,
+                   int kind, const uint32_t* lut, uint64_t* keys_soa, int W, unsigned long long* or_and,
+                   cudaStream_t st) {
+    k_keygen<DMAX><<<blocks_for(n, 256), 256, 0, st>>>(rows, n, pitch, assign_c, d, m, kind, lut, keys_soa, W,
+                                                      or_and);
+}
+}  // namespace
+
+hcg_status keygen_rows(const uint8_t* rows, uint64_t n, uint32_t pitch, const uint16_t* assign_c, int d, int m,
+                       int kind, const uint32_t* lut, uint64_t* keys_soa, int W, unsigned long long* or_and,
+                       int dmax, cudaStream_t st) {
+    if (n == 0) return HCG_OK;
+    switch (dmax) {
+        case 8: launch_keygen<8>(rows, n, pitch, assign_c, d, m, kind, lut, keys_soa, W, or_and, st); break;
+        case 16: launch_keygen<16>(rows, n, pitch, assign_c, d, m, kind, lut, keys_soa, W, or_and, st); break;
+        case 32: launch_keygen<32>(rows, n, pitch, assign_c, d, m, kind, lut, keys_soa, W, or_and, st); break;
+        case 64: launch_keygen<64>(rows, n, pitch, assign_c, d, m, kind, lut, keys_soa, W, or_and, st); break;
+        case 128: launch_keygen<128>(rows, n, pitch, assign_c, d, m, kind, lut, keys_soa, W, or_and, st); break;
+        default: return set_error(HCG_EINVAL, "unsupported curve dimension bucket");
+    }
+    return check_launch("k_keygen");
+}
+
+// Stable LSD radix sort of (key, val) pairs over the 8-bit digits selected by
+// digit_mask (bit s -> digit at shift 8s).  Double-buffered; on return *k/*v
+// hold the result.
+hcg_status radix_sort_pairs(uint64_t** k, uint32_t** v, uint64_t** k_alt, uint32_t** v_alt, uint64_t n,
+                            uint32_t digit_mask, uint32_t* counts, uint32_t* totals, cudaStream_t st) {
+    if (n == 0 || digit_mask == 0) return HCG_OK;
+    const uint32_t tiles = uint32_t((n + kSortTile - 1) / kSortTile);
+    for (int s = 0; s < 8; ++s) {
+        if (!((digit_mask >> s) & 1)) continue;
+        const int shift = 8 * s;
+        k_upsweep<<<tiles, kSortThreads, 0, st>>>(*k, n, shift, counts, tiles);
+        k_scan_rows<<<256, 1024, 0, st>>>(counts, tiles, totals);
+        k_downsweep<<<tiles, kSortThreads, 0, st>>>(*k, *v, *k_alt, *v_alt, n, shift, counts, totals, tiles);
+        std::swap(*k, *k_alt);
+        std::swap(*v, *v_alt);
+    }
+    return check_launch("radix pass");
+}
+
+size_t radix_counts_bytes(uint64_t n) {
+    const uint64_t tiles = (n + kSortTile - 1) / kSortTile;
+    return size_t(tiles) * 256 * 4 + 256 * 4;
+}
+
+void launch_iota(uint32_t* v, uint64_t n, cudaStream_t st) {
+    if (n) k_iota<<<blocks_for(n, 256), 256, 0, st>>>(v, n);
+}
+void launch_gather_word(const uint64_t* src, const uint32_t* perm, uint64_t* dst, uint64_t n, cudaStream_t st) {
+    if (n) k_gather_word<<<blocks_for(n, 256), 256, 0, st>>>(src, perm, dst, n);
+}
+void launch_pack_suffix(const uint64_t* keys_soa, const uint32_t* perm, uint64_t n, int ws, uint64_t top_mask,
+                        uint64_t* out, cudaStream_t st) {
+    if (n) k_pack_suffix<<<blocks_for(n, 256), 256, 0, st>>>(keys_soa, perm, n, ws, top_mask, out);
+}
+void launch_expand_keys(const uint64_t* suffix, uint64_t n, int ws, int w_full, const CurveDev& cv, uint64_t* out,
+                        cudaStream_t st) {
+    if (n) k_expand_keys<<<blocks_for(n, 256), 256, 0, st>>>(suffix, n, ws, w_full, cv, out);
+}
+
+}  // namespace hcg

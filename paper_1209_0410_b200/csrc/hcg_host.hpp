@@ -1,0 +1,94 @@
+// hcg_host.hpp -- host-side declarations shared by the .cu translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/hcg.h"
+
+namespace hcg {
+
+struct CurveDev;
+
+hcg_status set_error(hcg_status code, const std::string& msg);
+hcg_status check_launch(const char* what);
+
+// build.cu
+hcg_status keygen_rows(const uint8_t* rows, uint64_t n, uint32_t pitch, const uint16_t* assign_c, int d, int m,
+                       int kind, const uint32_t* lut, uint64_t* keys_soa, int W, unsigned long long* or_and,
+                       int dmax, cudaStream_t st);
+hcg_status radix_sort_pairs(uint64_t** k, uint32_t** v, uint64_t** k_alt, uint32_t** v_alt, uint64_t n,
+                            uint32_t digit_mask, uint32_t* counts, uint32_t* totals, cudaStream_t st);
+size_t radix_counts_bytes(uint64_t n);
+void launch_iota(uint32_t* v, uint64_t n, cudaStream_t st);
+void launch_gather_word(const uint64_t* src, const uint32_t* perm, uint64_t* dst, uint64_t n, cudaStream_t st);
+void launch_pack_suffix(const uint64_t* keys_soa, const uint32_t* perm, uint64_t n, int ws, uint64_t top_mask,
+                        uint64_t* out, cudaStream_t st);
+void launch_expand_keys(const uint64_t* suffix, uint64_t n, int ws, int w_full, const CurveDev& cv, uint64_t* out,
+                        cudaStream_t st);
+
+// search.cu
+struct LocateArgs {
+    const uint8_t* queries;
+    uint32_t nq;
+    uint32_t pitch;
+    const CurveDev* curves;  // device array
+    uint32_t C;
+    const uint16_t* assign;  // device, whole table
+    const uint32_t* lut;     // device, 256
+    int m, kind;
+    uint64_t n;
+    uint32_t depth;
+    uint32_t* out_begin;  // nq x C
+    uint64_t* out_rank;   // nq x C or null
+};
+hcg_status launch_locate(const LocateArgs& a, int dmax, int wsmax, cudaStream_t st);
+
+enum OutMode : int { kOutIds = 0, kOutPacked = 1, kOutCandidates = 2 };
+struct RefineArgs {
+    const uint8_t* queries;
+    uint32_t nq;
+    uint32_t pitch;
+    uint32_t d_full;
+    const uint8_t* rows;
+    const uint32_t* const* slots;  // device array of C pointers
+    uint32_t C;
+    const uint32_t* begins;  // nq x C
+    uint32_t take;
+    uint32_t k;
+    uint64_t id_base, id_stride;
+    int mode;
+    uint64_t* out_ids;     // kOutIds: nq x k ids; kOutCandidates: nq x cap ids
+    uint32_t* out_sqdist;  // kOutIds
+    uint32_t* out_len;     // kOutIds: len; kOutCandidates: count
+    uint64_t* out_packed;  // kOutPacked
+    uint32_t cap;          // kOutCandidates
+};
+// Scratch bytes the refine launch needs (global hash tables when the table
+// does not fit in shared memory); query with scratch == nullptr first.
+hcg_status launch_refine(const RefineArgs& a, void* scratch, size_t* scratch_bytes, int device,
+                         cudaStream_t st);
+
+hcg_status launch_merge(const uint64_t* packed, uint32_t parts, uint32_t nq, uint32_t k, uint64_t* out_ids,
+                        uint32_t* out_sqdist, uint32_t* out_len, cudaStream_t st);
+
+struct BruteArgs {
+    const uint8_t* rows;
+    uint64_t n;
+    uint32_t pitch;
+    const uint8_t* queries;
+    uint32_t nq;
+    uint32_t k;
+    uint64_t id_base, id_stride;
+};
+size_t brute_scratch_bytes(const BruteArgs& a);
+hcg_status launch_brute(const BruteArgs& a, uint64_t* scratch, uint64_t* out_ids, uint32_t* out_sqdist,
+                        uint32_t* out_len, cudaStream_t st);
+
+// datagen.cu
+hcg_status gen_rows(uint64_t first, uint64_t stride, uint64_t count, uint8_t* out, cudaStream_t st);
+hcg_status gen_queries(uint64_t first, uint64_t count, uint64_t n_db, uint8_t* out, cudaStream_t st);
+
+}  // namespace hcg

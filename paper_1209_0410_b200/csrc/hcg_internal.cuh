@@ -1,0 +1,184 @@
+// hcg_internal.cuh -- shared device helpers and host/device structs of the
+// B200 Hypercurves hot path (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/hcg.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "this library targets sm_100a (B200) only"
+#endif
+
+namespace hcg {
+
+constexpr int kMaxKeyWords = HCG_MAX_KEY_BITS / 64;  // 16
+constexpr uint32_t kEmpty = 0xFFFFFFFFu;
+constexpr uint64_t kNone = ~0ull;
+constexpr unsigned kFull = 0xFFFFFFFFu;
+
+// Per-curve description used by the locate kernel.  The sorted subindex c is
+// stored as suffix keys: every key of the curve shares the bits above `hv`
+// (the highest bit that varies over the database), so only bits [0, hv] are
+// kept, right-aligned in `ws` words (least significant word first).
+struct CurveDev {
+    const uint64_t* keys;   // n x ws suffix words, sorted
+    const uint32_t* slots;  // n, slot (row index) of each sorted entry
+    uint64_t prefix[kMaxKeyWords];  // full-width common key with bits <= hv cleared
+    uint32_t hv;    // highest varying bit
+    uint32_t ws;    // suffix words
+    uint32_t w;     // full key words = ceil(dims * m / 64)
+    uint32_t dims;  // projected dimensions feeding this curve
+    uint32_t off;   // offset of this curve's slots in the assignment table
+};
+
+// ---------------------------------------------------------------- keys ----
+// Skilling's axes->transpose on m-bit coordinates held in registers; the
+// coordinate count d is runtime (<= DMAX).  Branch-free form of the
+// per-bit-plane rotation (reference: proj/src/curve.cpp:100-123).
+template <int DMAX>
+__device__ __forceinline__ void hilbert_transpose(uint32_t (&x)[DMAX], int d, int m) {
+    for (uint32_t q = 1u << (m - 1); q > 1; q >>= 1) {
+        const uint32_t low = q - 1;
+#pragma unroll
+        for (int i = 0; i < DMAX; ++i) {
+            if (i < d) {
+                const bool set = (x[i] & q) != 0;
+                const uint32_t t = (x[0] ^ x[i]) & low;
+                const uint32_t x0 = x[0] ^ (set ? low : t);
+                if (i != 0) x[i] ^= set ? 0u : t;
+                x[0] = x0;
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 1; i < DMAX; ++i)
+        if (i < d) x[i] ^= x[i - 1];
+    uint32_t last = 0;
+#pragma unroll
+    for (int i = 0; i < DMAX; ++i)
+        if (i == d - 1) last = x[i];
+    uint32_t fix = 0;
+    for (uint32_t q = 1u << (m - 1); q > 1; q >>= 1)
+        if (last & q) fix ^= q - 1;
+#pragma unroll
+    for (int i = 0; i < DMAX; ++i)
+        if (i < d) x[i] ^= fix;
+}
+
+// key <<= s (1 <= s <= 128) on a WMAX-word little-endian integer.
+template <int WMAX>
+__device__ __forceinline__ void key_shl(uint64_t (&k)[WMAX], int s) {
+    const int ws = s >> 6, bs = s & 63;
+#pragma unroll
+    for (int w = WMAX - 1; w >= 0; --w) {
+        const uint64_t a0 = k[w];
+        const uint64_t a1 = w >= 1 ? k[w - 1] : 0ull;
+        const uint64_t a2 = w >= 2 ? k[w - 2] : 0ull;
+        const uint64_t a3 = w >= 3 ? k[w - 3] : 0ull;
+        const uint64_t hi = ws == 0 ? a0 : (ws == 1 ? a1 : a2);
+        const uint64_t lo = ws == 0 ? a1 : (ws == 1 ? a2 : a3);
+        k[w] = bs ? ((hi << bs) | (lo >> (64 - bs))) : hi;
+    }
+}
+
+// Curve key of one projected point: plane j (MSB first) of coordinate i lands
+// at key bit width-1-(j*d+i) (reference: proj/src/curve.cpp:62-75).
+// cells: the m-bit quantized coordinates (LUT output).
+template <int DMAX, int WMAX>
+__device__ __forceinline__ void make_key(uint32_t (&x)[DMAX], int d, int m, int kind,
+                                         uint64_t (&key)[WMAX]) {
+    if (kind == HCG_HILBERT && d > 1) hilbert_transpose<DMAX>(x, d, m);
+#pragma unroll
+    for (int w = 0; w < WMAX; ++w) key[w] = 0;
+    for (int j = 0; j < m; ++j) {
+        const int sh = m - 1 - j;
+        uint64_t c0 = 0, c1 = 0;
+#pragma unroll
+        for (int i = 0; i < DMAX; ++i) {
+            if (i < d) {
+                const uint64_t bit = (x[i] >> sh) & 1u;
+                const int p = d - 1 - i;
+                if (DMAX > 64 && p >= 64) c1 |= bit << (p - 64);
+                else c0 |= bit << p;
+            }
+        }
+        if (j > 0) key_shl<WMAX>(key, d);
+        key[0] |= c0;
+        if (WMAX > 1 && DMAX > 64) key[1] |= c1;
+    }
+}
+
+// ------------------------------------------------------------ distance ----
+// Squared L2 of 16 bytes, exact in u32: |a-b| per byte then a byte dot product.
+__device__ __forceinline__ uint32_t sad2_16(const uint4& a, const uint4& b, uint32_t acc) {
+    uint32_t d;
+    d = __vabsdiffu4(a.x, b.x); acc = __dp4a(d, d, acc);
+    d = __vabsdiffu4(a.y, b.y); acc = __dp4a(d, d, acc);
+    d = __vabsdiffu4(a.z, b.z); acc = __dp4a(d, d, acc);
+    d = __vabsdiffu4(a.w, b.w); acc = __dp4a(d, d, acc);
+    return acc;
+}
+
+__device__ __forceinline__ uint4 ldg_stream(const void* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+// ------------------------------------------------------------ warp top-k ----
+// A warp holds a sorted (ascending) list of KCAP = 32*R packed (sqdist<<32 |
+// slot) values in registers, blocked layout: element e lives in lane e / R,
+// register e % R.  Packing makes the reference's (distance, id) order
+// (vecio.cpp:102-105) a plain integer order.
+template <int R>
+struct WarpTopK {
+    uint64_t a[R];
+    uint64_t thr;  // current k-th smallest (kNone until k elements seen)
+    int thr_lane, thr_reg;
+
+    __device__ __forceinline__ void init(int k) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) a[r] = kNone;
+        thr = kNone;
+        thr_lane = (k - 1) / R;
+        thr_reg = (k - 1) % R;
+    }
+
+    // Insert a warp-uniform value x (must be distinct from every held value).
+    __device__ __forceinline__ void insert(uint64_t x, int lane) {
+        const uint64_t prev_last = __shfl_up_sync(kFull, a[R - 1], 1);
+        const bool first_lt = lane == 0 || prev_last < x;
+#pragma unroll
+        for (int r = R - 1; r >= 0; --r) {
+            const uint64_t p = r == 0 ? prev_last : a[r - 1];
+            const bool p_lt = r == 0 ? first_lt : (a[r - 1] < x);
+            if (!p_lt) a[r] = p;
+            else if (a[r] > x) a[r] = x;
+        }
+        uint64_t mine = a[0];
+#pragma unroll
+        for (int r = 1; r < R; ++r)
+            if (r == thr_reg) mine = a[r];
+        thr = __shfl_sync(kFull, mine, thr_lane);
+    }
+
+    // Offer one candidate per lane (kNone = no candidate).
+    __device__ __forceinline__ void offer(uint64_t cand, int lane) {
+        unsigned m = __ballot_sync(kFull, cand < thr);
+        while (m) {
+            const int src = __ffs(m) - 1;
+            const uint64_t x = __shfl_sync(kFull, cand, src);
+            insert(x, lane);
+            m &= ~(1u << src);
+            m &= __ballot_sync(kFull, cand < thr);
+        }
+    }
+};
+
+__device__ __forceinline__ uint32_t hash_slot(uint32_t s) { return s * 2654435761u; }
+
+}  // namespace hcg

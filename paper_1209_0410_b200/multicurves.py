@@ -1,0 +1,393 @@
+"""Host-side mirror of the reference's index interface over the C ABI.
+
+Names and argument meaning follow the reference's namespace hc
+(proj/include/hypercurves/multicurves.hpp, vecio.hpp, curve.hpp):
+ProjectionScheme, default_scheme, SearchParams, Neighbor, MulticurvesIndex
+with search / retrieve_candidates / candidate_union / subindex taps, and
+brute_force_knn.  Errors the reference raises as std::invalid_argument come
+back as HcgInvalidArgument (a ValueError).
+
+Buffers may be numpy arrays (host) or torch tensors (host or CUDA); outputs
+follow the queries: CUDA tensors in -> CUDA tensors out, else numpy.
+Everything runs on the sm_100a kernels in libhcg.so -- there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import NamedTuple
+
+import numpy as np
+
+from ._lib import HCG_HILBERT, HCG_ZORDER, HcgInvalidArgument, HcgScheme, check, lib
+
+ZORDER, HILBERT = HCG_ZORDER, HCG_HILBERT
+
+
+@dataclass(frozen=True)
+class View:
+    """How the reference sees a descriptor byte b: offset + b * scale (f32).
+
+    raw    : float(b)          -- bvecs widening (vecio.cpp:50-51)
+    lifted : 1 + b/256         -- SURVEY.md F4; the reference quantizer keeps
+                                  the byte order at m >= 16
+    """
+    offset: float
+    scale: float
+    name: str
+
+    def floats(self, rows_u8: np.ndarray) -> np.ndarray:
+        f = np.asarray(rows_u8).astype(np.float32)
+        if self.scale != 1.0:
+            f = f * np.float32(self.scale)
+        if self.offset != 0.0:
+            f = np.float32(self.offset) + f
+        return f
+
+
+RAW = View(0.0, 1.0, "raw")
+LIFTED = View(1.0, 1.0 / 256.0, "lifted")
+
+
+@dataclass
+class ProjectionScheme:
+    """multicurves.hpp:18-32."""
+    d_full: int
+    bits_per_dim: int = 8
+    curve_kind: int = HILBERT
+    seed: int = 0
+    assignment: list = field(default_factory=list)
+
+    def curves(self) -> int:
+        return len(self.assignment)
+
+    def dims_of(self, c: int) -> int:
+        return len(self.assignment[c])
+
+
+def default_scheme(d_full: int, curves: int, bits_per_dim: int = 8, kind: int = HILBERT,
+                   seed: int = 0) -> ProjectionScheme:
+    """Round-robin dims over curves.  The seeded permutation
+    (seed != 0) is unpinned by the reference and rejected."""
+    if seed != 0:
+        raise HcgInvalidArgument(-1, "seeded permutation is unpinned by the reference (SPEC.md:203)")
+    off = (C.c_uint32 * (curves + 1))()
+    asg = (C.c_uint32 * max(d_full, 1))()
+    check(lib().hcg_default_assignment(d_full, curves, off, asg))
+    assignment = [[int(asg[i]) for i in range(off[c], off[c + 1])] for c in range(curves)]
+    return ProjectionScheme(d_full, bits_per_dim, kind, seed, assignment)
+
+
+@dataclass
+class SearchParams:
+    """multicurves.hpp:69-72."""
+    k: int = 1
+    probe_depth: int = 1
+
+
+class Neighbor(NamedTuple):
+    """vecio.hpp:27-32: id and rooted Euclidean distance."""
+    id: int
+    distance: float
+
+
+def make_lut(view: View, bits_per_dim: int) -> np.ndarray:
+    lut = (C.c_uint32 * 256)()
+    check(lib().hcg_make_lut(C.c_float(view.offset), C.c_float(view.scale), bits_per_dim, lut))
+    return np.frombuffer(lut, dtype=np.uint32).copy()
+
+
+# ----------------------------------------------------------------- buffers ----
+def _torch():
+    import torch
+    return torch
+
+
+def _is_torch(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+def _is_cuda(x) -> bool:
+    return _is_torch(x) and x.is_cuda
+
+
+def _ptr(x):
+    if x is None:
+        return None
+    if _is_torch(x):
+        if not x.is_contiguous():
+            raise HcgInvalidArgument(-1, "tensor must be contiguous")
+        return x.data_ptr()
+    if not x.flags["C_CONTIGUOUS"]:
+        raise HcgInvalidArgument(-1, "array must be C-contiguous")
+    return x.ctypes.data
+
+
+def _u8_2d(x, d_full: int):
+    if _is_torch(x):
+        torch = _torch()
+        if x.dtype != torch.uint8:
+            raise HcgInvalidArgument(-1, "descriptors must be uint8")
+        x = x.contiguous()
+        if x.dim() == 1:
+            x = x.view(1, -1)
+    else:
+        x = np.ascontiguousarray(x)
+        if x.dtype != np.uint8:
+            raise HcgInvalidArgument(-1, "descriptors must be uint8")
+        if x.ndim == 1:
+            x = x.reshape(1, -1)
+    if x.shape[1] != d_full:
+        raise HcgInvalidArgument(-1, f"dimension mismatch: {x.shape[1]} vs {d_full}")
+    return x
+
+
+def _empty_like_kind(ref, shape, np_dtype):
+    if _is_cuda(ref):
+        torch = _torch()
+        tdt = {np.uint64: torch.uint64, np.uint32: torch.uint32, np.int64: torch.int64}[np_dtype]
+        return torch.empty(shape, dtype=tdt, device=ref.device)
+    return np.empty(shape, dtype=np_dtype)
+
+
+def _stream(stream, ref=None):
+    if stream is not None:
+        return stream if isinstance(stream, int) else int(stream.cuda_stream)
+    if ref is not None and _is_cuda(ref):
+        return int(_torch().cuda.current_stream(ref.device).cuda_stream)
+    return None
+
+
+# ------------------------------------------------------------------- index ----
+class MulticurvesIndex:
+    """hc::MulticurvesIndex (multicurves.hpp:74-107) resident on one B200.
+
+    rows: n x d_full uint8 descriptors (numpy or torch, host or device); the
+    id of row s is id_base + s * id_stride (ids 0..n-1 by default).
+    """
+
+    def __init__(self, rows, scheme: ProjectionScheme, view: View = RAW, device: int = 0,
+                 id_base: int = 0, id_stride: int = 1, stream=None):
+        self.scheme = scheme
+        self.view = view
+        self.device = device
+        self.id_base = id_base
+        self.id_stride = id_stride
+        self._h = None
+        d = scheme.d_full
+        rows = _u8_2d(rows, d) if (rows is not None and len(rows)) else np.zeros((0, d), np.uint8)
+        n = rows.shape[0]
+        off = [0]
+        flat = []
+        for slots in scheme.assignment:
+            flat += list(slots)
+            off.append(len(flat))
+        self._off = (C.c_uint32 * len(off))(*off)
+        self._asg = (C.c_uint32 * max(len(flat), 1))(*flat)
+        s = HcgScheme()
+        s.d_full = d
+        s.curves = scheme.curves()
+        s.bits_per_dim = scheme.bits_per_dim
+        s.curve_kind = scheme.curve_kind
+        s.assign_off = self._off
+        s.assign = self._asg
+        lut = make_lut(view, scheme.bits_per_dim)
+        for b in range(256):
+            s.cell_lut[b] = int(lut[b])
+        s.dist_scale = float(view.scale)
+        self._scheme_c = s
+        h = C.c_void_p()
+        check(lib().hcg_build(C.byref(s), _ptr(rows), n, id_base, id_stride, device,
+                              _stream(stream, rows), C.byref(h)))
+        self._h = h
+
+    # -- lifetime
+    def close(self) -> None:
+        if self._h:
+            lib().hcg_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- shape
+    def size(self) -> int:
+        return int(lib().hcg_size(self._h))
+
+    def curves(self) -> int:
+        return int(lib().hcg_curves(self._h))
+
+    def key_words(self, c: int) -> int:
+        return int(lib().hcg_key_words(self._h, c))
+
+    def device_bytes(self) -> int:
+        return int(lib().hcg_device_bytes(self._h))
+
+    def rooted(self, sqdist) -> np.ndarray:
+        """Reference distance (vecio.cpp:111): sqrt of the exact squared distance."""
+        s = np.asarray(sqdist.cpu() if _is_torch(sqdist) else sqdist).astype(np.float64)
+        return np.sqrt(s) * self.view.scale
+
+    # -- batched search (the hot path)
+    def search_batch(self, queries, k: int, probe_depth: int, stream=None, out=None):
+        """Top-k by (distance, id) of every query: (ids u64 [nq,k], sqdist u32
+        [nq,k], len u32 [nq]).  Padding entries are id 2^64-1 / sqdist 2^32-1."""
+        q = _u8_2d(queries, self.scheme.d_full)
+        nq = q.shape[0]
+        if out is None:
+            ids = _empty_like_kind(q, (nq, k), np.uint64)
+            sq = _empty_like_kind(q, (nq, k), np.uint32)
+            ln = _empty_like_kind(q, (nq,), np.uint32)
+        else:
+            ids, sq, ln = out
+        check(lib().hcg_search(self._h, _ptr(q), nq, k, probe_depth, _ptr(ids), _ptr(sq), _ptr(ln),
+                               _stream(stream, q)))
+        return ids, sq, ln
+
+    def search(self, query, params: SearchParams) -> list:
+        """hc::MulticurvesIndex::search for one query -> NeighborList."""
+        ids, sq, ln = self.search_batch(query, params.k, params.probe_depth)
+        ids = np.asarray(ids.cpu() if _is_torch(ids) else ids)[0]
+        d = self.rooted(sq)[0]
+        n = int(np.asarray(ln.cpu() if _is_torch(ln) else ln)[0])
+        return [Neighbor(int(ids[i]), float(d[i])) for i in range(n)]
+
+    def search_packed(self, queries, k: int, probe_depth: int, out=None, stream=None):
+        """Per-shard packed results (sqdist<<32 | id) for the sharded merge."""
+        q = _u8_2d(queries, self.scheme.d_full)
+        nq = q.shape[0]
+        if out is None:
+            out = _empty_like_kind(q, (nq, k), np.uint64)
+        check(lib().hcg_search_packed(self._h, _ptr(q), nq, k, probe_depth, _ptr(out),
+                                      _stream(stream, q)))
+        return out
+
+    # -- parity taps
+    def keys(self, rows, c: int) -> np.ndarray:
+        """curve_encode(kind, project(v, scheme, c)) of each row: [n, words] u64 (LS word first)."""
+        r = _u8_2d(rows, self.scheme.d_full)
+        out = np.zeros((r.shape[0], self.key_words(c)), np.uint64)
+        check(lib().hcg_keys(self._h, _ptr(r), r.shape[0], c, _ptr(out), _stream(None, r)))
+        return out
+
+    def subindex(self, c: int, with_keys: bool = False):
+        """SubIndex::entries() of curve c: ids (and full keys) in sorted order."""
+        n = self.size()
+        ids = np.zeros(n, np.uint64)
+        keys = np.zeros((n, self.key_words(c)), np.uint64) if with_keys else None
+        check(lib().hcg_sorted(self._h, c, _ptr(ids), _ptr(keys) if with_keys else None, None))
+        return (ids, keys) if with_keys else ids
+
+    def windows(self, queries, probe_depth: int):
+        """rank_of and window [begin, end) per (query, curve)."""
+        q = _u8_2d(queries, self.scheme.d_full)
+        nq, C_ = q.shape[0], self.curves()
+        r = np.zeros((nq, C_), np.uint64)
+        b = np.zeros((nq, C_), np.uint64)
+        e = np.zeros((nq, C_), np.uint64)
+        check(lib().hcg_windows(self._h, _ptr(q), nq, probe_depth, _ptr(r), _ptr(b), _ptr(e),
+                                _stream(None, q)))
+        return r, b, e
+
+    def retrieve_candidates(self, query, c: int, depth: int) -> np.ndarray:
+        """Ids of the window on curve c (multicurves.hpp:83-85), in key order."""
+        _, b, e = self.windows(query, depth)
+        ids = self.subindex(c)
+        return ids[int(b[0, c]):int(e[0, c])]
+
+    def candidates(self, queries, probe_depth: int):
+        """Deduplicated candidate ids per query (list of sorted arrays)."""
+        q = _u8_2d(queries, self.scheme.d_full)
+        nq = q.shape[0]
+        cap = self.curves() * min(probe_depth, max(self.size(), 1))
+        out = np.zeros((nq, max(cap, 1)), np.uint64)
+        cnt = np.zeros(nq, np.uint32)
+        check(lib().hcg_candidates(self._h, _ptr(q), nq, probe_depth, _ptr(out), max(cap, 1),
+                                   _ptr(cnt), _stream(None, q)))
+        return [np.sort(out[i, :cnt[i]]) for i in range(nq)]
+
+    def candidate_union(self, query, depth: int) -> np.ndarray:
+        """multicurves.hpp:87-89 (sorted ascending)."""
+        return self.candidates(query, depth)[0]
+
+    def brute_force(self, queries, k: int, stream=None):
+        """brute_force_knn (vecio.cpp:115-122) over the indexed rows, on the GPU."""
+        q = _u8_2d(queries, self.scheme.d_full)
+        nq = q.shape[0]
+        ids = _empty_like_kind(q, (nq, k), np.uint64)
+        sq = _empty_like_kind(q, (nq, k), np.uint32)
+        ln = _empty_like_kind(q, (nq,), np.uint32)
+        check(lib().hcg_brute_force(self._h, _ptr(q), nq, k, _ptr(ids), _ptr(sq), _ptr(ln),
+                                    _stream(stream, q)))
+        return ids, sq, ln
+
+
+def merge_packed(packed, k: int, device: int = 0, stream=None):
+    """Hypershard aggregate: packed [parts, nq, k] -> top-k."""
+    parts, nq = int(packed.shape[0]), int(packed.shape[1])
+    ids = _empty_like_kind(packed, (nq, k), np.uint64)
+    sq = _empty_like_kind(packed, (nq, k), np.uint32)
+    ln = _empty_like_kind(packed, (nq,), np.uint32)
+    check(lib().hcg_merge_packed(_ptr(packed), parts, nq, k, _ptr(ids), _ptr(sq), _ptr(ln), device,
+                                 _stream(stream, packed)))
+    return ids, sq, ln
+
+
+# ------------------------------------------------------------ equivalence ----
+def binomial_tail(trials: int, p: float, phi: int) -> float:
+    if not (0.0 < p < 1.0):
+        raise HcgInvalidArgument(-1, "p must be in (0, 1)")
+    return float(lib().hcg_binomial_tail(trials, p, phi))
+
+
+def miss_bound(Phi: int, shards: int, phi: int) -> float:
+    return float(lib().hcg_miss_bound(Phi, shards, phi))
+
+
+def plan_depth(Phi: int, shards: int, target: float) -> int:
+    return int(lib().hcg_plan_depth(Phi, shards, target))
+
+
+def shard_probe_depth(depth: int, shards: int, target: float = 0.02) -> int:
+    """Per-shard probe depth 2*phi* for a sequential depth D (Phi = ceil(D/2),
+    SPEC.md:329) at a miss-probability target."""
+    Phi = (depth + 1) // 2
+    return 2 * plan_depth(Phi, shards, target)
+
+
+# ------------------------------------------------------------- synthetic ----
+def gen_rows(first: int, count: int, stride: int = 1, device: int = 0, stream=None):
+    """Rows first + i*stride of the SURVEY.md §8(d) generator, as a CUDA uint8 tensor."""
+    torch = _torch()
+    out = torch.empty((count, 128), dtype=torch.uint8, device=f"cuda:{device}")
+    check(lib().hcg_gen_rows(first, stride, count, _ptr(out) if count else None, device,
+                             _stream(stream, out)))
+    return out
+
+
+def gen_queries(first: int, count: int, n_db: int, device: int = 0, stream=None):
+    torch = _torch()
+    out = torch.empty((count, 128), dtype=torch.uint8, device=f"cuda:{device}")
+    check(lib().hcg_gen_queries(first, count, n_db, _ptr(out) if count else None, device,
+                                _stream(stream, out)))
+    return out
+
+
+def recall_at(found_ids, true_ids, k: int) -> float:
+    """Mean |found[:k] ∩ true[:k]| / k over queries."""
+    f = np.asarray(found_ids)[:, :k]
+    t = np.asarray(true_ids)[:, :k]
+    hits = 0
+    for a, b in zip(f, t):
+        hits += len(set(a.tolist()) & set(b.tolist()) - {2**64 - 1})
+    return hits / (k * max(len(f), 1))
+
+
+__all__ = [
+    "View", "RAW", "LIFTED", "ProjectionScheme", "default_scheme", "SearchParams", "Neighbor",
+    "MulticurvesIndex", "merge_packed", "binomial_tail", "miss_bound", "plan_depth",
+    "shard_probe_depth", "gen_rows", "gen_queries", "make_lut", "recall_at", "ZORDER", "HILBERT",
+]
