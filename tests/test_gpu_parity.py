@@ -44,6 +44,8 @@ def _check_search(gi, oi, view, qs, k, depth):
 @pytest.mark.parametrize("kind", [H.HILBERT, H.ZORDER], ids=["hilbert", "zorder"])
 @pytest.mark.parametrize("curves", [1, 2, 4, 8, 16])
 def test_keys_sorted_windows_search(view, m, kind, curves):
+    if (128 // curves) * m > 1024:
+        pytest.skip("key wider than HC_MAX_KEY_BITS (the reference rejects it too)")
     n, nq = 3000, 48
     rows = P.gen_rows(0, n)
     qs = P.gen_queries(0, nq, n)
