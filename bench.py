@@ -1,0 +1,471 @@
+#!/usr/bin/env python3
+"""bench.py -- Hypercurves approximate-kNN hot path on B200 (BASELINE.json).
+
+One "step" = one batched search of a fresh batch of synthetic queries through
+the whole hot path (per-curve keys -> lower_bound -> windows -> dedup ->
+gather -> exact L2 -> top-k; at N>1 also the NCCL all-gather + merge).
+
+  N=1 : configs[1] -- 10M x 128-d uint8 (synthetic SIFT-like),
+        100K queries per step, k=10, 8 Hilbert curves, probe depth 350,
+        lifted view (1 + b/256, m=16; recall@10 ~0.99).
+  N>1 : configs[2] -- 100M x 128-d sharded id mod N over N ranks (one process
+        per GPU, torchrun), per-shard depth from the equivalence planner
+        (miss < 2%), NCCL all-gather of packed top-k + K4.
+
+value   : queries/s with queries already resident in HBM (device timed,
+          CUDA events, max over ranks).
+e2e     : the same through the public API with pinned HOST query buffers and a
+          host read-back of every step's results (H2D + D2H inside the timing).
+roofline: the refine kernel (gather + L2 + top-k) -- algorithmic bytes per
+          launch / its CUDA-event duration vs the measured HBM copy peak.
+cpu_baseline : the reference's CPU path (oracle/_ref: the reference's own
+          curve.cpp + vecio.cpp + the multicurves.hpp restatement) on this
+          host's cores, over a bounded query sample of the same workload.
+
+--impl reference runs only that CPU reference path (rank 0; other ranks exit).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "kNN queries/sec at fixed probe depth & recall@10, 1/2/4/8 B200; HBM GB/s"
+DATA = "synthetic: SURVEY.md §8(d) counter-based SIFT-like uint8 generator (same bytes on CPU and GPU)"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--n", type=int, default=0, help="database rows (default 10M at N=1, 100M at N>1)")
+    p.add_argument("--queries", type=int, default=100_000, help="queries per step")
+    p.add_argument("--k", type=int, default=10)
+    p.add_argument("--depth", type=int, default=350)
+    p.add_argument("--curves", type=int, default=8)
+    p.add_argument("--view", choices=["lifted", "raw"], default="lifted")
+    p.add_argument("--kind", choices=["hilbert", "zorder"], default="hilbert")
+    p.add_argument("--shard-depth", default="planned",
+                   help="N>1 per-shard depth: planned | full | optimist | <int>")
+    p.add_argument("--recall-sample", type=int, default=1000)
+    p.add_argument("--cpu-sample", type=int, default=4000, help="queries in the CPU baseline sample")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--latency-batches", default="1,16,256,4096,65536")
+    p.add_argument("--latency-reps", type=int, default=20)
+    return p.parse_args()
+
+
+# --------------------------------------------------------------- plumbing ----
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap", "utilization.gpu"]
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == len(self.FIELDS):
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        loaded = [r for r in self.rows if (num(r[6]) or 0) > 0] or self.rows
+        sm = [num(r[0]) for r in loaded if num(r[0]) is not None]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": num(self.rows[0][1]), "reasons": reasons, "samples": len(self.rows),
+                "samples_under_load": len(loaded)}
+
+
+def measured_peak_gbs():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(config_key: str):
+    """dram bytes per refine launch from a committed ncu --set full summary, if any."""
+    path = os.path.join(ROOT, "profiles", "refine_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        e = d.get(config_key)
+        return e if e else None
+    except Exception:
+        return None
+
+
+# --------------------------------------------------------- CPU reference ----
+def cpu_reference_qps(rows_u8, queries_u8, curves, m, kind, view, k, depth, threads, reps=1):
+    """The reference's CPU path (oracle/_ref) on a bounded query sample; returns
+    (q/s, seconds, results of the last rep)."""
+    from oracle import pyoracle as P
+    ri = P.RefIndex(rows_u8, curves, m, kind, view)
+    best = None
+    res = None
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        res = ri.search(queries_u8, k, depth, threads=threads)
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    del ri
+    return queries_u8.shape[0] / best, best, res
+
+
+# ------------------------------------------------------------------- ours ----
+def run_ours(a):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1209_0410_b200 as H
+    from paper_1209_0410_b200.sharded import ShardedIndex, recall
+
+    rank, world, local = dist_env()
+    if world != a.gpus:
+        a.gpus = world
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    view = H.LIFTED if a.view == "lifted" else H.RAW
+    m = 16 if a.view == "lifted" else 8
+    kind = H.HILBERT if a.kind == "hilbert" else H.ZORDER
+    n_total = a.n or (10_000_000 if world == 1 else 100_000_000)
+    Q, k, D, C = a.queries, a.k, a.depth, a.curves
+    if world == 1:
+        shard_depth = D
+    elif a.shard_depth == "planned":
+        shard_depth = H.shard_probe_depth(D, world, 0.02)
+    elif a.shard_depth == "full":
+        shard_depth = D
+    elif a.shard_depth == "optimist":
+        shard_depth = 2 * (((D + 1) // 2 + world - 1) // world)
+    else:
+        shard_depth = int(a.shard_depth)
+    scheme = H.default_scheme(128, C, m, kind)
+
+    stream = torch.cuda.current_stream(dev)
+    t0 = time.perf_counter()
+    sidx = ShardedIndex.from_generator(n_total, scheme, view, rank, world, local)
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t0
+    if world > 1:
+        dist.barrier()
+
+    nb = a.warmup + a.steps
+    batches = [H.gen_queries(b * Q, Q, n_total, device=local) for b in range(nb)]
+    out = (torch.empty((Q, k), dtype=torch.uint64, device=dev),
+           torch.empty((Q, k), dtype=torch.uint32, device=dev),
+           torch.empty((Q,), dtype=torch.uint32, device=dev))
+
+    def step(b):
+        sidx.search(batches[b], k, shard_depth, out=out)
+
+    def timed(fn):
+        for b in range(a.warmup):
+            fn(b)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for s in range(a.steps):
+            fn(a.warmup + s)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    ms_total = timed(step)
+
+    # e2e: pinned host queries in, host results out, through the public API.
+    host_batches = [bt.cpu().pin_memory() for bt in batches]
+    host_out = (torch.empty((Q, k), dtype=torch.uint64).pin_memory(),
+                torch.empty((Q, k), dtype=torch.uint32).pin_memory(),
+                torch.empty((Q,), dtype=torch.uint32).pin_memory())
+    dq = torch.empty((Q, 128), dtype=torch.uint8, device=dev)
+
+    def step_e2e(b):
+        if world == 1:
+            sidx.local.search_batch(host_batches[b], k, shard_depth, out=host_out)  # library stages H2D/D2H
+        else:
+            dq.copy_(host_batches[b], non_blocking=True)
+            r = sidx.search(dq, k, shard_depth, out=out)
+            for h, d_ in zip(host_out, r):
+                h.copy_(d_, non_blocking=True)
+            stream.synchronize()
+
+    ms_e2e = timed(step_e2e)
+    clocks.stop()
+    h2d = Q * 128
+    d2h = Q * k * 8 + Q * k * 4 + Q * 4
+
+    # refine-kernel roofline (outside the timed region): per-launch device time.
+    tl, tr = [], []
+    for b in range(a.warmup, nb):
+        ml, mr = sidx.local.search_timed(batches[b], k, shard_depth, out=out)
+        tl.append(ml)
+        tr.append(mr)
+    U = sidx.local.candidate_counts(batches[a.warmup], shard_depth).astype(np.float64)
+    take = min(shard_depth, sidx.local.size())
+    bytes_refine = float(U.sum() * 128 + Q * (4 * C * take + 4 * C + 128) + Q * (12 * k + 4))
+    refine_ms = statistics.mean(tr)
+    peak, peak_src = measured_peak_gbs()
+    achieved = bytes_refine / (refine_ms * 1e-3) / 1e9
+    logn = max(1, int(np.ceil(np.log2(max(2, sidx.local.size())))))
+    bytes_q = float(U.mean() * 128 + 4 * C * take + 16 * C * logn + 128 + 8 * k)
+
+    # recall@k on a query sample against exact brute force (GPU K5, merged across shards).
+    rs = min(a.recall_sample, Q)
+    qs = batches[0][:rs].contiguous()
+    got = sidx.search(qs, k, shard_depth)
+    exact = sidx.brute_force(qs, k)
+    rec = recall(got[0].cpu().numpy(), exact[0].cpu().numpy(), k)
+
+    # latency per batch size (device resident, per call, p50/p99)
+    lat = {}
+    for bs in [int(x) for x in a.latency_batches.split(",") if x]:
+        if bs > Q:
+            continue
+        qb = batches[0][:bs].contiguous()
+        o = (torch.empty((bs, k), dtype=torch.uint64, device=dev),
+             torch.empty((bs, k), dtype=torch.uint32, device=dev),
+             torch.empty((bs,), dtype=torch.uint32, device=dev))
+        for _ in range(3):
+            sidx.search(qb, k, shard_depth, out=o)
+        ts = []
+        for _ in range(a.latency_reps):
+            if world > 1:
+                dist.barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            sidx.search(qb, k, shard_depth, out=o)
+            e1.record(stream)
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        ts.sort()
+        lat[str(bs)] = {"p50_ms": round(ts[len(ts) // 2], 4), "p99_ms": round(ts[min(len(ts) - 1, int(0.99 * len(ts)))], 4),
+                        "qps_at_p50": round(bs / (ts[len(ts) // 2] * 1e-3), 1)}
+
+    cpu = None
+    parity = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        S = min(a.cpu_sample, Q)
+        rows_h = H.gen_rows(0, n_total, device=local).cpu().numpy()
+        qh = batches[0][:S].cpu().numpy()
+        qps_cpu, secs, (rids, rdist, rln) = cpu_reference_qps(rows_h, qh, C, m, kind, 1 if a.view == "lifted" else 0,
+                                                             k, D, threads)
+        del rows_h
+        gi, gs, gl = sidx.local.search_batch(qh, k, D)
+        same = (np.array_equal(gl, rln) and np.array_equal(gi, rids)
+                and np.array_equal(sidx.local.rooted(gs), rdist))
+        parity = {"sample_queries": S, "ids_and_distances_identical": bool(same)}
+        from oracle import pyoracle as P
+        cpu = {"value": round(qps_cpu, 1), "unit": "queries/s", "cores": threads,
+               "kind": "reference" if P.ref_available() else "port",
+               "sample": f"{S} queries of step 0's batch over the same {n_total} rows "
+                         f"(reference curve.cpp/vecio.cpp + multicurves.hpp restatement, "
+                         f"{threads} threads, {secs:.2f} s wall)"}
+
+    if rank == 0:
+        ms_step = ms_total / a.steps
+        value = Q * a.steps / (ms_total * 1e-3)
+        e2e_value = Q * a.steps / (ms_e2e * 1e-3)
+        traffic = ncu_traffic(f"N{world}_Q{Q}_D{shard_depth}_{a.view}")
+        line = {
+            "metric": METRIC,
+            "value": round(value, 1),
+            "unit": "queries/s",
+            "n_gpus": world,
+            "steps": a.steps,
+            "warmup": a.warmup,
+            "ms_per_step": round(ms_step, 4),
+            "higher_is_better": True,
+            "scaling": "weak" if world == 1 else "strong",
+            "vs_baseline": None,
+            "dtype": "u8",
+            "data": DATA,
+            "config": {
+                "workload": ("configs[1]: 10M x 128-d, 100K queries/step, k=10, 8 curves, fixed probe depth"
+                             if world == 1 else
+                             "configs[2]: 100M x 128-d sharded id mod N, k=10, NCCL allgather top-k merge"),
+                "n_db": n_total, "queries_per_step": Q, "k": k, "curves": C, "probe_depth": D,
+                "shard_probe_depth": shard_depth, "curve": a.kind, "view": a.view, "bits_per_dim": m,
+                "recall_at_k": round(rec, 4), "recall_sample": rs,
+                "l2": "inputs larger than L2 (descriptors + sorted curves > 2.8 GB vs 126 MB L2); "
+                      "a fresh query batch every step",
+                "build_s": round(build_s, 3),
+                "device_index_bytes": sidx.local.device_bytes(),
+            },
+            "roofline": {
+                "bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic,
+                "kernel": "k_refine (dedup + gather + exact L2 + top-k)",
+                "algorithmic_bytes_per_launch": bytes_refine,
+                "launch_ms": round(refine_ms, 4), "locate_ms": round(statistics.mean(tl), 4),
+                "peak_source": peak_src,
+                "bytes_per_query_B_q": round(bytes_q, 1),
+                "unique_candidates_per_query": round(float(U.mean()), 1),
+                "step_hbm_gbs": round(value * bytes_q / 1e9, 1),
+            },
+            "cpu_baseline": cpu,
+            "parity_vs_reference": parity,
+            "e2e": {"value": round(e2e_value, 1), "unit": "queries/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "gpu_launches": a.steps * (2 if world == 1 else 3),
+            "clocks": clocks.summary(),
+            "latency": lat,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+# -------------------------------------------------------------- reference ----
+def run_reference(a):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import pyoracle as P
+
+    view = 1 if a.view == "lifted" else 0
+    m = 16 if a.view == "lifted" else 8
+    kind = 1 if a.kind == "hilbert" else 0
+    n_total = a.n or (10_000_000 if world == 1 else 100_000_000)
+    threads = os.cpu_count() or 1
+    k, D, C = a.k, a.depth, a.curves
+    if world == 1:
+        rows = P.gen_rows(0, n_total, threads)
+        depth = D
+        note = f"{n_total} rows"
+        shards_on_host = 1
+    else:
+        # The host must run every shard of the configs[2] partition; one shard
+        # (capped at 12.5M rows, the N=8 shard size) is built and timed, and the
+        # host throughput is that shard's rate divided by the shard count.
+        from paper_1209_0410_b200.multicurves import shard_probe_depth  # pure host math
+        cnt = min((n_total + world - 1) // world, 12_500_000)
+        rows = P.gen_rows(0, cnt, threads, stride=world)
+        depth = shard_probe_depth(D, world, 0.02) if a.shard_depth == "planned" else D
+        note = f"shard 0 of {world} ({cnt} rows, per-shard depth {depth}); q/s = shard rate / {world}"
+        shards_on_host = world
+    t0 = time.perf_counter()
+    ri = P.RefIndex(rows, C, m, kind, view)
+    build_s = time.perf_counter() - t0
+    S = min(a.cpu_sample, a.queries)
+    steps_q = [P.gen_queries(b * a.queries, S, n_total, threads) for b in range(a.warmup + a.steps)]
+    for b in range(a.warmup):
+        ri.search(steps_q[b], k, depth, threads)
+    t0 = time.perf_counter()
+    for s in range(a.steps):
+        ri.search(steps_q[a.warmup + s], k, depth, threads)
+    dt = time.perf_counter() - t0
+    value = S * a.steps / dt / shards_on_host
+    kind_s = "reference" if P.ref_available() else "port"
+    line = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": round(value, 1),
+        "unit": "queries/s",
+        "n_gpus": world,
+        "steps": a.steps,
+        "warmup": a.warmup,
+        "ms_per_step": round(dt / a.steps * 1e3, 3),
+        "higher_is_better": True,
+        "scaling": "weak" if world == 1 else "strong",
+        "vs_baseline": None,
+        "dtype": "u8",
+        "data": DATA,
+        "config": {"workload": "configs[1]" if world == 1 else "configs[2]", "n_db": n_total,
+                   "queries_per_step_sample": S, "k": k, "curves": C, "probe_depth": D,
+                   "shard_probe_depth": depth, "view": a.view, "bits_per_dim": m, "curve": a.kind,
+                   "build_s": round(build_s, 2)},
+        "cpu_baseline": {"value": round(value, 1), "unit": "queries/s", "cores": threads, "kind": kind_s,
+                         "sample": f"{S} queries per step over {note}; reference curve.cpp/vecio.cpp + "
+                                   f"multicurves.hpp restatement, query-parallel on {threads} threads"},
+        "e2e": {"value": round(value, 1), "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

@@ -128,6 +128,13 @@ hcg_status hcg_search(const hcg_index* index, const uint8_t* queries, uint32_t n
                       uint32_t depth, uint64_t* out_ids, uint32_t* out_sqdist, uint32_t* out_len,
                       void* stream);
 
+/* hcg_search with per-kernel device times: records CUDA events around the
+ * locate and refine launches on `stream` and synchronises it; ms_out[0] is the
+ * locate kernel, ms_out[1] the refine kernel (instrumentation for bench.py). */
+hcg_status hcg_search_timed(const hcg_index* index, const uint8_t* queries, uint32_t nq, uint32_t k,
+                            uint32_t depth, uint64_t* out_ids, uint32_t* out_sqdist,
+                            uint32_t* out_len, float* ms_out, void* stream);
+
 /* Per-shard search writing packed (sqdist << 32 | id) u64 per result, nq x k,
  * padding UINT64_MAX; requires ids < 2^32.  Input to hcg_merge_packed. */
 hcg_status hcg_search_packed(const hcg_index* index, const uint8_t* queries, uint32_t nq,
@@ -153,7 +160,8 @@ hcg_status hcg_windows(const hcg_index* index, const uint8_t* queries, uint32_t 
                        uint64_t* out_rank, uint64_t* out_begin, uint64_t* out_end, void* stream);
 /* Deduplicated candidate ids per query (set semantics, order unspecified):
  * out_ids is nq x cap, out_count[q] the number of unique candidates.  Fails
- * with HCG_ECAPACITY when a query has more than cap candidates. */
+ * with HCG_ECAPACITY when a query has more than cap candidates.  With
+ * out_ids == NULL and cap == 0 only the counts are produced. */
 hcg_status hcg_candidates(const hcg_index* index, const uint8_t* queries, uint32_t nq,
                           uint32_t depth, uint64_t* out_ids, uint32_t cap, uint32_t* out_count,
                           void* stream);

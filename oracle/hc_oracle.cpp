@@ -492,13 +492,17 @@ int orc_brute_force(const float* rows, const uint64_t* ids, uint64_t n, uint32_t
     return ORC_OK;
 }
 
-void orc_gen_rows(uint64_t i0, uint64_t count, uint8_t* out, int threads) {
+void orc_gen_rows_strided(uint64_t first, uint64_t stride, uint64_t count, uint8_t* out, int threads) {
     const GenTables& g = gen_tables();
     const uint64_t chunk = 4096;
     parallel_for((count + chunk - 1) / chunk, threads, [&](uint64_t b) {
         const uint64_t e = std::min(count, (b + 1) * chunk);
-        for (uint64_t i = b * chunk; i < e; ++i) gen_row(g, i0 + i, out + i * kD);
+        for (uint64_t i = b * chunk; i < e; ++i) gen_row(g, first + i * stride, out + i * kD);
     });
+}
+
+void orc_gen_rows(uint64_t i0, uint64_t count, uint8_t* out, int threads) {
+    orc_gen_rows_strided(i0, 1, count, out, threads);
 }
 
 // Queries perturb database row H(4,q,~0) % n_db.

@@ -85,6 +85,7 @@ def orc() -> C.CDLL:
         L.orc_brute_force.argtypes = [_f32p, C.c_void_p, C.c_uint64, C.c_uint32, _f32p, C.c_uint64,
                                       C.c_uint64, _u64p, _f64p, _u32p, C.c_int]
         L.orc_gen_rows.argtypes = [C.c_uint64, C.c_uint64, _u8p, C.c_int]
+        L.orc_gen_rows_strided.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, _u8p, C.c_int]
         L.orc_gen_queries.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, _u8p, C.c_int]
         _orc = L
     return _orc
@@ -94,9 +95,9 @@ def nthreads() -> int:
     return max(1, os.cpu_count() or 1)
 
 
-def gen_rows(i0: int, count: int, threads: int | None = None) -> np.ndarray:
+def gen_rows(i0: int, count: int, threads: int | None = None, stride: int = 1) -> np.ndarray:
     out = np.empty((count, 128), np.uint8)
-    orc().orc_gen_rows(i0, count, out, threads or nthreads())
+    orc().orc_gen_rows_strided(i0, stride, count, out, threads or nthreads())
     return out
 
 

@@ -27,7 +27,7 @@ HCG_MAX_KEY_BITS = 1024
 EXPORTS = [
     "hcg_last_error", "hcg_version", "hcg_make_lut", "hcg_default_assignment", "hcg_build",
     "hcg_free", "hcg_size", "hcg_curves", "hcg_key_words", "hcg_device_bytes", "hcg_search",
-    "hcg_search_packed", "hcg_merge_packed", "hcg_keys", "hcg_sorted", "hcg_windows",
+    "hcg_search_timed", "hcg_search_packed", "hcg_merge_packed", "hcg_keys", "hcg_sorted", "hcg_windows",
     "hcg_candidates", "hcg_brute_force", "hcg_binomial_tail", "hcg_miss_bound",
     "hcg_plan_depth", "hcg_gen_rows", "hcg_gen_queries",
 ]
@@ -85,6 +85,7 @@ def lib() -> C.CDLL:
     L.hcg_device_bytes.restype = u64
     L.hcg_device_bytes.argtypes = [vp]
     L.hcg_search.argtypes = [vp, vp, u32, u32, u32, vp, vp, vp, vp]
+    L.hcg_search_timed.argtypes = [vp, vp, u32, u32, u32, vp, vp, vp, P(C.c_float), vp]
     L.hcg_search_packed.argtypes = [vp, vp, u32, u32, u32, vp, vp]
     L.hcg_merge_packed.argtypes = [vp, u32, u32, u32, vp, vp, vp, C.c_int, vp]
     L.hcg_keys.argtypes = [vp, vp, u64, u32, vp, vp]
@@ -101,7 +102,7 @@ def lib() -> C.CDLL:
     L.hcg_gen_rows.argtypes = [u64, u64, u64, vp, C.c_int, vp]
     L.hcg_gen_queries.argtypes = [u64, u64, u64, vp, C.c_int, vp]
     for name in ("hcg_make_lut", "hcg_default_assignment", "hcg_build", "hcg_free", "hcg_search",
-                 "hcg_search_packed", "hcg_merge_packed", "hcg_keys", "hcg_sorted", "hcg_windows",
+                 "hcg_search_timed", "hcg_search_packed", "hcg_merge_packed", "hcg_keys", "hcg_sorted", "hcg_windows",
                  "hcg_candidates", "hcg_brute_force", "hcg_gen_rows", "hcg_gen_queries"):
         getattr(L, name).restype = C.c_int
     del u8

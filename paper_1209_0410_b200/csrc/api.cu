@@ -495,7 +495,7 @@ uint64_t hcg_device_bytes(const hcg_index* ix) { return ix ? ix->bytes : 0; }
 
 static hcg_status search_impl(const hcg_index* ix, const uint8_t* queries, uint32_t nq, uint32_t k, uint32_t depth,
                               uint64_t* out_ids, uint32_t* out_sqdist, uint32_t* out_len, uint64_t* out_packed,
-                              void* stream) {
+                              void* stream, float* ms_out = nullptr) {
     HCG_TRY(check_search_args(ix, k, depth));
     if (nq == 0) return HCG_OK;
     if (!queries) return set_error(HCG_EINVAL, "null queries");
@@ -529,7 +529,13 @@ static hcg_status search_impl(const hcg_index* ix, const uint8_t* queries, uint3
         HCG_TRY(stage_rows(sc, queries, nq, ix->d_full, ix->pitch, &dq));
         uint32_t* begins = sc.alloc<uint32_t>(size_t(nq) * ix->C);
         if (!begins) return set_error(HCG_ENOMEM, "window buffer");
+        cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+        if (ms_out) {
+            for (auto& e : ev) HCG_TRY_CUDA(cudaEventCreate(&e));
+            HCG_TRY_CUDA(cudaEventRecord(ev[0], st));
+        }
         HCG_TRY(locate(ix, sc, dq, nq, depth, begins, nullptr));
+        if (ms_out) HCG_TRY_CUDA(cudaEventRecord(ev[1], st));
         RefineArgs a = refine_args(ix, dq, nq, depth, k, begins);
         if (packed) {
             a.mode = kOutPacked;
@@ -541,6 +547,13 @@ static hcg_status search_impl(const hcg_index* ix, const uint8_t* queries, uint3
             a.out_len = ol.dev;
         }
         HCG_TRY(run_refine(ix, sc, a));
+        if (ms_out) {
+            HCG_TRY_CUDA(cudaEventRecord(ev[2], st));
+            HCG_TRY_CUDA(cudaEventSynchronize(ev[2]));
+            HCG_TRY_CUDA(cudaEventElapsedTime(&ms_out[0], ev[0], ev[1]));
+            HCG_TRY_CUDA(cudaEventElapsedTime(&ms_out[1], ev[1], ev[2]));
+            for (auto& e : ev) cudaEventDestroy(e);
+        }
     }
     HCG_TRY(finish_out(sc, oi));
     HCG_TRY(finish_out(sc, os));
@@ -553,6 +566,13 @@ static hcg_status search_impl(const hcg_index* ix, const uint8_t* queries, uint3
 hcg_status hcg_search(const hcg_index* ix, const uint8_t* queries, uint32_t nq, uint32_t k, uint32_t depth,
                       uint64_t* out_ids, uint32_t* out_sqdist, uint32_t* out_len, void* stream) {
     return search_impl(ix, queries, nq, k, depth, out_ids, out_sqdist, out_len, nullptr, stream);
+}
+
+hcg_status hcg_search_timed(const hcg_index* ix, const uint8_t* queries, uint32_t nq, uint32_t k, uint32_t depth,
+                            uint64_t* out_ids, uint32_t* out_sqdist, uint32_t* out_len, float* ms_out, void* stream) {
+    if (!ms_out) return set_error(HCG_EINVAL, "null ms_out");
+    ms_out[0] = ms_out[1] = 0.0f;
+    return search_impl(ix, queries, nq, k, depth, out_ids, out_sqdist, out_len, nullptr, stream, ms_out);
 }
 
 hcg_status hcg_search_packed(const hcg_index* ix, const uint8_t* queries, uint32_t nq, uint32_t k, uint32_t depth,
@@ -685,7 +705,7 @@ hcg_status hcg_candidates(const hcg_index* ix, const uint8_t* queries, uint32_t 
                           uint32_t cap, uint32_t* out_count, void* stream) {
     HCG_TRY(check_search_args(ix, 1, depth));
     if (nq == 0) return HCG_OK;
-    if (!queries || !out_ids || !out_count) return set_error(HCG_EINVAL, "null buffer");
+    if (!queries || !out_count || (!out_ids && cap)) return set_error(HCG_EINVAL, "null buffer");
     DeviceGuard g(ix->device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     Scratch sc(st);
@@ -714,8 +734,9 @@ hcg_status hcg_candidates(const hcg_index* ix, const uint8_t* queries, uint32_t 
     std::vector<uint32_t> counts(nq);
     if (oc.host) std::memcpy(counts.data(), out_count, nq * 4);
     else HCG_TRY_CUDA(cudaMemcpy(counts.data(), out_count, nq * 4, cudaMemcpyDeviceToHost));
-    for (uint32_t c : counts)
-        if (c > cap) return set_error(HCG_ECAPACITY, "candidate set larger than cap");
+    if (out_ids)
+        for (uint32_t c : counts)
+            if (c > cap) return set_error(HCG_ECAPACITY, "candidate set larger than cap");
     return HCG_OK;
 }
 

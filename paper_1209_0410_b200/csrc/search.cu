@@ -228,8 +228,9 @@ __global__ void __launch_bounds__(kRefineThreads) k_refine(RefineArgs a, uint32_
 
         if (a.mode == kOutCandidates) {
             const uint32_t lim = U < a.cap ? U : a.cap;
-            for (uint32_t i = tid; i < lim; i += kRefineThreads)
-                a.out_ids[uint64_t(q) * a.cap + i] = a.id_base + uint64_t(list[i]) * a.id_stride;
+            if (a.out_ids)
+                for (uint32_t i = tid; i < lim; i += kRefineThreads)
+                    a.out_ids[uint64_t(q) * a.cap + i] = a.id_base + uint64_t(list[i]) * a.id_stride;
             if (tid == 0) a.out_len[q] = U;
             __syncthreads();
             continue;

@@ -247,6 +247,16 @@ class MulticurvesIndex:
                                _stream(stream, q)))
         return ids, sq, ln
 
+    def search_timed(self, queries, k: int, probe_depth: int, out, stream=None):
+        """search_batch into preallocated outputs, returning the device time (ms)
+        of the locate and refine kernels measured with CUDA events on `stream`."""
+        q = _u8_2d(queries, self.scheme.d_full)
+        ids, sq, ln = out
+        ms = (C.c_float * 2)()
+        check(lib().hcg_search_timed(self._h, _ptr(q), q.shape[0], k, probe_depth, _ptr(ids), _ptr(sq),
+                                     _ptr(ln), ms, _stream(stream, q)))
+        return float(ms[0]), float(ms[1])
+
     def search(self, query, params: SearchParams) -> list:
         """hc::MulticurvesIndex::search for one query -> NeighborList."""
         ids, sq, ln = self.search_batch(query, params.k, params.probe_depth)
@@ -309,6 +319,14 @@ class MulticurvesIndex:
                                    _ptr(cnt), _stream(None, q)))
         return [np.sort(out[i, :cnt[i]]) for i in range(nq)]
 
+    def candidate_counts(self, queries, probe_depth: int) -> np.ndarray:
+        """|candidate_union| per query (unique candidates U_q)."""
+        q = _u8_2d(queries, self.scheme.d_full)
+        cnt = np.zeros(q.shape[0], np.uint32)
+        check(lib().hcg_candidates(self._h, _ptr(q), q.shape[0], probe_depth, None, 0, _ptr(cnt),
+                                   _stream(None, q)))
+        return cnt
+
     def candidate_union(self, query, depth: int) -> np.ndarray:
         """multicurves.hpp:87-89 (sorted ascending)."""
         return self.candidates(query, depth)[0]
@@ -325,12 +343,15 @@ class MulticurvesIndex:
         return ids, sq, ln
 
 
-def merge_packed(packed, k: int, device: int = 0, stream=None):
+def merge_packed(packed, k: int, device: int = 0, stream=None, out=None):
     """Hypershard aggregate: packed [parts, nq, k] -> top-k."""
     parts, nq = int(packed.shape[0]), int(packed.shape[1])
-    ids = _empty_like_kind(packed, (nq, k), np.uint64)
-    sq = _empty_like_kind(packed, (nq, k), np.uint32)
-    ln = _empty_like_kind(packed, (nq,), np.uint32)
+    if out is None:
+        ids = _empty_like_kind(packed, (nq, k), np.uint64)
+        sq = _empty_like_kind(packed, (nq, k), np.uint32)
+        ln = _empty_like_kind(packed, (nq,), np.uint32)
+    else:
+        ids, sq, ln = out
     check(lib().hcg_merge_packed(_ptr(packed), parts, nq, k, _ptr(ids), _ptr(sq), _ptr(ln), device,
                                  _stream(stream, packed)))
     return ids, sq, ln
