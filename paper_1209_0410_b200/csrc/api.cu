@@ -5,6 +5,8 @@
 // turns the codes back into the reference's exceptions).
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -62,11 +64,27 @@ namespace {
         if (r_ != HCG_OK) return r_;        \
     } while (0)
 
+// Keep stream-ordered scratch cached in the device's default pool: with the
+// default release threshold (0) every synchronise hands the memory back and
+// the next call re-maps it, which dominates small-batch latency.
+void keep_pool(int dev) {
+    static bool done[64] = {};
+    if (dev < 0 || dev >= 64 || done[dev]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    cudaGetLastError();
+    done[dev] = true;
+}
+
 struct DeviceGuard {
     int prev = -1;
     explicit DeviceGuard(int dev) {
         if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
         if (prev != dev) cudaSetDevice(dev);
+        keep_pool(dev);
     }
     ~DeviceGuard() {
         int cur = -1;
@@ -362,12 +380,28 @@ RefineArgs refine_args(const hcg_index* ix, const uint8_t* dq, uint32_t nq, uint
     return a;
 }
 
-hcg_status run_refine(const hcg_index* ix, Scratch& sc, const RefineArgs& a) {
+hcg_status run_refine(const hcg_index* ix, Scratch& sc, const RefineArgs& a_in) {
+    RefineArgs a = a_in;
+    static unsigned long long* prof = nullptr;
+    if (getenv("HCG_REFINE_PROFILE")) {  // phase counters for tools/tune_refine.py
+        if (!prof) cudaMalloc(&prof, 64);
+        a.prof = prof;
+    }
     size_t need = 0;
     HCG_TRY(launch_refine(a, nullptr, &need, ix->device, sc.st));
     void* scratch = need ? sc.alloc<uint8_t>(need) : reinterpret_cast<void*>(1);
     if (!scratch) return set_error(HCG_ENOMEM, "refine scratch");
-    return launch_refine(a, need ? scratch : reinterpret_cast<void*>(1), &need, ix->device, sc.st);
+    if (a.prof) cudaMemsetAsync(a.prof, 0, 64, sc.st);
+    const hcg_status rc = launch_refine(a, need ? scratch : reinterpret_cast<void*>(1), &need, ix->device, sc.st);
+    if (a.prof && rc == HCG_OK) {
+        unsigned long long h[4];
+        cudaMemcpyAsync(h, a.prof, 32, cudaMemcpyDeviceToHost, sc.st);
+        cudaStreamSynchronize(sc.st);
+        const double tot = double(h[0] + h[1] + h[2] + h[3]);
+        fprintf(stderr, "[hcg refine phases, warp-cycles] wait+barrier %.1f%%  dedup %.1f%%  gather %.1f%%  merge-barrier %.1f%%  (%.3g total)\n",
+                100 * h[0] / tot, 100 * h[1] / tot, 100 * h[2] / tot, 100 * h[3] / tot, tot);
+    }
+    return rc;
 }
 
 // Copy a host-side vector to a user buffer that may be host or device memory.

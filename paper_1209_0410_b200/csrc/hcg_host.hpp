@@ -65,6 +65,7 @@ struct RefineArgs {
     uint32_t* out_len;     // kOutIds: len; kOutCandidates: count
     uint64_t* out_packed;  // kOutPacked
     uint32_t cap;          // kOutCandidates
+    unsigned long long* prof;  // optional phase-cycle counters (tools/tune_refine.py)
 };
 // Scratch bytes the refine launch needs (global hash tables when the table
 // does not fit in shared memory); query with scratch == nullptr first.

@@ -18,11 +18,18 @@
 //   K5  k_brute  : exact kNN over all rows (brute_force_knn, vecio.cpp:115-122)
 //                  for recall ground truth; chunked, then merged by K4.
 #include <algorithm>
+#include <cstdlib>
 
 #include "hcg_internal.cuh"
 #include "hcg_host.hpp"
 
 namespace hcg {
+
+#define HCG_RET_IF(x)                   \
+    do {                                \
+        const hcg_status r_ = (x);      \
+        if (r_ != HCG_OK) return r_;    \
+    } while (0)
 
 __device__ __forceinline__ unsigned lanemask_lt_s() {
     unsigned m;
@@ -143,6 +150,7 @@ hcg_status launch_locate(const LocateArgs& a, int dmax, int wsmax, cudaStream_t 
 
 // ----------------------------------------------------------------- K3b ----
 constexpr int kRefineThreads = 256;
+constexpr int kRefineMaxSmem = 200 * 1024;
 
 template <int R>
 __device__ __forceinline__ void write_result(const RefineArgs& a, uint32_t q, const WarpTopK<R>& fin, int lane,
@@ -166,17 +174,314 @@ __device__ __forceinline__ void write_result(const RefineArgs& a, uint32_t q, co
     if (lane == 0 && a.mode == kOutIds) a.out_len[q] = U < a.k ? U : a.k;
 }
 
-template <int R, int CR>
-__global__ void __launch_bounds__(kRefineThreads) k_refine(RefineArgs a, uint32_t table_bits, uint32_t* gtables) {
-    constexpr int KCAP = 32 * R;
+__device__ __forceinline__ void cp_async4(void* smem_dst, const void* src) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// Gather U list entries per group of 8 lanes (one 128-B row per lane group,
+// 16 B per lane and chunk), exact squared L2 with vabsdiff4 + dp4a, a
+// reduce-scatter over the group so lane l8 holds row h*8+l8, and the per-warp
+// top-k.  A warp covers list[e0 .. e0 + 4U).
+template <int R, int CR, int U>
+__device__ __forceinline__ void gather_rows(const RefineArgs& a, const uint32_t* list, uint32_t e0, uint32_t n,
+                                            const uint4 (&qv)[CR], uint32_t chunks, int lane, WarpTopK<R>& tk) {
+    const int l8 = lane & 7, grp = lane >> 3;
+    const uint32_t g0 = e0 + grp * U;
+    uint32_t sl[U];
+#pragma unroll
+    for (int r = 0; r < U; ++r) sl[r] = g0 + r < n ? list[g0 + r] : kEmpty;
+    uint4 v[U][CR];
+#pragma unroll
+    for (int r = 0; r < U; ++r) {
+#pragma unroll
+        for (int t = 0; t < CR; ++t) {
+            const uint32_t ch = l8 + 8 * t;
+            v[r][t] = (sl[r] != kEmpty && ch < chunks) ? ldg_stream(a.rows + uint64_t(sl[r]) * a.pitch + ch * 16)
+                                                       : make_uint4(0, 0, 0, 0);
+        }
+    }
+#pragma unroll
+    for (int h = 0; h < U / 8; ++h) {
+        uint32_t acc[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            acc[r] = 0;
+#pragma unroll
+            for (int t = 0; t < CR; ++t) acc[r] = sad2_16(v[h * 8 + r][t], qv[t], acc[r]);
+        }
+        const bool b2 = l8 & 4, b1 = l8 & 2, b0 = l8 & 1;
+        uint32_t s4[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const uint32_t send = b2 ? acc[i] : acc[i + 4];
+            const uint32_t keep = b2 ? acc[i + 4] : acc[i];
+            s4[i] = keep + __shfl_xor_sync(kFull, send, 4);
+        }
+        uint32_t s2[2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const uint32_t send = b1 ? s4[i] : s4[i + 2];
+            const uint32_t keep = b1 ? s4[i + 2] : s4[i];
+            s2[i] = keep + __shfl_xor_sync(kFull, send, 2);
+        }
+        const uint32_t S = (b0 ? s2[1] : s2[0]) + __shfl_xor_sync(kFull, b0 ? s2[0] : s2[1], 1);
+        const uint32_t e = g0 + h * 8 + l8;
+        const uint32_t me = e < n ? list[e] : kEmpty;
+        tk.offer(me != kEmpty ? ((uint64_t(S) << 32) | me) : kNone, lane);
+    }
+}
+
+// Exclusive scan of one value per thread over a 256-thread block (ends with a barrier).
+__device__ __forceinline__ uint32_t block_excl_scan256_u(uint32_t v, uint32_t* wsum) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t inc = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t t = __shfl_up_sync(kFull, inc, off);
+        if (lane >= off) inc += t;
+    }
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    uint32_t before = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) before += w < warp ? wsum[w] : 0u;
+    __syncthreads();
+    return before + inc - v;
+}
+
+// ------------------------------------------------------------- K3b ----
+// Candidate union (multicurves.hpp:87-89): one CTA per query (persistent).
+// The C windows' ids are read (coalesced) into shared memory, then
+// deduplicated without atomics: in round r every pending position i stores
+// the tag (r, i) into slot h_r(id[i]) of a u16 table; after a barrier it
+// reads the slot back -- its own tag: first copy of the id, appended to the
+// query's unique list in HBM; the tag of another copy of the same id:
+// dropped; a different id: collision, retried with the next hash.  All copies
+// of an id hit the same slot in every round, so they resolve together; the
+// rare ids still pending after kUnionRounds keep their lowest position.
+constexpr int kUnionRounds = 6;
+constexpr uint32_t kUnionMaxT = 32 * 256;  // one u32 pending mask per thread
+
+__global__ void __launch_bounds__(kRefineThreads) k_union(RefineArgs a, uint32_t* __restrict__ lists,
+                                                          uint32_t* __restrict__ counts, uint32_t tb) {
     extern __shared__ __align__(16) unsigned char smem[];
+    const uint32_t T = a.C * a.take;
+    const uint32_t** sptr = reinterpret_cast<const uint32_t**>(smem);
+    uint32_t* sbeg = reinterpret_cast<uint32_t*>(sptr + a.C);  // [2][C]
+    uint32_t* wsum = sbeg + 2 * a.C;                            // [8] scan scratch
+    uint32_t* ids2 = wsum + 8;                                  // [2][T], cp.async double buffer
+    uint32_t* tab = ids2 + 2 * T;                               // [1 << tb] tags
+    const int tid = threadIdx.x;
+    const uint32_t take = a.take;
+    const uint32_t jn = (T + kRefineThreads - 1) / kRefineThreads;  // <= 32
+    const uint32_t shift = 32 - tb;
+
+    auto stage = [&](int buf) {
+        const uint32_t* beg = sbeg + buf * a.C;
+        uint32_t* dst = ids2 + buf * T;
+        uint32_t c = tid / take, p = tid - c * take;  // walk (curve, position) without dividing
+        for (uint32_t i = tid; i < T; i += kRefineThreads) {
+            cp_async4(dst + i, sptr[c] + beg[c] + p);
+            p += kRefineThreads;
+            while (p >= take && c + 1 < a.C) {
+                p -= take;
+                ++c;
+            }
+        }
+    };
+
+    for (uint32_t c = tid; c < a.C; c += kRefineThreads) sptr[c] = a.slots[c];
+    uint32_t q = blockIdx.x;
+    if (q < a.nq)
+        for (uint32_t c = tid; c < a.C; c += kRefineThreads) sbeg[c] = a.begins[uint64_t(q) * a.C + c];
+    __syncthreads();
+    if (q < a.nq) stage(0);
+    cp_async_commit();
+
+    for (uint32_t it = 0; q < a.nq; q += gridDim.x, ++it) {
+        const int cur = it & 1;
+        const uint32_t qn = q + gridDim.x;
+        if (qn < a.nq)
+            for (uint32_t c = tid; c < a.C; c += kRefineThreads)
+                sbeg[(cur ^ 1) * a.C + c] = a.begins[uint64_t(qn) * a.C + c];
+        cp_async_wait_all();
+        __syncthreads();  // ids of q landed; next begins visible
+        if (qn < a.nq) stage(cur ^ 1);  // prefetch the next query while deduping this one
+        cp_async_commit();
+        const uint32_t* idbuf = ids2 + cur * T;
+
+        // positions of this thread: i = tid + 256 j, j < jn (bit j of the masks)
+        uint32_t pending = 0;
+        for (uint32_t j = 0; j < jn; ++j)
+            if (tid + j * kRefineThreads < T) pending |= 1u << j;
+        uint32_t keep = 0;
+#pragma unroll 1
+        for (int r = 0; r < kUnionRounds; ++r) {
+            const uint32_t mul = 0x9E3779B1u + 0x7F4A7C16u * uint32_t(r);  // odd multipliers
+            const uint32_t tagr = uint32_t(r + 1) << 16;
+            for (uint32_t pm = pending; pm; pm &= pm - 1) {
+                const uint32_t i = tid + uint32_t(__ffs(pm) - 1) * kRefineThreads;
+                tab[(idbuf[i] * (mul | 1u)) >> shift] = tagr | i;
+            }
+            __syncthreads();
+            for (uint32_t pm = pending; pm; pm &= pm - 1) {
+                const uint32_t j = __ffs(pm) - 1;
+                const uint32_t i = tid + j * kRefineThreads;
+                const uint32_t s = idbuf[i];
+                const uint32_t o = tab[(s * (mul | 1u)) >> shift];
+                if (o == (tagr | i)) {
+                    keep |= 1u << j;
+                    pending &= ~(1u << j);
+                } else if (idbuf[o & 0xFFFFu] == s) {
+                    pending &= ~(1u << j);
+                }
+            }
+            if (!__syncthreads_or(pending != 0)) break;
+        }
+        // Leftovers (rare): all copies of such an id are still pending, so the
+        // copy at the lowest position is the first one.
+        for (uint32_t pm = pending; pm; pm &= pm - 1) {
+            const uint32_t j = __ffs(pm) - 1;
+            const uint32_t i = tid + j * kRefineThreads;
+            const uint32_t s = idbuf[i];
+            bool first = true;
+            for (uint32_t i2 = 0; i2 < i; ++i2)
+                if (idbuf[i2] == s) {
+                    first = false;
+                    break;
+                }
+            if (first) keep |= 1u << j;
+        }
+        // Compact: block exclusive scan of the kept counts.
+        const uint32_t mine = __popc(keep);
+        const uint32_t off = block_excl_scan256_u(mine, wsum);
+        uint32_t* out = lists + uint64_t(q) * T + off;
+        uint32_t w = 0;
+        for (uint32_t pm = keep; pm; pm &= pm - 1) out[w++] = idbuf[tid + uint32_t(__ffs(pm) - 1) * kRefineThreads];
+        if (tid == kRefineThreads - 1) counts[q] = off + mine;
+    }
+    cp_async_wait_all();
+}
+
+// ------------------------------------------------------------- K3c ----
+// Gather + exact L2 + top-k: one WARP per query (persistent), no shared
+// memory, no barriers.  Each pass covers 32 list entries: the 4 groups of 8
+// lanes own 8 rows each (one 16-B chunk per lane and row, 8 LDG.128 in flight
+// per lane); the next pass's slots are prefetched while the rows load.  The
+// reduce-scatter leaves row (8*grp + l8)'s squared distance in lane l8 of
+// group grp, which offers (sqdist << 32 | slot) to the warp top-k.
+template <int R, int CR, int MINB>
+__global__ void __launch_bounds__(kRefineThreads, MINB) k_gather(RefineArgs a, const uint32_t* __restrict__ lists,
+                                                                 const uint32_t* __restrict__ counts,
+                                                                 uint32_t lstride) {
+    const int lane = threadIdx.x & 31, l8 = lane & 7, grp = lane >> 3;
+    const uint32_t chunks = a.pitch >> 4;
+    const uint32_t nw = gridDim.x * (kRefineThreads / 32);
+    for (uint32_t q = (blockIdx.x * kRefineThreads + threadIdx.x) >> 5; q < a.nq; q += nw) {
+        const uint32_t n = counts[q];
+        const uint32_t* list = lists + uint64_t(q) * lstride;
+        uint4 qv[CR];
+        const uint8_t* qrow = a.queries + uint64_t(q) * a.pitch;
+#pragma unroll
+        for (int t = 0; t < CR; ++t) {
+            const uint32_t ch = l8 + 8 * t;
+            qv[t] = ch < chunks ? *reinterpret_cast<const uint4*>(qrow + ch * 16) : make_uint4(0, 0, 0, 0);
+        }
+        WarpTopK<R> tk;
+        tk.init(int(a.k));
+        uint32_t nx[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const uint32_t e = grp * 8 + r;
+            nx[r] = e < n ? __ldg(list + e) : kEmpty;
+        }
+        for (uint32_t base = 0; base < n; base += 32) {
+            uint32_t sl[8];
+#pragma unroll
+            for (int r = 0; r < 8; ++r) sl[r] = nx[r];
+            uint4 v[8][CR];
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+#pragma unroll
+                for (int t = 0; t < CR; ++t) {
+                    const uint32_t ch = l8 + 8 * t;
+                    v[r][t] = (sl[r] != kEmpty && ch < chunks)
+                                  ? ldg_stream(a.rows + uint64_t(sl[r]) * a.pitch + ch * 16)
+                                  : make_uint4(0, 0, 0, 0);
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                const uint32_t e = base + 32 + grp * 8 + r;
+                nx[r] = e < n ? __ldg(list + e) : kEmpty;
+            }
+            uint32_t acc[8];
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                acc[r] = 0;
+#pragma unroll
+                for (int t = 0; t < CR; ++t) acc[r] = sad2_16(v[r][t], qv[t], acc[r]);
+            }
+            const bool b2 = l8 & 4, b1 = l8 & 2, b0 = l8 & 1;
+            uint32_t s4[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const uint32_t send = b2 ? acc[i] : acc[i + 4];
+                const uint32_t keep = b2 ? acc[i + 4] : acc[i];
+                s4[i] = keep + __shfl_xor_sync(kFull, send, 4);
+            }
+            uint32_t s2[2];
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const uint32_t send = b1 ? s4[i] : s4[i + 2];
+                const uint32_t keep = b1 ? s4[i + 2] : s4[i];
+                s2[i] = keep + __shfl_xor_sync(kFull, send, 2);
+            }
+            const uint32_t S = (b0 ? s2[1] : s2[0]) + __shfl_xor_sync(kFull, b0 ? s2[0] : s2[1], 1);
+            uint32_t me = sl[0];
+#pragma unroll
+            for (int r = 1; r < 8; ++r)
+                if (r == l8) me = sl[r];
+            tk.offer(me != kEmpty ? ((uint64_t(S) << 32) | me) : kNone, lane);
+        }
+        write_result<R>(a, q, tk, lane, n);
+    }
+}
+
+// Candidate-union tap: unique slots -> ids.
+__global__ void k_lists_to_ids(RefineArgs a, const uint32_t* __restrict__ lists, const uint32_t* __restrict__ counts,
+                               uint32_t lstride) {
+    const uint32_t q = blockIdx.x;
+    if (q >= a.nq) return;
+    const uint32_t n = counts[q];
+    const uint32_t lim = n < a.cap ? n : a.cap;
+    if (a.out_ids)
+        for (uint32_t i = threadIdx.x; i < lim; i += blockDim.x)
+            a.out_ids[uint64_t(q) * a.cap + i] = a.id_base + uint64_t(lists[uint64_t(q) * lstride + i]) * a.id_stride;
+    if (threadIdx.x == 0) a.out_len[q] = n;
+}
+
+// K3b general fallback (also the candidate_union tap): CTA-wide dedup of the
+// window ids (read straight from HBM) into a CAS hash set -- in shared memory
+// or, for very large curves x depth, in a per-CTA global scratch table -- then
+// the same gather/score/top-k.
+template <int R, int CR>
+__global__ void __launch_bounds__(kRefineThreads) k_refine_cas(RefineArgs a, uint32_t table_bits,
+                                                               uint32_t* gtables) {
+    constexpr int KCAP = 32 * R;
+    constexpr int kWarps = kRefineThreads / 32;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const uint32_t T = a.C * a.take;
     uint64_t* mbuf = reinterpret_cast<uint64_t*>(smem);
-    uint32_t* sbeg = reinterpret_cast<uint32_t*>(mbuf + 8 * KCAP);
+    uint32_t* sbeg = reinterpret_cast<uint32_t*>(mbuf + kWarps * KCAP);
     uint32_t* scount = sbeg + a.C;
     uint32_t* list = scount + 4;
-    uint32_t* table = gtables ? gtables + (uint64_t(blockIdx.x) << table_bits) : list + uint64_t(a.C) * a.take;
+    uint32_t* table = gtables ? gtables + (uint64_t(blockIdx.x) << table_bits) : list + T;
     const uint32_t tsize = 1u << table_bits, tmask = tsize - 1;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, l8 = lane & 7, grp = lane >> 3;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t chunks = a.pitch >> 4;
     const unsigned lt = lanemask_lt_s();
 
@@ -188,12 +493,10 @@ __global__ void __launch_bounds__(kRefineThreads) k_refine(RefineArgs a, uint32_
         const uint8_t* qrow = a.queries + uint64_t(q) * a.pitch;
 #pragma unroll
         for (int t = 0; t < CR; ++t) {
-            const uint32_t ch = l8 + 8 * t;
+            const uint32_t ch = (lane & 7) + 8 * t;
             qv[t] = ch < chunks ? *reinterpret_cast<const uint4*>(qrow + ch * 16) : make_uint4(0, 0, 0, 0);
         }
         __syncthreads();
-
-        // -- candidate union: windows of every curve, dedup in the hash set.
         for (uint32_t c = 0; c < a.C; ++c) {
             const uint32_t* sl = a.slots[c] + sbeg[c];
             for (uint32_t p0 = warp * 32; p0 < a.take; p0 += kRefineThreads) {
@@ -224,65 +527,20 @@ __global__ void __launch_bounds__(kRefineThreads) k_refine(RefineArgs a, uint32_
             }
         }
         __syncthreads();
-        const uint32_t U = *scount;
-
+        const uint32_t Ucnt = *scount;
         if (a.mode == kOutCandidates) {
-            const uint32_t lim = U < a.cap ? U : a.cap;
+            const uint32_t lim = Ucnt < a.cap ? Ucnt : a.cap;
             if (a.out_ids)
                 for (uint32_t i = tid; i < lim; i += kRefineThreads)
                     a.out_ids[uint64_t(q) * a.cap + i] = a.id_base + uint64_t(list[i]) * a.id_stride;
-            if (tid == 0) a.out_len[q] = U;
+            if (tid == 0) a.out_len[q] = Ucnt;
             __syncthreads();
             continue;
         }
-
-        // -- gather + exact distance + per-warp top-k.
         WarpTopK<R> tk;
         tk.init(int(a.k));
-        for (uint32_t base = warp * 32; base < U; base += kRefineThreads) {
-            const uint32_t e0 = base + grp * 8;
-            uint32_t sl[8];
-#pragma unroll
-            for (int r = 0; r < 8; ++r) sl[r] = e0 + r < U ? list[e0 + r] : kEmpty;
-            uint4 v[8][CR];
-#pragma unroll
-            for (int r = 0; r < 8; ++r) {
-#pragma unroll
-                for (int t = 0; t < CR; ++t) {
-                    const uint32_t ch = l8 + 8 * t;
-                    v[r][t] = (sl[r] != kEmpty && ch < chunks)
-                                  ? ldg_stream(a.rows + uint64_t(sl[r]) * a.pitch + ch * 16)
-                                  : make_uint4(0, 0, 0, 0);
-                }
-            }
-            uint32_t acc[8];
-#pragma unroll
-            for (int r = 0; r < 8; ++r) {
-                acc[r] = 0;
-#pragma unroll
-                for (int t = 0; t < CR; ++t) acc[r] = sad2_16(v[r][t], qv[t], acc[r]);
-            }
-            // Reduce-scatter over the 8 lanes of the group: lane l8 ends with row l8.
-            const bool b2 = l8 & 4, b1 = l8 & 2, b0 = l8 & 1;
-            uint32_t s4[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const uint32_t send = b2 ? acc[i] : acc[i + 4];
-                const uint32_t keep = b2 ? acc[i + 4] : acc[i];
-                s4[i] = keep + __shfl_xor_sync(kFull, send, 4);
-            }
-            uint32_t s2[2];
-#pragma unroll
-            for (int i = 0; i < 2; ++i) {
-                const uint32_t send = b1 ? s4[i] : s4[i + 2];
-                const uint32_t keep = b1 ? s4[i + 2] : s4[i];
-                s2[i] = keep + __shfl_xor_sync(kFull, send, 2);
-            }
-            const uint32_t S = (b0 ? s2[1] : s2[0]) + __shfl_xor_sync(kFull, b0 ? s2[0] : s2[1], 1);
-            const uint32_t mine = e0 + l8 < U ? list[e0 + l8] : kEmpty;
-            const uint64_t cand = mine != kEmpty ? ((uint64_t(S) << 32) | mine) : kNone;
-            tk.offer(cand, lane);
-        }
+        for (uint32_t base = warp * 32; base < Ucnt; base += kRefineThreads)
+            gather_rows<R, CR, 8>(a, list, base, Ucnt, qv, chunks, lane, tk);
 #pragma unroll
         for (int r = 0; r < R; ++r) mbuf[warp * KCAP + lane * R + r] = tk.a[r];
         __syncthreads();
@@ -290,9 +548,9 @@ __global__ void __launch_bounds__(kRefineThreads) k_refine(RefineArgs a, uint32_
             WarpTopK<R> fin;
             fin.init(int(a.k));
             const uint32_t kr = (a.k + 31) & ~31u;
-            for (int w = 0; w < 8; ++w)
+            for (int w = 0; w < kWarps; ++w)
                 for (uint32_t i = 0; i < kr; i += 32) fin.offer(mbuf[w * KCAP + i + lane], lane);
-            write_result<R>(a, q, fin, lane, U);
+            write_result<R>(a, q, fin, lane, Ucnt);
         }
         __syncthreads();
     }
@@ -301,56 +559,104 @@ __global__ void __launch_bounds__(kRefineThreads) k_refine(RefineArgs a, uint32_
 namespace {
 int r_bucket(uint32_t k) { return k <= 32 ? 1 : k <= 64 ? 2 : k <= 128 ? 4 : 8; }
 
-template <int R, int CR>
-hcg_status refine_launch(const RefineArgs& a, uint32_t table_bits, bool gtab, void* scratch, size_t* scratch_bytes,
-                         int device, cudaStream_t st) {
-    auto kern = k_refine<R, CR>;
-    const size_t fixed = size_t(8) * 32 * R * 8 + size_t(a.C) * 4 + 16 + size_t(a.C) * a.take * 4;
-    const size_t smem = fixed + (gtab ? 0 : (size_t(4) << table_bits));
-    int sms = 148;
+template <class K>
+hcg_status opt_in_smem(K kern, int device, bool* configured) {
+    if (device < 64 && !configured[device]) {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kRefineMaxSmem) != cudaSuccess ||
+            cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100) != cudaSuccess)
+            return set_error(HCG_ECUDA, "refine: cannot opt in to dynamic shared memory");
+        configured[device] = true;
+    }
+    return HCG_OK;
+}
+
+uint32_t persistent_grid(const void* kern, size_t smem, int device, uint32_t nq) {
+    int sms = 148, per_sm = 1;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess)
-        return set_error(HCG_ECAPACITY, "refine shared memory request too large");
-    int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRefineThreads, smem);
-    if (per_sm < 1) return set_error(HCG_ECAPACITY, "refine kernel does not fit on an SM");
-    uint32_t grid = a.nq;
-    if (gtab) grid = std::min<uint32_t>(a.nq, uint32_t(sms * per_sm));
-    const size_t need = gtab ? (size_t(grid) << table_bits) * 4 : 0;
+    return std::min<uint32_t>(nq, uint32_t(sms * std::max(per_sm, 1)));
+}
+
+template <int R, int CR>
+hcg_status cas_launch(const RefineArgs& a, uint32_t tb, bool gtab, void* scratch, size_t* scratch_bytes, int device,
+                      cudaStream_t st) {
+    auto kern = k_refine_cas<R, CR>;
+    const uint64_t T = uint64_t(a.C) * a.take;
+    const size_t smem = size_t(8) * 32 * R * 8 + size_t(a.C) * 4 + 16 + T * 4 + (gtab ? 0 : (size_t(4) << tb));
+    if (smem > size_t(kRefineMaxSmem)) return set_error(HCG_ECAPACITY, "curves x depth exceeds the per-query candidate capacity");
+    static bool configured[64] = {};
+    HCG_RET_IF(opt_in_smem(kern, device, configured));
+    const uint32_t grid = gtab ? persistent_grid(reinterpret_cast<const void*>(kern), smem, device, a.nq) : a.nq;
+    const size_t need = gtab ? (size_t(grid) << tb) * 4 : 0;
     if (!scratch) {
         *scratch_bytes = need;
         return HCG_OK;
     }
-    if (a.nq == 0) return HCG_OK;
-    kern<<<grid, kRefineThreads, smem, st>>>(a, table_bits, gtab ? static_cast<uint32_t*>(scratch) : nullptr);
-    return check_launch("k_refine");
+    kern<<<grid, kRefineThreads, smem, st>>>(a, tb, gtab ? static_cast<uint32_t*>(scratch) : nullptr);
+    return check_launch("k_refine_cas");
+}
+
+size_t union_smem_bytes(uint32_t C, uint32_t T, uint32_t tb) {
+    return size_t(C) * 16 + 32 + size_t(T) * 8 + (size_t(4) << tb);
+}
+
+template <int R, int CR>
+hcg_status refine_dispatch(const RefineArgs& a, void* scratch, size_t* scratch_bytes, int device, cudaStream_t st) {
+    const uint32_t T = a.C * a.take;
+    uint32_t tb = 5;
+    while ((uint64_t(1) << tb) * 7 < uint64_t(T) * 10) ++tb;
+    if (T <= kUnionMaxT && union_smem_bytes(a.C, T, tb) <= 160 * 1024) {
+        // union -> lists in HBM -> warp-per-query gather
+        const size_t lists_bytes = (size_t(a.nq) * T * 4 + 255) & ~size_t(255);
+        if (!scratch) {
+            *scratch_bytes = lists_bytes + size_t(a.nq) * 4 + 256;
+            return HCG_OK;
+        }
+        if (a.nq == 0) return HCG_OK;
+        uint32_t* lists = static_cast<uint32_t*>(scratch);
+        uint32_t* counts = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(scratch) + lists_bytes);
+        const size_t usmem = union_smem_bytes(a.C, T, tb);
+        static bool cfg_u[64] = {};
+        HCG_RET_IF(opt_in_smem(k_union, device, cfg_u));
+        const uint32_t ugrid = persistent_grid(reinterpret_cast<const void*>(k_union), usmem, device, a.nq);
+        k_union<<<ugrid, kRefineThreads, usmem, st>>>(a, lists, counts, tb);
+        HCG_RET_IF(check_launch("k_union"));
+        if (a.mode == kOutCandidates) {
+            k_lists_to_ids<<<a.nq, 128, 0, st>>>(a, lists, counts, T);
+            return check_launch("k_lists_to_ids");
+        }
+        constexpr int MINB = R <= 2 ? 4 : 2;
+        auto kern = k_gather<R, CR, MINB>;
+        int sms = 148, per_sm = 1;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRefineThreads, 0);
+        const uint32_t warps_needed = a.nq;
+        const uint32_t blocks = std::min<uint32_t>((warps_needed + 7) / 8, uint32_t(sms * std::max(per_sm, 1)));
+        kern<<<blocks, kRefineThreads, 0, st>>>(a, lists, counts, T);
+        return check_launch("k_gather");
+    }
+    const bool gtab = size_t(T) * 4 + (size_t(4) << tb) > 160 * 1024;
+    if (tb > 30) return set_error(HCG_ECAPACITY, "candidate set too large");
+    if (scratch && a.nq == 0) return HCG_OK;
+    return cas_launch<R, CR>(a, tb, gtab, scratch, scratch_bytes, device, st);
 }
 
 template <int R>
-hcg_status refine_cr(const RefineArgs& a, uint32_t tb, bool gtab, void* scratch, size_t* sb, int device,
-                     cudaStream_t st) {
+hcg_status refine_cr(const RefineArgs& a, void* scratch, size_t* sb, int device, cudaStream_t st) {
     const uint32_t chunks = a.pitch / 16;
-    if (chunks <= 8) return refine_launch<R, 1>(a, tb, gtab, scratch, sb, device, st);
-    if (chunks <= 16) return refine_launch<R, 2>(a, tb, gtab, scratch, sb, device, st);
-    return refine_launch<R, 4>(a, tb, gtab, scratch, sb, device, st);
+    if (chunks <= 8) return refine_dispatch<R, 1>(a, scratch, sb, device, st);
+    if (chunks <= 16) return refine_dispatch<R, 2>(a, scratch, sb, device, st);
+    return refine_dispatch<R, 4>(a, scratch, sb, device, st);
 }
 }  // namespace
 
 hcg_status launch_refine(const RefineArgs& a, void* scratch, size_t* scratch_bytes, int device, cudaStream_t st) {
     if (scratch_bytes) *scratch_bytes = 0;
-    const uint64_t T = uint64_t(a.C) * a.take;
-    // Hash set at <= 0.7 load factor, at least 32 slots.
-    uint32_t tb = 5;
-    while ((uint64_t(1) << tb) * 7 < T * 10) ++tb;
-    if (tb > 30) return set_error(HCG_ECAPACITY, "candidate set too large");
-    const size_t list_bytes = T * 4;
-    if (list_bytes > 150 * 1024) return set_error(HCG_ECAPACITY, "curves x depth exceeds the per-query candidate capacity");
-    const bool gtab = list_bytes + (size_t(4) << tb) > 160 * 1024;
     switch (r_bucket(a.k)) {
-        case 1: return refine_cr<1>(a, tb, gtab, scratch, scratch_bytes, device, st);
-        case 2: return refine_cr<2>(a, tb, gtab, scratch, scratch_bytes, device, st);
-        case 4: return refine_cr<4>(a, tb, gtab, scratch, scratch_bytes, device, st);
-        default: return refine_cr<8>(a, tb, gtab, scratch, scratch_bytes, device, st);
+        case 1: return refine_cr<1>(a, scratch, scratch_bytes, device, st);
+        case 2: return refine_cr<2>(a, scratch, scratch_bytes, device, st);
+        case 4: return refine_cr<4>(a, scratch, scratch_bytes, device, st);
+        default: return refine_cr<8>(a, scratch, scratch_bytes, device, st);
     }
 }
 
