@@ -265,8 +265,20 @@ __device__ __forceinline__ uint32_t block_excl_scan256_u(uint32_t v, uint32_t* w
 constexpr int kUnionRounds = 6;
 constexpr uint32_t kUnionMaxT = 32 * 256;  // one u32 pending mask per thread
 
-__global__ void __launch_bounds__(kRefineThreads) k_union(RefineArgs a, uint32_t* __restrict__ lists,
-                                                          uint32_t* __restrict__ counts, uint32_t tb) {
+__device__ __forceinline__ void publish(uint32_t* flag, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t acquire(const uint32_t* flag) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    return v;
+}
+
+// One CTA deduplicating queries q0, q0 + qstep, ...; with `flags`, each
+// finished list is published with a release store of `epoch` to flags[q].
+__device__ __forceinline__ void union_cta(const RefineArgs& a, uint32_t* __restrict__ lists,
+                                          uint32_t* __restrict__ counts, uint32_t lstride, uint32_t tb,
+                                          uint32_t q0, uint32_t qstep, uint32_t* flags, uint32_t epoch) {
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t T = a.C * a.take;
     const uint32_t** sptr = reinterpret_cast<const uint32_t**>(smem);
@@ -282,28 +294,23 @@ __global__ void __launch_bounds__(kRefineThreads) k_union(RefineArgs a, uint32_t
     auto stage = [&](int buf) {
         const uint32_t* beg = sbeg + buf * a.C;
         uint32_t* dst = ids2 + buf * T;
-        uint32_t c = tid / take, p = tid - c * take;  // walk (curve, position) without dividing
-        for (uint32_t i = tid; i < T; i += kRefineThreads) {
-            cp_async4(dst + i, sptr[c] + beg[c] + p);
-            p += kRefineThreads;
-            while (p >= take && c + 1 < a.C) {
-                p -= take;
-                ++c;
-            }
+        for (uint32_t c = 0; c < a.C; ++c) {
+            const uint32_t* src = sptr[c] + beg[c];
+            for (uint32_t p = tid; p < take; p += kRefineThreads) cp_async4(dst + c * take + p, src + p);
         }
     };
 
     for (uint32_t c = tid; c < a.C; c += kRefineThreads) sptr[c] = a.slots[c];
-    uint32_t q = blockIdx.x;
+    uint32_t q = q0;
     if (q < a.nq)
         for (uint32_t c = tid; c < a.C; c += kRefineThreads) sbeg[c] = a.begins[uint64_t(q) * a.C + c];
     __syncthreads();
     if (q < a.nq) stage(0);
     cp_async_commit();
 
-    for (uint32_t it = 0; q < a.nq; q += gridDim.x, ++it) {
+    for (uint32_t it = 0; q < a.nq; q += qstep, ++it) {
         const int cur = it & 1;
-        const uint32_t qn = q + gridDim.x;
+        const uint32_t qn = q + qstep;
         if (qn < a.nq)
             for (uint32_t c = tid; c < a.C; c += kRefineThreads)
                 sbeg[(cur ^ 1) * a.C + c] = a.begins[uint64_t(qn) * a.C + c];
@@ -358,12 +365,23 @@ __global__ void __launch_bounds__(kRefineThreads) k_union(RefineArgs a, uint32_t
         // Compact: block exclusive scan of the kept counts.
         const uint32_t mine = __popc(keep);
         const uint32_t off = block_excl_scan256_u(mine, wsum);
-        uint32_t* out = lists + uint64_t(q) * T + off;
+        uint32_t* out = lists + uint64_t(q) * lstride + off;
         uint32_t w = 0;
         for (uint32_t pm = keep; pm; pm &= pm - 1) out[w++] = idbuf[tid + uint32_t(__ffs(pm) - 1) * kRefineThreads];
         if (tid == kRefineThreads - 1) counts[q] = off + mine;
+        if (flags) {
+            __threadfence();
+            __syncthreads();
+            if (tid == 0) publish(flags + q, epoch);
+        }
     }
     cp_async_wait_all();
+}
+
+__global__ void __launch_bounds__(kRefineThreads) k_union(RefineArgs a, uint32_t* __restrict__ lists,
+                                                          uint32_t* __restrict__ counts, uint32_t lstride,
+                                                          uint32_t tb) {
+    union_cta(a, lists, counts, lstride, tb, blockIdx.x, gridDim.x, nullptr, 0);
 }
 
 // ------------------------------------------------------------- K3c ----
@@ -373,15 +391,23 @@ __global__ void __launch_bounds__(kRefineThreads) k_union(RefineArgs a, uint32_t
 // per lane); the next pass's slots are prefetched while the rows load.  The
 // reduce-scatter leaves row (8*grp + l8)'s squared distance in lane l8 of
 // group grp, which offers (sqdist << 32 | slot) to the warp top-k.
-template <int R, int CR, int MINB>
-__global__ void __launch_bounds__(kRefineThreads, MINB) k_gather(RefineArgs a, const uint32_t* __restrict__ lists,
-                                                                 const uint32_t* __restrict__ counts,
-                                                                 uint32_t lstride) {
+// One warp scoring queries q0, q0 + qstep, ...; with `flags` it first waits
+// (acquire) for the union CTA to publish the query's list.  Lists are read
+// with ld.global.cg: they are written during the same launch by other SMs.
+template <int R, int CR>
+__device__ __forceinline__ void gather_warp(const RefineArgs& a, const uint32_t* lists, const uint32_t* counts,
+                                            uint32_t lstride, uint32_t q0, uint32_t qstep, const uint32_t* flags,
+                                            uint32_t epoch) {
     const int lane = threadIdx.x & 31, l8 = lane & 7, grp = lane >> 3;
     const uint32_t chunks = a.pitch >> 4;
-    const uint32_t nw = gridDim.x * (kRefineThreads / 32);
-    for (uint32_t q = (blockIdx.x * kRefineThreads + threadIdx.x) >> 5; q < a.nq; q += nw) {
-        const uint32_t n = counts[q];
+    for (uint32_t q = q0; q < a.nq; q += qstep) {
+        if (flags) {
+            if (lane == 0)
+                while (acquire(flags + q) != epoch) __nanosleep(256);
+            __syncwarp();
+            (void)acquire(flags + q);
+        }
+        const uint32_t n = __ldcg(counts + q);
         const uint32_t* list = lists + uint64_t(q) * lstride;
         uint4 qv[CR];
         const uint8_t* qrow = a.queries + uint64_t(q) * a.pitch;
@@ -396,7 +422,7 @@ __global__ void __launch_bounds__(kRefineThreads, MINB) k_gather(RefineArgs a, c
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
             const uint32_t e = grp * 8 + r;
-            nx[r] = e < n ? __ldg(list + e) : kEmpty;
+            nx[r] = e < n ? __ldcg(list + e) : kEmpty;
         }
         for (uint32_t base = 0; base < n; base += 32) {
             uint32_t sl[8];
@@ -416,7 +442,7 @@ __global__ void __launch_bounds__(kRefineThreads, MINB) k_gather(RefineArgs a, c
 #pragma unroll
             for (int r = 0; r < 8; ++r) {
                 const uint32_t e = base + 32 + grp * 8 + r;
-                nx[r] = e < n ? __ldg(list + e) : kEmpty;
+                nx[r] = e < n ? __ldcg(list + e) : kEmpty;
             }
             uint32_t acc[8];
 #pragma unroll
@@ -451,9 +477,35 @@ __global__ void __launch_bounds__(kRefineThreads, MINB) k_gather(RefineArgs a, c
     }
 }
 
+template <int R, int CR, int MINB>
+__global__ void __launch_bounds__(kRefineThreads, MINB) k_gather(RefineArgs a, const uint32_t* __restrict__ lists,
+                                                                 const uint32_t* __restrict__ counts,
+                                                                 uint32_t lstride) {
+    gather_warp<R, CR>(a, lists, counts, lstride, (blockIdx.x * kRefineThreads + threadIdx.x) >> 5,
+                       gridDim.x * (kRefineThreads / 32), nullptr, 0);
+}
+
+// Union and gather in ONE persistent launch: CTAs [0, n_union) deduplicate
+// (union_cta) and publish per-query ready flags, the other CTAs' warps score
+// (gather_warp) as the lists become ready, so the shared-memory-bound dedup
+// overlaps the HBM-bound gather on every SM.  Union CTAs never wait, so the
+// launch makes progress even when not every CTA is resident.
+template <int R, int CR, int MINB>
+__global__ void __launch_bounds__(kRefineThreads, MINB) k_refine_fused(RefineArgs a, uint32_t* lists, uint32_t* counts,
+                                                                       uint32_t lstride, uint32_t tb, uint32_t n_union,
+                                                                       uint32_t* flags, uint32_t epoch) {
+    if (blockIdx.x < n_union) {
+        union_cta(a, lists, counts, lstride, tb, blockIdx.x, n_union, flags, epoch);
+    } else {
+        const uint32_t gw = (blockIdx.x - n_union) * (kRefineThreads / 32) + (threadIdx.x >> 5);
+        gather_warp<R, CR>(a, lists, counts, lstride, gw, (gridDim.x - n_union) * (kRefineThreads / 32), flags,
+                           epoch);
+    }
+}
+
 // Candidate-union tap: unique slots -> ids.
 __global__ void k_lists_to_ids(RefineArgs a, const uint32_t* __restrict__ lists, const uint32_t* __restrict__ counts,
-                               uint32_t lstride) {
+                               uint32_t lstride) {  // lstride: entries per query list
     const uint32_t q = blockIdx.x;
     if (q >= a.nq) return;
     const uint32_t n = counts[q];
@@ -600,39 +652,70 @@ size_t union_smem_bytes(uint32_t C, uint32_t T, uint32_t tb) {
     return size_t(C) * 16 + 32 + size_t(T) * 8 + (size_t(4) << tb);
 }
 
+int env_int(const char* name, int dflt) {
+    const char* e = getenv(name);
+    return e ? atoi(e) : dflt;
+}
+
 template <int R, int CR>
 hcg_status refine_dispatch(const RefineArgs& a, void* scratch, size_t* scratch_bytes, int device, cudaStream_t st) {
     const uint32_t T = a.C * a.take;
     uint32_t tb = 5;
     while ((uint64_t(1) << tb) * 7 < uint64_t(T) * 10) ++tb;
-    if (T <= kUnionMaxT && union_smem_bytes(a.C, T, tb) <= 160 * 1024) {
+    const int mode_env = env_int("HCG_REFINE_MODE", 1);  // 0 CTA-per-query CAS kernel, 1 union+gather
+    if (mode_env != 0 && T <= kUnionMaxT && union_smem_bytes(a.C, T, tb) <= 160 * 1024) {
         // union -> lists in HBM -> warp-per-query gather
-        const size_t lists_bytes = (size_t(a.nq) * T * 4 + 255) & ~size_t(255);
+        const uint32_t lstride = (T + 31) & ~31u;  // 128-B aligned per-query lists
+        // the union's tag table at <= ~0.35 load factor: most ids settle in round 1
+        const uint32_t utb = std::min<uint32_t>(tb + env_int("HCG_UNION_TB_EXTRA", 1), 16);
+        const size_t lists_bytes = size_t(a.nq) * lstride * 4;
+        const size_t counts_bytes = (size_t(a.nq) * 4 + 255) & ~size_t(255);
         if (!scratch) {
-            *scratch_bytes = lists_bytes + size_t(a.nq) * 4 + 256;
+            *scratch_bytes = lists_bytes + 2 * counts_bytes;
             return HCG_OK;
         }
         if (a.nq == 0) return HCG_OK;
         uint32_t* lists = static_cast<uint32_t*>(scratch);
         uint32_t* counts = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(scratch) + lists_bytes);
-        const size_t usmem = union_smem_bytes(a.C, T, tb);
-        static bool cfg_u[64] = {};
-        HCG_RET_IF(opt_in_smem(k_union, device, cfg_u));
-        const uint32_t ugrid = persistent_grid(reinterpret_cast<const void*>(k_union), usmem, device, a.nq);
-        k_union<<<ugrid, kRefineThreads, usmem, st>>>(a, lists, counts, tb);
-        HCG_RET_IF(check_launch("k_union"));
+        uint32_t* flags = counts + counts_bytes / 4;
+        const size_t usmem = union_smem_bytes(a.C, T, utb);
         if (a.mode == kOutCandidates) {
-            k_lists_to_ids<<<a.nq, 128, 0, st>>>(a, lists, counts, T);
+            static bool cfg_u[64] = {};
+            HCG_RET_IF(opt_in_smem(k_union, device, cfg_u));
+            const uint32_t ugrid = persistent_grid(reinterpret_cast<const void*>(k_union), usmem, device, a.nq);
+            k_union<<<ugrid, kRefineThreads, usmem, st>>>(a, lists, counts, lstride, utb);
+            HCG_RET_IF(check_launch("k_union"));
+            k_lists_to_ids<<<a.nq, 128, 0, st>>>(a, lists, counts, lstride);
             return check_launch("k_lists_to_ids");
         }
         constexpr int MINB = R <= 2 ? 4 : 2;
-        auto kern = k_gather<R, CR, MINB>;
-        int sms = 148, per_sm = 1;
+        int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+        if (env_int("HCG_REFINE_FUSED", 0)) {
+            auto kern = k_refine_fused<R, CR, MINB>;
+            static bool cfg_f[64] = {};
+            HCG_RET_IF(opt_in_smem(kern, device, cfg_f));
+            int per_sm = 1;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRefineThreads, usmem);
+            per_sm = std::max(per_sm, 2);
+            const int u_sm = std::min(env_int("HCG_UNION_PER_SM", 1), per_sm - 1);
+            const uint32_t n_union = std::min<uint32_t>(a.nq, uint32_t(sms * u_sm));
+            const uint32_t n_gather = std::min<uint32_t>((a.nq + 7) / 8, uint32_t(sms * (per_sm - u_sm)));
+            HCG_RET_IF(cudaMemsetAsync(flags, 0, size_t(a.nq) * 4, st) == cudaSuccess
+                           ? HCG_OK : set_error(HCG_ECUDA, "flags memset"));
+            kern<<<n_union + n_gather, kRefineThreads, usmem, st>>>(a, lists, counts, lstride, utb, n_union, flags, 1u);
+            return check_launch("k_refine_fused");
+        }
+        static bool cfg_u[64] = {};
+        HCG_RET_IF(opt_in_smem(k_union, device, cfg_u));
+        const uint32_t ugrid = persistent_grid(reinterpret_cast<const void*>(k_union), usmem, device, a.nq);
+        k_union<<<ugrid, kRefineThreads, usmem, st>>>(a, lists, counts, lstride, utb);
+        HCG_RET_IF(check_launch("k_union"));
+        auto kern = k_gather<R, CR, MINB>;
+        int per_sm = 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRefineThreads, 0);
-        const uint32_t warps_needed = a.nq;
-        const uint32_t blocks = std::min<uint32_t>((warps_needed + 7) / 8, uint32_t(sms * std::max(per_sm, 1)));
-        kern<<<blocks, kRefineThreads, 0, st>>>(a, lists, counts, T);
+        const uint32_t blocks = std::min<uint32_t>((a.nq + 7) / 8, uint32_t(sms * std::max(per_sm, 1)));
+        kern<<<blocks, kRefineThreads, 0, st>>>(a, lists, counts, lstride);
         return check_launch("k_gather");
     }
     const bool gtab = size_t(T) * 4 + (size_t(4) << tb) > 160 * 1024;
