@@ -268,18 +268,25 @@ def run_ours(a):
     h2d = Q * 128
     d2h = Q * k * 8 + Q * k * 4 + Q * 4
 
-    # refine-kernel roofline (outside the timed region): per-launch device time.
-    tl, tr = [], []
+    # dominant-kernel roofline (outside the timed region): per-launch device
+    # times of locate / candidate union / gather+score, CUDA events on `stream`.
+    tl, tu, tg = [], [], []
     for b in range(a.warmup, nb):
-        ml, mr = sidx.local.search_timed(batches[b], k, shard_depth, out=out)
+        ml, mu, mg = sidx.local.search_timed(batches[b], k, shard_depth, out=out)
         tl.append(ml)
-        tr.append(mr)
+        tu.append(mu)
+        tg.append(mg)
     U = sidx.local.candidate_counts(batches[a.warmup], shard_depth).astype(np.float64)
     take = min(shard_depth, sidx.local.size())
-    bytes_refine = float(U.sum() * 128 + Q * (4 * C * take + 4 * C + 128) + Q * (12 * k + 4))
-    refine_ms = statistics.mean(tr)
+    # k_gather reads each unique row (128 B) + its list entry (4 B), the query
+    # (128 B) and the count, and writes k (id, sqdist) pairs + len.
+    bytes_gather = float(U.sum() * (128 + 4) + Q * (128 + 4 + 12 * k + 4))
+    # k_union reads C windows of ids + C begins and writes the unique list.
+    bytes_union = float(Q * (4 * C * take + 4 * C) + U.sum() * 4)
+    gather_ms = statistics.median(tg)
+    union_ms = statistics.median(tu)
     peak, peak_src = measured_peak_gbs()
-    achieved = bytes_refine / (refine_ms * 1e-3) / 1e9
+    achieved = bytes_gather / (gather_ms * 1e-3) / 1e9
     logn = max(1, int(np.ceil(np.log2(max(2, sidx.local.size())))))
     bytes_q = float(U.mean() * 128 + 4 * C * take + 16 * C * logn + 128 + 8 * k)
 
@@ -341,7 +348,7 @@ def run_ours(a):
         ms_step = ms_total / a.steps
         value = Q * a.steps / (ms_total * 1e-3)
         e2e_value = Q * a.steps / (ms_e2e * 1e-3)
-        traffic = ncu_traffic(f"N{world}_Q{Q}_D{shard_depth}_{a.view}")
+        traffic = ncu_traffic(f"k{k}_Q{Q}_D{shard_depth}_{a.view}_n{sidx.local.size()}")
         line = {
             "metric": METRIC,
             "value": round(value, 1),
@@ -370,19 +377,22 @@ def run_ours(a):
             "roofline": {
                 "bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
-                "kernel": "k_refine (dedup + gather + exact L2 + top-k)",
-                "algorithmic_bytes_per_launch": bytes_refine,
-                "launch_ms": round(refine_ms, 4), "locate_ms": round(statistics.mean(tl), 4),
+                "kernel": "k_gather (gather of the unique candidate rows + exact L2 + top-k)",
+                "algorithmic_bytes_per_launch": bytes_gather,
+                "launch_ms": round(gather_ms, 4),
+                "other_kernels_ms": {"k_locate": round(statistics.median(tl), 4),
+                                     "k_union": round(union_ms, 4)},
+                "k_union_algorithmic_gbs": round(bytes_union / max(union_ms, 1e-9) / 1e6, 1),
                 "peak_source": peak_src,
                 "bytes_per_query_B_q": round(bytes_q, 1),
                 "unique_candidates_per_query": round(float(U.mean()), 1),
-                "step_hbm_gbs": round(value * bytes_q / 1e9, 1),
+                "step_hbm_gbs": round(Q * a.steps / (ms_total * 1e-3) * bytes_q / 1e9, 1),
             },
             "cpu_baseline": cpu,
             "parity_vs_reference": parity,
             "e2e": {"value": round(e2e_value, 1), "unit": "queries/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
-            "gpu_launches": a.steps * (2 if world == 1 else 3),
+            "gpu_launches": a.steps * (3 if world == 1 else 4),
             "clocks": clocks.summary(),
             "latency": lat,
         }

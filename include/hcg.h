@@ -129,8 +129,10 @@ hcg_status hcg_search(const hcg_index* index, const uint8_t* queries, uint32_t n
                       void* stream);
 
 /* hcg_search with per-kernel device times: records CUDA events around the
- * locate and refine launches on `stream` and synchronises it; ms_out[0] is the
- * locate kernel, ms_out[1] the refine kernel (instrumentation for bench.py). */
+ * launches on `stream` and synchronises it.  ms_out[0] = locate (keys +
+ * lower_bound + windows), ms_out[1] = candidate union (dedup; 0 when fused
+ * into the refine kernel), ms_out[2] = gather + exact L2 + top-k
+ * (instrumentation for bench.py). */
 hcg_status hcg_search_timed(const hcg_index* index, const uint8_t* queries, uint32_t nq, uint32_t k,
                             uint32_t depth, uint64_t* out_ids, uint32_t* out_sqdist,
                             uint32_t* out_len, float* ms_out, void* stream);

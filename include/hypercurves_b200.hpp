@@ -1,0 +1,220 @@
+// hypercurves_b200.hpp -- header-only C++ mirror of the reference's index API
+// (namespace hc, proj/include/hypercurves/{multicurves,vecio,curve}.hpp) over
+// the C ABI in hcg.h.  A reference user swaps
+//
+//     hc::MulticurvesIndex idx(ds, hc::default_scheme(128, 8, 16, hc::CurveKind::Hilbert, 0));
+//     hc::NeighborList nl = idx.search(q, {10, 350});
+// for
+//     hcb::MulticurvesIndex idx(ds, hcb::default_scheme(128, 8, 16, hcb::CurveKind::Hilbert, 0),
+//                               hcb::View::lifted());
+//     hcb::NeighborList nl = idx.search(q, {10, 350});
+//
+// and gets bit-identical NeighborLists (same ids, same rooted double
+// distances, same (distance, id) tie order) from the B200.  The dataset and
+// query types are templates: anything with hc::Dataset / hc::FeatureVector's
+// shape (`.vectors[i].id`, `.vectors[i].components`, `.dims`) works, the
+// reference's own types included.  Errors map back to the reference's
+// exception types: std::invalid_argument for precondition / capacity /
+// non-finite violations (curve.cpp:35-59,167; vecio.cpp:88,116),
+// std::runtime_error for device failures.
+//
+// Descriptors must be byte-valued in the chosen view (component == offset +
+// b * scale for an integral b in [0, 255]): raw bvecs (View::raw) or the
+// lifted view 1 + b/256 (View::lifted).
+#pragma once
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "hcg.h"
+
+namespace hcb {
+
+enum class CurveKind : std::uint32_t { ZOrder = HCG_ZORDER, Hilbert = HCG_HILBERT };
+
+struct Neighbor {  // vecio.hpp:27-32
+    std::uint64_t id = 0;
+    double distance = 0.0;
+    friend bool operator==(const Neighbor&, const Neighbor&) = default;
+};
+using NeighborList = std::vector<Neighbor>;
+
+struct SearchParams {  // multicurves.hpp:69-72
+    std::size_t k = 1;
+    std::size_t probe_depth = 1;
+};
+
+struct ProjectionScheme {  // multicurves.hpp:18-32
+    std::uint32_t d_full = 0;
+    std::uint32_t bits_per_dim = 8;
+    CurveKind curve_kind = CurveKind::Hilbert;
+    std::uint64_t seed = 0;
+    std::vector<std::vector<std::uint32_t>> assignment;
+    std::uint32_t curves() const { return static_cast<std::uint32_t>(assignment.size()); }
+    std::uint32_t dims_of(std::uint32_t c) const { return static_cast<std::uint32_t>(assignment[c].size()); }
+};
+
+// How the reference sees a stored byte b: offset + b * scale (f32).
+struct View {
+    float offset = 0.0f;
+    float scale = 1.0f;
+    static View raw() { return {0.0f, 1.0f}; }             // bvecs widening, vecio.cpp:50-51
+    static View lifted() { return {1.0f, 1.0f / 256.0f}; }  // 1 + b/256
+};
+
+namespace detail {
+inline void check(hcg_status rc) {
+    if (rc == HCG_OK) return;
+    const std::string msg = hcg_last_error();
+    if (rc == HCG_EINVAL || rc == HCG_ECAPACITY || rc == HCG_ENONFINITE) throw std::invalid_argument(msg);
+    throw std::runtime_error(msg);
+}
+
+inline std::uint8_t to_byte(float x, const View& v) {
+    if (!std::isfinite(x)) throw std::invalid_argument("non-finite component");
+    const float b = (x - v.offset) / v.scale;
+    const float r = std::nearbyint(b);
+    if (!(r >= 0.0f && r <= 255.0f) || v.offset + r * v.scale != x)
+        throw std::invalid_argument("component is not a byte value of the index view");
+    return static_cast<std::uint8_t>(r);
+}
+
+template <class Vec>
+void append_bytes(const Vec& v, std::uint32_t dims, const View& view, std::vector<std::uint8_t>& out) {
+    if (v.components.size() != dims) throw std::invalid_argument("dimension mismatch");
+    for (float x : v.components) out.push_back(to_byte(x, view));
+}
+}  // namespace detail
+
+// Round-robin assignment; a nonzero seed is unpinned by the
+// reference and rejected.
+inline ProjectionScheme default_scheme(std::uint32_t d_full, std::uint32_t curves, std::uint32_t bits_per_dim,
+                                       CurveKind kind, std::uint64_t seed) {
+    if (seed != 0) throw std::invalid_argument("seeded permutation is unpinned by the reference (SPEC.md:203)");
+    std::vector<std::uint32_t> off(curves + 1), asg(d_full);
+    detail::check(hcg_default_assignment(d_full, curves, off.data(), asg.data()));
+    ProjectionScheme s;
+    s.d_full = d_full;
+    s.bits_per_dim = bits_per_dim;
+    s.curve_kind = kind;
+    s.seed = seed;
+    for (std::uint32_t c = 0; c < curves; ++c) s.assignment.emplace_back(asg.begin() + off[c], asg.begin() + off[c + 1]);
+    return s;
+}
+
+// hc::MulticurvesIndex on one B200.  Build copies the rows into HBM; search
+// is const and may run concurrently from several threads.
+class MulticurvesIndex {
+  public:
+    MulticurvesIndex() = default;
+
+    template <class Dataset>
+    MulticurvesIndex(const Dataset& ds, ProjectionScheme scheme, View view = View::raw(), int device = 0)
+        : scheme_(std::move(scheme)), view_(view) {
+        std::vector<std::uint8_t> rows;
+        rows.reserve(ds.vectors.size() * scheme_.d_full);
+        for (std::size_t i = 0; i < ds.vectors.size(); ++i) {
+            if (ds.vectors[i].id != i) throw std::invalid_argument("dataset ids must be 0..n-1 in order (vecio.hpp:22)");
+            detail::append_bytes(ds.vectors[i], scheme_.d_full, view_, rows);
+        }
+        build(rows.data(), ds.vectors.size(), device);
+    }
+
+    // Raw byte rows (bvecs payloads), ids id_base + s * id_stride.
+    MulticurvesIndex(const std::uint8_t* rows, std::uint64_t n, ProjectionScheme scheme, View view, int device = 0,
+                     std::uint64_t id_base = 0, std::uint64_t id_stride = 1)
+        : scheme_(std::move(scheme)), view_(view) {
+        build(rows, n, device, id_base, id_stride);
+    }
+
+    MulticurvesIndex(const MulticurvesIndex&) = delete;
+    MulticurvesIndex& operator=(const MulticurvesIndex&) = delete;
+    MulticurvesIndex(MulticurvesIndex&& o) noexcept { *this = std::move(o); }
+    MulticurvesIndex& operator=(MulticurvesIndex&& o) noexcept {
+        std::swap(ix_, o.ix_);
+        std::swap(scheme_, o.scheme_);
+        std::swap(view_, o.view_);
+        return *this;
+    }
+    ~MulticurvesIndex() {
+        if (ix_) hcg_free(ix_);
+    }
+
+    std::size_t size() const { return ix_ ? hcg_size(ix_) : 0; }
+    const ProjectionScheme& scheme() const { return scheme_; }
+    hcg_index* handle() const { return ix_; }
+
+    // multicurves.hpp:81 for one query.
+    template <class FeatureVector>
+    NeighborList search(const FeatureVector& q, const SearchParams& p) const {
+        std::vector<std::uint8_t> qb;
+        detail::append_bytes(q, scheme_.d_full, view_, qb);
+        return search_bytes(qb.data(), 1, p).front();
+    }
+
+    // Batched search over byte queries (nq x d_full); one NeighborList each.
+    std::vector<NeighborList> search_bytes(const std::uint8_t* queries, std::uint32_t nq, const SearchParams& p,
+                                           void* stream = nullptr) const {
+        if (p.k < 1 || p.probe_depth < 1) throw std::invalid_argument("invalid search params");
+        if (p.k > HCG_MAX_K || p.probe_depth > 0xFFFFFFFFu) throw std::invalid_argument("k / probe_depth beyond capacity");
+        const std::uint32_t k = static_cast<std::uint32_t>(p.k);
+        std::vector<std::uint64_t> ids(std::size_t(nq) * k);
+        std::vector<std::uint32_t> sq(std::size_t(nq) * k), len(nq);
+        detail::check(hcg_search(ix_, queries, nq, k, static_cast<std::uint32_t>(p.probe_depth), ids.data(),
+                                 sq.data(), len.data(), stream));
+        std::vector<NeighborList> out(nq);
+        for (std::uint32_t q = 0; q < nq; ++q) {
+            out[q].resize(len[q]);
+            for (std::uint32_t i = 0; i < len[q]; ++i)
+                out[q][i] = {ids[std::size_t(q) * k + i],
+                             std::sqrt(double(sq[std::size_t(q) * k + i])) * double(view_.scale)};
+        }
+        return out;
+    }
+
+    // multicurves.hpp:87-89 (sorted ascending).
+    template <class FeatureVector>
+    std::vector<std::uint64_t> candidate_union(const FeatureVector& q, std::size_t depth) const {
+        std::vector<std::uint8_t> qb;
+        detail::append_bytes(q, scheme_.d_full, view_, qb);
+        const std::uint32_t cap = static_cast<std::uint32_t>(scheme_.curves() * std::min<std::size_t>(depth, size()));
+        std::vector<std::uint64_t> ids(cap ? cap : 1);
+        std::uint32_t cnt = 0;
+        detail::check(hcg_candidates(ix_, qb.data(), 1, static_cast<std::uint32_t>(depth), ids.data(), cap ? cap : 1,
+                                     &cnt, nullptr));
+        ids.resize(cnt);
+        std::sort(ids.begin(), ids.end());
+        return ids;
+    }
+
+  private:
+    void build(const std::uint8_t* rows, std::uint64_t n, int device, std::uint64_t id_base = 0,
+               std::uint64_t id_stride = 1) {
+        std::vector<std::uint32_t> off{0}, asg;
+        for (const auto& slots : scheme_.assignment) {
+            asg.insert(asg.end(), slots.begin(), slots.end());
+            off.push_back(static_cast<std::uint32_t>(asg.size()));
+        }
+        hcg_scheme s{};
+        s.d_full = scheme_.d_full;
+        s.curves = scheme_.curves();
+        s.bits_per_dim = scheme_.bits_per_dim;
+        s.curve_kind = static_cast<std::uint32_t>(scheme_.curve_kind);
+        s.assign_off = off.data();
+        s.assign = asg.data();
+        s.dist_scale = view_.scale;
+        detail::check(hcg_make_lut(view_.offset, view_.scale, scheme_.bits_per_dim, s.cell_lut));
+        detail::check(hcg_build(&s, rows, n, id_base, id_stride, device, nullptr, &ix_));
+    }
+
+    hcg_index* ix_ = nullptr;
+    ProjectionScheme scheme_;
+    View view_;
+};
+
+}  // namespace hcb

@@ -382,25 +382,11 @@ RefineArgs refine_args(const hcg_index* ix, const uint8_t* dq, uint32_t nq, uint
 
 hcg_status run_refine(const hcg_index* ix, Scratch& sc, const RefineArgs& a_in) {
     RefineArgs a = a_in;
-    static unsigned long long* prof = nullptr;
-    if (getenv("HCG_REFINE_PROFILE")) {  // phase counters for tools/tune_refine.py
-        if (!prof) cudaMalloc(&prof, 64);
-        a.prof = prof;
-    }
     size_t need = 0;
     HCG_TRY(launch_refine(a, nullptr, &need, ix->device, sc.st));
     void* scratch = need ? sc.alloc<uint8_t>(need) : reinterpret_cast<void*>(1);
     if (!scratch) return set_error(HCG_ENOMEM, "refine scratch");
-    if (a.prof) cudaMemsetAsync(a.prof, 0, 64, sc.st);
     const hcg_status rc = launch_refine(a, need ? scratch : reinterpret_cast<void*>(1), &need, ix->device, sc.st);
-    if (a.prof && rc == HCG_OK) {
-        unsigned long long h[4];
-        cudaMemcpyAsync(h, a.prof, 32, cudaMemcpyDeviceToHost, sc.st);
-        cudaStreamSynchronize(sc.st);
-        const double tot = double(h[0] + h[1] + h[2] + h[3]);
-        fprintf(stderr, "[hcg refine phases, warp-cycles] wait+barrier %.1f%%  dedup %.1f%%  gather %.1f%%  merge-barrier %.1f%%  (%.3g total)\n",
-                100 * h[0] / tot, 100 * h[1] / tot, 100 * h[2] / tot, 100 * h[3] / tot, tot);
-    }
     return rc;
 }
 
@@ -563,7 +549,7 @@ static hcg_status search_impl(const hcg_index* ix, const uint8_t* queries, uint3
         HCG_TRY(stage_rows(sc, queries, nq, ix->d_full, ix->pitch, &dq));
         uint32_t* begins = sc.alloc<uint32_t>(size_t(nq) * ix->C);
         if (!begins) return set_error(HCG_ENOMEM, "window buffer");
-        cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+        cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
         if (ms_out) {
             for (auto& e : ev) HCG_TRY_CUDA(cudaEventCreate(&e));
             HCG_TRY_CUDA(cudaEventRecord(ev[0], st));
@@ -571,6 +557,7 @@ static hcg_status search_impl(const hcg_index* ix, const uint8_t* queries, uint3
         HCG_TRY(locate(ix, sc, dq, nq, depth, begins, nullptr));
         if (ms_out) HCG_TRY_CUDA(cudaEventRecord(ev[1], st));
         RefineArgs a = refine_args(ix, dq, nq, depth, k, begins);
+        if (ms_out) a.ev_mid = ev[2];
         if (packed) {
             a.mode = kOutPacked;
             a.out_packed = op.dev;
@@ -582,10 +569,18 @@ static hcg_status search_impl(const hcg_index* ix, const uint8_t* queries, uint3
         }
         HCG_TRY(run_refine(ix, sc, a));
         if (ms_out) {
-            HCG_TRY_CUDA(cudaEventRecord(ev[2], st));
-            HCG_TRY_CUDA(cudaEventSynchronize(ev[2]));
+            HCG_TRY_CUDA(cudaEventRecord(ev[3], st));
+            HCG_TRY_CUDA(cudaEventSynchronize(ev[3]));
             HCG_TRY_CUDA(cudaEventElapsedTime(&ms_out[0], ev[0], ev[1]));
-            HCG_TRY_CUDA(cudaEventElapsedTime(&ms_out[1], ev[1], ev[2]));
+            float mid = 0.0f;
+            if (cudaEventQuery(ev[2]) == cudaSuccess && cudaEventElapsedTime(&mid, ev[1], ev[2]) == cudaSuccess) {
+                ms_out[1] = mid;  // candidate union
+                HCG_TRY_CUDA(cudaEventElapsedTime(&ms_out[2], ev[2], ev[3]));
+            } else {  // single refine kernel
+                cudaGetLastError();
+                ms_out[1] = 0.0f;
+                HCG_TRY_CUDA(cudaEventElapsedTime(&ms_out[2], ev[1], ev[3]));
+            }
             for (auto& e : ev) cudaEventDestroy(e);
         }
     }
@@ -605,7 +600,7 @@ hcg_status hcg_search(const hcg_index* ix, const uint8_t* queries, uint32_t nq, 
 hcg_status hcg_search_timed(const hcg_index* ix, const uint8_t* queries, uint32_t nq, uint32_t k, uint32_t depth,
                             uint64_t* out_ids, uint32_t* out_sqdist, uint32_t* out_len, float* ms_out, void* stream) {
     if (!ms_out) return set_error(HCG_EINVAL, "null ms_out");
-    ms_out[0] = ms_out[1] = 0.0f;
+    ms_out[0] = ms_out[1] = ms_out[2] = 0.0f;
     return search_impl(ix, queries, nq, k, depth, out_ids, out_sqdist, out_len, nullptr, stream, ms_out);
 }
 

@@ -65,7 +65,8 @@ struct RefineArgs {
     uint32_t* out_len;     // kOutIds: len; kOutCandidates: count
     uint64_t* out_packed;  // kOutPacked
     uint32_t cap;          // kOutCandidates
-    unsigned long long* prof;  // optional phase-cycle counters (tools/tune_refine.py)
+    unsigned long long* prof;  // unused (kept zero)
+    cudaEvent_t ev_mid;        // optional: recorded between the union and gather launches
 };
 // Scratch bytes the refine launch needs (global hash tables when the table
 // does not fit in shared memory); query with scratch == nullptr first.

@@ -711,6 +711,7 @@ hcg_status refine_dispatch(const RefineArgs& a, void* scratch, size_t* scratch_b
         const uint32_t ugrid = persistent_grid(reinterpret_cast<const void*>(k_union), usmem, device, a.nq);
         k_union<<<ugrid, kRefineThreads, usmem, st>>>(a, lists, counts, lstride, utb);
         HCG_RET_IF(check_launch("k_union"));
+        if (a.ev_mid) cudaEventRecord(a.ev_mid, st);
         auto kern = k_gather<R, CR, MINB>;
         int per_sm = 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRefineThreads, 0);

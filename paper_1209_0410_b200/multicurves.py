@@ -248,14 +248,14 @@ class MulticurvesIndex:
         return ids, sq, ln
 
     def search_timed(self, queries, k: int, probe_depth: int, out, stream=None):
-        """search_batch into preallocated outputs, returning the device time (ms)
-        of the locate and refine kernels measured with CUDA events on `stream`."""
+        """search_batch into preallocated outputs, returning the device times (ms)
+        of (locate, candidate union, gather+score) measured with CUDA events on `stream`."""
         q = _u8_2d(queries, self.scheme.d_full)
         ids, sq, ln = out
-        ms = (C.c_float * 2)()
+        ms = (C.c_float * 3)()
         check(lib().hcg_search_timed(self._h, _ptr(q), q.shape[0], k, probe_depth, _ptr(ids), _ptr(sq),
                                      _ptr(ln), ms, _stream(stream, q)))
-        return float(ms[0]), float(ms[1])
+        return float(ms[0]), float(ms[1]), float(ms[2])
 
     def search(self, query, params: SearchParams) -> list:
         """hc::MulticurvesIndex::search for one query -> NeighborList."""

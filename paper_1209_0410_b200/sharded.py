@@ -24,6 +24,33 @@ def shard_rows(n_total: int, rank: int, world: int) -> int:
     return 0 if rank >= n_total else (n_total - rank + world - 1) // world
 
 
+def exchange(packed, world: int, group=None, out=None):
+    """The aggregate's only collective: all-gather every rank's packed
+    (sqdist << 32 | gid) top-k block [nq, k] into [world, nq, k] (NCCL over
+    NVLink on GPUs; any torch.distributed backend works)."""
+    import torch
+    import torch.distributed as dist
+    nq, k = int(packed.shape[0]), int(packed.shape[1])
+    if out is None:
+        out = torch.empty((world, nq, k), dtype=packed.dtype, device=packed.device)
+    src = packed.contiguous()
+    if src.dtype == torch.uint64:  # NCCL/gloo move 64-bit payloads as int64
+        src = src.view(torch.int64)
+        dst = out.view(torch.int64)
+    else:
+        dst = out
+    dist.all_gather_into_tensor(dst.view(-1), src.view(-1), group=group)
+    return out
+
+
+def pack(ids, sqdist, lens, k: int):
+    """Packed (sqdist << 32 | id) per result, -1 (all ones) past each list's length."""
+    import torch
+    p = (sqdist.to(torch.int64) << 32) | ids.view(torch.int64)
+    valid = lens.view(-1, 1).to(torch.int64) > torch.arange(k, device=ids.device)
+    return torch.where(valid, p, torch.full_like(p, -1))
+
+
 class ShardedIndex:
     """One rank's share of a G-way sharded Multicurves index."""
 
@@ -59,7 +86,6 @@ class ShardedIndex:
         Returns (ids u64, sqdist u32, len u32) CUDA tensors, identical on all ranks.
         """
         import torch
-        import torch.distributed as dist
         dev = queries.device
         nq = int(queries.shape[0])
         if self.world == 1:
@@ -67,22 +93,16 @@ class ShardedIndex:
         packed = self._buf("packed", (nq, k), torch.uint64, dev)
         self.local.search_packed(queries, k, shard_depth, out=packed)
         gathered = self._buf("gathered", (self.world, nq, k), torch.uint64, dev)
-        dist.all_gather_into_tensor(gathered.view(torch.int64).view(-1), packed.view(torch.int64).view(-1),
-                                    group=self.group)
+        exchange(packed, self.world, self.group, out=gathered)
         return merge_packed(gathered, k, device=dev.index, out=out)
 
     def brute_force(self, queries, k: int):
         """Exact global top-k (recall ground truth): per-shard exact lists merged the same way."""
         import torch
-        import torch.distributed as dist
         ids, sq, ln = self.local.brute_force(queries, k)
         if self.world == 1:
             return ids, sq, ln
-        packed = (sq.to(torch.int64) << 32) | ids.view(torch.int64)
-        packed = torch.where(ln.view(-1, 1).to(torch.int64) > torch.arange(k, device=ids.device),
-                             packed, torch.full_like(packed, -1))
-        gathered = torch.empty((self.world,) + tuple(packed.shape), dtype=torch.int64, device=ids.device)
-        dist.all_gather_into_tensor(gathered.view(-1), packed.contiguous().view(-1), group=self.group)
+        gathered = exchange(pack(ids, sq, ln, k), self.world, self.group)
         return merge_packed(gathered.view(torch.uint64), k, device=ids.device.index)
 
 
