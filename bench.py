@@ -470,6 +470,8 @@ def run_reference(a):
 
 
 def main():
+    # one JSON line on rank 0's stdout: keep NCCL's banner out of it
+    os.environ.setdefault("NCCL_DEBUG", "WARN")
     a = parse()
     if a.impl == "reference":
         run_reference(a)
