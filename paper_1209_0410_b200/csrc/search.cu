@@ -1,22 +1,25 @@
 // search.cu -- batched query path on the B200 (Alg. 2).
 //
-//   K3a k_locate : one thread per (query, curve): project + quantize + curve
-//                  key (fused K1), compare against the curve's common key
-//                  prefix, lower_bound over the sorted suffix keys
-//                  (SubIndex::rank_of, multicurves.hpp:57-58) and the window
-//                  begin (SubIndex::window, multicurves.hpp:60-63).
-//   K3b k_refine : one CTA per query: read every curve's window of slots
-//                  (coalesced), dedup them in a shared-memory hash set
-//                  (candidate_union, multicurves.hpp:87-89), gather the
-//                  candidate descriptors with 128-bit streaming loads (8 lanes
-//                  per 128-B row, 8 rows in flight per lane), exact integer
-//                  squared L2 (vecio.cpp:87-95) with vabsdiff4+dp4a, and a
-//                  warp-register top-k on packed (sqdist<<32 | slot), which is
-//                  the reference's (distance, id) order (vecio.cpp:101-113).
-//   K4  k_merge  : one warp per query, k-way merge of per-shard / per-chunk
-//                  sorted lists (hypershard aggregate).
-//   K5  k_brute  : exact kNN over all rows (brute_force_knn, vecio.cpp:115-122)
-//                  for recall ground truth; chunked, then merged by K4.
+//   K3a k_locate    : one thread per (query, curve): project + quantize + curve
+//                     key (fused K1), compare against the curve's common key
+//                     prefix, lower_bound over the sorted suffix keys
+//                     (SubIndex::rank_of, multicurves.hpp:57-58) and the window
+//                     begin (SubIndex::window, multicurves.hpp:60-63).
+//   K3b k_union     : one CTA per query: the C windows' ids (cp.async,
+//                     prefetched one query ahead) deduplicated in shared memory
+//                     without atomics (candidate_union, multicurves.hpp:87-89);
+//                     unique list -> HBM.  k_union_cas: the same with a global
+//                     CAS table for very large curves x depth.
+//   K3c k_gather    : one WARP per query: gather the unique candidate rows
+//                     (8 lanes per 128-B row, 8 rows in flight per lane, next
+//                     slots prefetched), exact squared L2 (vecio.cpp:87-95) with
+//                     vabsdiff4 + dp4a, warp-register top-k on packed
+//                     (sqdist<<32 | slot) == the reference's (distance, id)
+//                     order (vecio.cpp:101-113).
+//   K4  k_merge     : one warp per query, k-way merge of per-shard / per-chunk
+//                     sorted lists (hypershard aggregate).
+//   K5  k_brute     : exact kNN over all rows (brute_force_knn, vecio.cpp:115-122)
+//                     for recall ground truth; chunked, then merged by K4.
 #include <algorithm>
 #include <cstdlib>
 
@@ -265,20 +268,10 @@ __device__ __forceinline__ uint32_t block_excl_scan256_u(uint32_t v, uint32_t* w
 constexpr int kUnionRounds = 6;
 constexpr uint32_t kUnionMaxT = 32 * 256;  // one u32 pending mask per thread
 
-__device__ __forceinline__ void publish(uint32_t* flag, uint32_t v) {
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(v) : "memory");
-}
-__device__ __forceinline__ uint32_t acquire(const uint32_t* flag) {
-    uint32_t v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
-    return v;
-}
-
-// One CTA deduplicating queries q0, q0 + qstep, ...; with `flags`, each
-// finished list is published with a release store of `epoch` to flags[q].
+// One CTA deduplicating queries q0, q0 + qstep, ...
 __device__ __forceinline__ void union_cta(const RefineArgs& a, uint32_t* __restrict__ lists,
                                           uint32_t* __restrict__ counts, uint32_t lstride, uint32_t tb,
-                                          uint32_t q0, uint32_t qstep, uint32_t* flags, uint32_t epoch) {
+                                          uint32_t q0, uint32_t qstep) {
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t T = a.C * a.take;
     const uint32_t** sptr = reinterpret_cast<const uint32_t**>(smem);
@@ -369,11 +362,6 @@ __device__ __forceinline__ void union_cta(const RefineArgs& a, uint32_t* __restr
         uint32_t w = 0;
         for (uint32_t pm = keep; pm; pm &= pm - 1) out[w++] = idbuf[tid + uint32_t(__ffs(pm) - 1) * kRefineThreads];
         if (tid == kRefineThreads - 1) counts[q] = off + mine;
-        if (flags) {
-            __threadfence();
-            __syncthreads();
-            if (tid == 0) publish(flags + q, epoch);
-        }
     }
     cp_async_wait_all();
 }
@@ -381,7 +369,7 @@ __device__ __forceinline__ void union_cta(const RefineArgs& a, uint32_t* __restr
 __global__ void __launch_bounds__(kRefineThreads) k_union(RefineArgs a, uint32_t* __restrict__ lists,
                                                           uint32_t* __restrict__ counts, uint32_t lstride,
                                                           uint32_t tb) {
-    union_cta(a, lists, counts, lstride, tb, blockIdx.x, gridDim.x, nullptr, 0);
+    union_cta(a, lists, counts, lstride, tb, blockIdx.x, gridDim.x);
 }
 
 // ------------------------------------------------------------- K3c ----
@@ -391,22 +379,14 @@ __global__ void __launch_bounds__(kRefineThreads) k_union(RefineArgs a, uint32_t
 // per lane); the next pass's slots are prefetched while the rows load.  The
 // reduce-scatter leaves row (8*grp + l8)'s squared distance in lane l8 of
 // group grp, which offers (sqdist << 32 | slot) to the warp top-k.
-// One warp scoring queries q0, q0 + qstep, ...; with `flags` it first waits
-// (acquire) for the union CTA to publish the query's list.  Lists are read
-// with ld.global.cg: they are written during the same launch by other SMs.
+// One warp scoring queries q0, q0 + qstep, ...  Lists are read with
+// ld.global.cg (L2): they were written by the preceding union launch.
 template <int R, int CR>
 __device__ __forceinline__ void gather_warp(const RefineArgs& a, const uint32_t* lists, const uint32_t* counts,
-                                            uint32_t lstride, uint32_t q0, uint32_t qstep, const uint32_t* flags,
-                                            uint32_t epoch) {
+                                            uint32_t lstride, uint32_t q0, uint32_t qstep) {
     const int lane = threadIdx.x & 31, l8 = lane & 7, grp = lane >> 3;
     const uint32_t chunks = a.pitch >> 4;
     for (uint32_t q = q0; q < a.nq; q += qstep) {
-        if (flags) {
-            if (lane == 0)
-                while (acquire(flags + q) != epoch) __nanosleep(256);
-            __syncwarp();
-            (void)acquire(flags + q);
-        }
         const uint32_t n = __ldcg(counts + q);
         const uint32_t* list = lists + uint64_t(q) * lstride;
         uint4 qv[CR];
@@ -482,25 +462,7 @@ __global__ void __launch_bounds__(kRefineThreads, MINB) k_gather(RefineArgs a, c
                                                                  const uint32_t* __restrict__ counts,
                                                                  uint32_t lstride) {
     gather_warp<R, CR>(a, lists, counts, lstride, (blockIdx.x * kRefineThreads + threadIdx.x) >> 5,
-                       gridDim.x * (kRefineThreads / 32), nullptr, 0);
-}
-
-// Union and gather in ONE persistent launch: CTAs [0, n_union) deduplicate
-// (union_cta) and publish per-query ready flags, the other CTAs' warps score
-// (gather_warp) as the lists become ready, so the shared-memory-bound dedup
-// overlaps the HBM-bound gather on every SM.  Union CTAs never wait, so the
-// launch makes progress even when not every CTA is resident.
-template <int R, int CR, int MINB>
-__global__ void __launch_bounds__(kRefineThreads, MINB) k_refine_fused(RefineArgs a, uint32_t* lists, uint32_t* counts,
-                                                                       uint32_t lstride, uint32_t tb, uint32_t n_union,
-                                                                       uint32_t* flags, uint32_t epoch) {
-    if (blockIdx.x < n_union) {
-        union_cta(a, lists, counts, lstride, tb, blockIdx.x, n_union, flags, epoch);
-    } else {
-        const uint32_t gw = (blockIdx.x - n_union) * (kRefineThreads / 32) + (threadIdx.x >> 5);
-        gather_warp<R, CR>(a, lists, counts, lstride, gw, (gridDim.x - n_union) * (kRefineThreads / 32), flags,
-                           epoch);
-    }
+                       gridDim.x * (kRefineThreads / 32));
 }
 
 // Candidate-union tap: unique slots -> ids.
@@ -516,48 +478,33 @@ __global__ void k_lists_to_ids(RefineArgs a, const uint32_t* __restrict__ lists,
     if (threadIdx.x == 0) a.out_len[q] = n;
 }
 
-// K3b general fallback (also the candidate_union tap): CTA-wide dedup of the
-// window ids (read straight from HBM) into a CAS hash set -- in shared memory
-// or, for very large curves x depth, in a per-CTA global scratch table -- then
-// the same gather/score/top-k.
-template <int R, int CR>
-__global__ void __launch_bounds__(kRefineThreads) k_refine_cas(RefineArgs a, uint32_t table_bits,
-                                                               uint32_t* gtables) {
-    constexpr int KCAP = 32 * R;
-    constexpr int kWarps = kRefineThreads / 32;
-    extern __shared__ __align__(16) unsigned char smem[];
+// K3b for large curves x depth (T > kUnionMaxT or beyond the shared budget):
+// the same candidate union with an atomicCAS hash set in a per-CTA GLOBAL
+// scratch table (cleared per query), ids read straight from the curves;
+// unique ids are appended (warp-aggregated) to the query's list in HBM.
+__global__ void __launch_bounds__(kRefineThreads) k_union_cas(RefineArgs a, uint32_t* __restrict__ lists,
+                                                              uint32_t* __restrict__ counts, uint32_t lstride,
+                                                              uint32_t tb, uint32_t* __restrict__ gtables) {
+    __shared__ uint32_t cnt;
     const uint32_t T = a.C * a.take;
-    uint64_t* mbuf = reinterpret_cast<uint64_t*>(smem);
-    uint32_t* sbeg = reinterpret_cast<uint32_t*>(mbuf + kWarps * KCAP);
-    uint32_t* scount = sbeg + a.C;
-    uint32_t* list = scount + 4;
-    uint32_t* table = gtables ? gtables + (uint64_t(blockIdx.x) << table_bits) : list + T;
-    const uint32_t tsize = 1u << table_bits, tmask = tsize - 1;
+    uint32_t* table = gtables + (uint64_t(blockIdx.x) << tb);
+    const uint32_t tsize = 1u << tb, tmask = tsize - 1;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t chunks = a.pitch >> 4;
     const unsigned lt = lanemask_lt_s();
-
     for (uint32_t q = blockIdx.x; q < a.nq; q += gridDim.x) {
         for (uint32_t i = tid; i < tsize; i += kRefineThreads) table[i] = kEmpty;
-        for (uint32_t c = tid; c < a.C; c += kRefineThreads) sbeg[c] = a.begins[uint64_t(q) * a.C + c];
-        if (tid == 0) *scount = 0;
-        uint4 qv[CR];
-        const uint8_t* qrow = a.queries + uint64_t(q) * a.pitch;
-#pragma unroll
-        for (int t = 0; t < CR; ++t) {
-            const uint32_t ch = (lane & 7) + 8 * t;
-            qv[t] = ch < chunks ? *reinterpret_cast<const uint4*>(qrow + ch * 16) : make_uint4(0, 0, 0, 0);
-        }
+        if (tid == 0) cnt = 0;
         __syncthreads();
+        uint32_t* out = lists + uint64_t(q) * lstride;
         for (uint32_t c = 0; c < a.C; ++c) {
-            const uint32_t* sl = a.slots[c] + sbeg[c];
+            const uint32_t* sl = a.slots[c] + a.begins[uint64_t(q) * a.C + c];
             for (uint32_t p0 = warp * 32; p0 < a.take; p0 += kRefineThreads) {
                 const uint32_t p = p0 + lane;
                 const bool has = p < a.take;
                 const uint32_t s = has ? __ldg(sl + p) : 0u;
                 bool fresh = false;
                 if (has) {
-                    uint32_t h = hash_slot(s) >> (32 - table_bits);
+                    uint32_t h = hash_slot(s) >> (32 - tb);
                     while (true) {
                         const uint32_t prev = atomicCAS(&table[h], kEmpty, s);
                         if (prev == kEmpty) {
@@ -572,40 +519,17 @@ __global__ void __launch_bounds__(kRefineThreads) k_refine_cas(RefineArgs a, uin
                 if (b) {
                     const int leader = __ffs(b) - 1;
                     uint32_t base = 0;
-                    if (lane == leader) base = atomicAdd(scount, uint32_t(__popc(b)));
+                    if (lane == leader) base = atomicAdd(&cnt, uint32_t(__popc(b)));
                     base = __shfl_sync(kFull, base, leader);
-                    if (fresh) list[base + __popc(b & lt)] = s;
+                    if (fresh) out[base + __popc(b & lt)] = s;
                 }
             }
         }
         __syncthreads();
-        const uint32_t Ucnt = *scount;
-        if (a.mode == kOutCandidates) {
-            const uint32_t lim = Ucnt < a.cap ? Ucnt : a.cap;
-            if (a.out_ids)
-                for (uint32_t i = tid; i < lim; i += kRefineThreads)
-                    a.out_ids[uint64_t(q) * a.cap + i] = a.id_base + uint64_t(list[i]) * a.id_stride;
-            if (tid == 0) a.out_len[q] = Ucnt;
-            __syncthreads();
-            continue;
-        }
-        WarpTopK<R> tk;
-        tk.init(int(a.k));
-        for (uint32_t base = warp * 32; base < Ucnt; base += kRefineThreads)
-            gather_rows<R, CR, 8>(a, list, base, Ucnt, qv, chunks, lane, tk);
-#pragma unroll
-        for (int r = 0; r < R; ++r) mbuf[warp * KCAP + lane * R + r] = tk.a[r];
-        __syncthreads();
-        if (warp == 0) {
-            WarpTopK<R> fin;
-            fin.init(int(a.k));
-            const uint32_t kr = (a.k + 31) & ~31u;
-            for (int w = 0; w < kWarps; ++w)
-                for (uint32_t i = 0; i < kr; i += 32) fin.offer(mbuf[w * KCAP + i + lane], lane);
-            write_result<R>(a, q, fin, lane, Ucnt);
-        }
+        if (tid == 0) counts[q] = cnt;
         __syncthreads();
     }
+    (void)T;
 }
 
 namespace {
@@ -629,100 +553,73 @@ uint32_t persistent_grid(const void* kern, size_t smem, int device, uint32_t nq)
     return std::min<uint32_t>(nq, uint32_t(sms * std::max(per_sm, 1)));
 }
 
-template <int R, int CR>
-hcg_status cas_launch(const RefineArgs& a, uint32_t tb, bool gtab, void* scratch, size_t* scratch_bytes, int device,
-                      cudaStream_t st) {
-    auto kern = k_refine_cas<R, CR>;
-    const uint64_t T = uint64_t(a.C) * a.take;
-    const size_t smem = size_t(8) * 32 * R * 8 + size_t(a.C) * 4 + 16 + T * 4 + (gtab ? 0 : (size_t(4) << tb));
-    if (smem > size_t(kRefineMaxSmem)) return set_error(HCG_ECAPACITY, "curves x depth exceeds the per-query candidate capacity");
-    static bool configured[64] = {};
-    HCG_RET_IF(opt_in_smem(kern, device, configured));
-    const uint32_t grid = gtab ? persistent_grid(reinterpret_cast<const void*>(kern), smem, device, a.nq) : a.nq;
-    const size_t need = gtab ? (size_t(grid) << tb) * 4 : 0;
-    if (!scratch) {
-        *scratch_bytes = need;
-        return HCG_OK;
-    }
-    kern<<<grid, kRefineThreads, smem, st>>>(a, tb, gtab ? static_cast<uint32_t*>(scratch) : nullptr);
-    return check_launch("k_refine_cas");
-}
-
 size_t union_smem_bytes(uint32_t C, uint32_t T, uint32_t tb) {
     return size_t(C) * 16 + 32 + size_t(T) * 8 + (size_t(4) << tb);
 }
 
-int env_int(const char* name, int dflt) {
-    const char* e = getenv(name);
-    return e ? atoi(e) : dflt;
-}
+
+// Query chunk so the per-call list scratch stays within kListBudget.
+constexpr size_t kListBudget = size_t(2) << 30;
 
 template <int R, int CR>
-hcg_status refine_dispatch(const RefineArgs& a, void* scratch, size_t* scratch_bytes, int device, cudaStream_t st) {
-    const uint32_t T = a.C * a.take;
+hcg_status refine_dispatch(const RefineArgs& a_in, void* scratch, size_t* scratch_bytes, int device, cudaStream_t st) {
+    const uint32_t T = a_in.C * a_in.take;
     uint32_t tb = 5;
     while ((uint64_t(1) << tb) * 7 < uint64_t(T) * 10) ++tb;
-    const int mode_env = env_int("HCG_REFINE_MODE", 1);  // 0 CTA-per-query CAS kernel, 1 union+gather
-    if (mode_env != 0 && T <= kUnionMaxT && union_smem_bytes(a.C, T, tb) <= 160 * 1024) {
-        // union -> lists in HBM -> warp-per-query gather
-        const uint32_t lstride = (T + 31) & ~31u;  // 128-B aligned per-query lists
-        // the union's tag table at <= ~0.35 load factor: most ids settle in round 1
-        const uint32_t utb = std::min<uint32_t>(tb + env_int("HCG_UNION_TB_EXTRA", 1), 16);
-        const size_t lists_bytes = size_t(a.nq) * lstride * 4;
-        const size_t counts_bytes = (size_t(a.nq) * 4 + 255) & ~size_t(255);
-        if (!scratch) {
-            *scratch_bytes = lists_bytes + 2 * counts_bytes;
-            return HCG_OK;
-        }
-        if (a.nq == 0) return HCG_OK;
-        uint32_t* lists = static_cast<uint32_t*>(scratch);
-        uint32_t* counts = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(scratch) + lists_bytes);
-        uint32_t* flags = counts + counts_bytes / 4;
-        const size_t usmem = union_smem_bytes(a.C, T, utb);
-        if (a.mode == kOutCandidates) {
-            static bool cfg_u[64] = {};
-            HCG_RET_IF(opt_in_smem(k_union, device, cfg_u));
+    if (tb > 28) return set_error(HCG_ECAPACITY, "candidate set too large");
+    const uint32_t lstride = (T + 31) & ~31u;  // 128-B aligned per-query lists
+    // the shared-memory union's tag table at <= ~0.35 load factor
+    const uint32_t utb = std::min<uint32_t>(tb + 1, 16);
+    const size_t usmem = union_smem_bytes(a_in.C, T, utb);
+    const bool smem_union = T <= kUnionMaxT && usmem <= 160 * 1024;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    const uint32_t chunk = uint32_t(std::max<size_t>(1, std::min<size_t>(a_in.nq, kListBudget / (size_t(lstride) * 4))));
+    const uint32_t cas_ctas = uint32_t(sms) * 4;
+    const size_t lists_bytes = size_t(chunk) * lstride * 4;
+    const size_t counts_bytes = (size_t(chunk) * 4 + 255) & ~size_t(255);
+    const size_t table_bytes = smem_union ? 0 : (size_t(cas_ctas) << tb) * 4;
+    if (!scratch) {
+        *scratch_bytes = lists_bytes + counts_bytes + table_bytes;
+        return HCG_OK;
+    }
+    if (a_in.nq == 0) return HCG_OK;
+    uint32_t* lists = static_cast<uint32_t*>(scratch);
+    uint32_t* counts = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(scratch) + lists_bytes);
+    uint32_t* gtab = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(scratch) + lists_bytes + counts_bytes);
+    constexpr int MINB = R <= 2 ? 4 : 2;
+    auto gk = k_gather<R, CR, MINB>;
+    static bool cfg_u[64] = {};
+    if (smem_union) HCG_RET_IF(opt_in_smem(k_union, device, cfg_u));
+    int g_per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_per_sm, gk, kRefineThreads, 0);
+    for (uint32_t q0 = 0; q0 < a_in.nq; q0 += chunk) {
+        RefineArgs a = a_in;
+        a.nq = std::min(chunk, a_in.nq - q0);
+        a.queries = a_in.queries + uint64_t(q0) * a_in.pitch;
+        a.begins = a_in.begins + uint64_t(q0) * a_in.C;
+        if (a.out_ids) a.out_ids += uint64_t(q0) * (a_in.mode == kOutCandidates ? a_in.cap : a_in.k);
+        if (a.out_sqdist) a.out_sqdist += uint64_t(q0) * a_in.k;
+        if (a.out_len) a.out_len += q0;
+        if (a.out_packed) a.out_packed += uint64_t(q0) * a_in.k;
+        if (smem_union) {
             const uint32_t ugrid = persistent_grid(reinterpret_cast<const void*>(k_union), usmem, device, a.nq);
             k_union<<<ugrid, kRefineThreads, usmem, st>>>(a, lists, counts, lstride, utb);
-            HCG_RET_IF(check_launch("k_union"));
+        } else {
+            k_union_cas<<<std::min(a.nq, cas_ctas), kRefineThreads, 0, st>>>(a, lists, counts, lstride, tb, gtab);
+        }
+        HCG_RET_IF(check_launch("candidate union"));
+        if (a.ev_mid && q0 + chunk >= a_in.nq) cudaEventRecord(a.ev_mid, st);
+        if (a.mode == kOutCandidates) {
             k_lists_to_ids<<<a.nq, 128, 0, st>>>(a, lists, counts, lstride);
-            return check_launch("k_lists_to_ids");
+            HCG_RET_IF(check_launch("k_lists_to_ids"));
+            continue;
         }
-        constexpr int MINB = R <= 2 ? 4 : 2;
-        int sms = 148;
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-        if (env_int("HCG_REFINE_FUSED", 0)) {
-            auto kern = k_refine_fused<R, CR, MINB>;
-            static bool cfg_f[64] = {};
-            HCG_RET_IF(opt_in_smem(kern, device, cfg_f));
-            int per_sm = 1;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRefineThreads, usmem);
-            per_sm = std::max(per_sm, 2);
-            const int u_sm = std::min(env_int("HCG_UNION_PER_SM", 1), per_sm - 1);
-            const uint32_t n_union = std::min<uint32_t>(a.nq, uint32_t(sms * u_sm));
-            const uint32_t n_gather = std::min<uint32_t>((a.nq + 7) / 8, uint32_t(sms * (per_sm - u_sm)));
-            HCG_RET_IF(cudaMemsetAsync(flags, 0, size_t(a.nq) * 4, st) == cudaSuccess
-                           ? HCG_OK : set_error(HCG_ECUDA, "flags memset"));
-            kern<<<n_union + n_gather, kRefineThreads, usmem, st>>>(a, lists, counts, lstride, utb, n_union, flags, 1u);
-            return check_launch("k_refine_fused");
-        }
-        static bool cfg_u[64] = {};
-        HCG_RET_IF(opt_in_smem(k_union, device, cfg_u));
-        const uint32_t ugrid = persistent_grid(reinterpret_cast<const void*>(k_union), usmem, device, a.nq);
-        k_union<<<ugrid, kRefineThreads, usmem, st>>>(a, lists, counts, lstride, utb);
-        HCG_RET_IF(check_launch("k_union"));
-        if (a.ev_mid) cudaEventRecord(a.ev_mid, st);
-        auto kern = k_gather<R, CR, MINB>;
-        int per_sm = 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRefineThreads, 0);
-        const uint32_t blocks = std::min<uint32_t>((a.nq + 7) / 8, uint32_t(sms * std::max(per_sm, 1)));
-        kern<<<blocks, kRefineThreads, 0, st>>>(a, lists, counts, lstride);
-        return check_launch("k_gather");
+        const uint32_t blocks = std::min<uint32_t>((a.nq + 7) / 8, uint32_t(sms * std::max(g_per_sm, 1)));
+        gk<<<blocks, kRefineThreads, 0, st>>>(a, lists, counts, lstride);
+        HCG_RET_IF(check_launch("k_gather"));
     }
-    const bool gtab = size_t(T) * 4 + (size_t(4) << tb) > 160 * 1024;
-    if (tb > 30) return set_error(HCG_ECAPACITY, "candidate set too large");
-    if (scratch && a.nq == 0) return HCG_OK;
-    return cas_launch<R, CR>(a, tb, gtab, scratch, scratch_bytes, device, st);
+    return HCG_OK;
 }
 
 template <int R>

@@ -108,6 +108,21 @@ def test_uniform_bytes_ties_and_uneven_scheme():
                 _check_search(gi, oi, view, qs, 12, depth)
 
 
+def test_very_large_candidate_sets():
+    """curves x depth beyond the shared-memory union (global CAS table path)."""
+    rows = P.gen_rows(0, 6000)
+    qs = P.gen_queries(0, 24, 6000)
+    for curves, m, depth in ((16, 8, 5000), (8, 16, 4096)):
+        gi = H.MulticurvesIndex(rows, H.default_scheme(128, curves, m), H.LIFTED if m == 16 else H.RAW)
+        view = H.LIFTED if m == 16 else H.RAW
+        oi = _oracle(rows, view, curves, m, H.HILBERT)
+        _check_search(gi, oi, view, qs, 10, depth)
+        _check_search(gi, oi, view, qs, 100, depth)
+        cands = gi.candidates(qs[:3], depth)
+        for q in range(3):
+            np.testing.assert_array_equal(cands[q], oi.candidates(view.floats(qs[q]), depth))
+
+
 def test_tiny_and_empty_indexes():
     rows = P.gen_rows(0, 5)
     qs = P.gen_queries(0, 4, 5)

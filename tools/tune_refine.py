@@ -26,23 +26,3 @@ gat = sorted(x[2] for x in t)[4]
 ref = uni + gat
 print(f"depth={D} k={k} U={U.mean():.1f} locate_ms={loc:.3f} union_ms={uni:.3f} gather_ms={gat:.3f} "
       f"refine_ms={ref:.3f} refine_GB/s={bytes_ / ref / 1e6:.0f}", flush=True)
-
-if os.environ.get("FUSED_SWEEP"):
-    for mode, fused, usm in (("0", "0", "1"), ("1", "0", "1"), ("1", "1", "1"), ("0", "0", "1"), ("1", "0", "1")):
-        os.environ["HCG_REFINE_MODE"] = mode
-        os.environ["HCG_REFINE_FUSED"] = fused
-        os.environ["HCG_UNION_PER_SM"] = usm
-        for b in range(2):
-            ix.search_timed(qs[b], k, D, out=out)
-        ms = sorted(sum(ix.search_timed(qs[b % 4], k, D, out=out)[1:]) for b in range(6))[3]
-        print(f"mode={mode} fused={fused} union_per_sm={usm} refine_ms={ms:.3f} GB/s={bytes_ / ms / 1e6:.0f}", flush=True)
-
-if os.environ.get("TB_SWEEP"):
-    os.environ["HCG_REFINE_MODE"] = "1"
-    os.environ["HCG_REFINE_FUSED"] = "0"
-    for extra in ("0", "1", "2", "0", "1", "2"):
-        os.environ["HCG_UNION_TB_EXTRA"] = extra
-        for b in range(2):
-            ix.search_timed(qs[b], k, D, out=out)
-        ms = sorted(sum(ix.search_timed(qs[b % 4], k, D, out=out)[1:]) for b in range(6))[3]
-        print(f"union_tb_extra={extra} refine_ms={ms:.3f}", flush=True)
