@@ -184,58 +184,6 @@ __device__ __forceinline__ void cp_async4(void* smem_dst, const void* src) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
-// Gather U list entries per group of 8 lanes (one 128-B row per lane group,
-// 16 B per lane and chunk), exact squared L2 with vabsdiff4 + dp4a, a
-// reduce-scatter over the group so lane l8 holds row h*8+l8, and the per-warp
-// top-k.  A warp covers list[e0 .. e0 + 4U).
-template <int R, int CR, int U>
-__device__ __forceinline__ void gather_rows(const RefineArgs& a, const uint32_t* list, uint32_t e0, uint32_t n,
-                                            const uint4 (&qv)[CR], uint32_t chunks, int lane, WarpTopK<R>& tk) {
-    const int l8 = lane & 7, grp = lane >> 3;
-    const uint32_t g0 = e0 + grp * U;
-    uint32_t sl[U];
-#pragma unroll
-    for (int r = 0; r < U; ++r) sl[r] = g0 + r < n ? list[g0 + r] : kEmpty;
-    uint4 v[U][CR];
-#pragma unroll
-    for (int r = 0; r < U; ++r) {
-#pragma unroll
-        for (int t = 0; t < CR; ++t) {
-            const uint32_t ch = l8 + 8 * t;
-            v[r][t] = (sl[r] != kEmpty && ch < chunks) ? ldg_stream(a.rows + uint64_t(sl[r]) * a.pitch + ch * 16)
-                                                       : make_uint4(0, 0, 0, 0);
-        }
-    }
-#pragma unroll
-    for (int h = 0; h < U / 8; ++h) {
-        uint32_t acc[8];
-#pragma unroll
-        for (int r = 0; r < 8; ++r) {
-            acc[r] = 0;
-#pragma unroll
-            for (int t = 0; t < CR; ++t) acc[r] = sad2_16(v[h * 8 + r][t], qv[t], acc[r]);
-        }
-        const bool b2 = l8 & 4, b1 = l8 & 2, b0 = l8 & 1;
-        uint32_t s4[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const uint32_t send = b2 ? acc[i] : acc[i + 4];
-            const uint32_t keep = b2 ? acc[i + 4] : acc[i];
-            s4[i] = keep + __shfl_xor_sync(kFull, send, 4);
-        }
-        uint32_t s2[2];
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-            const uint32_t send = b1 ? s4[i] : s4[i + 2];
-            const uint32_t keep = b1 ? s4[i + 2] : s4[i];
-            s2[i] = keep + __shfl_xor_sync(kFull, send, 2);
-        }
-        const uint32_t S = (b0 ? s2[1] : s2[0]) + __shfl_xor_sync(kFull, b0 ? s2[0] : s2[1], 1);
-        const uint32_t e = g0 + h * 8 + l8;
-        const uint32_t me = e < n ? list[e] : kEmpty;
-        tk.offer(me != kEmpty ? ((uint64_t(S) << 32) | me) : kNone, lane);
-    }
-}
 
 // Exclusive scan of one value per thread over a 256-thread block (ends with a barrier).
 __device__ __forceinline__ uint32_t block_excl_scan256_u(uint32_t v, uint32_t* wsum) {
@@ -379,90 +327,133 @@ __global__ void __launch_bounds__(kRefineThreads) k_union(RefineArgs a, uint32_t
 // per lane); the next pass's slots are prefetched while the rows load.  The
 // reduce-scatter leaves row (8*grp + l8)'s squared distance in lane l8 of
 // group grp, which offers (sqdist << 32 | slot) to the warp top-k.
-// One warp scoring queries q0, q0 + qstep, ...  Lists are read with
-// ld.global.cg (L2): they were written by the preceding union launch.
+// Score list entries [start, start+32), [start+step, ...) of one query into a
+// warp top-k: the 4 groups of 8 lanes own 8 rows each per pass (one 16-B chunk
+// per lane and row, 8 LDG.128 in flight per lane) and the next pass's slots
+// are prefetched while the rows load.  The reduce-scatter leaves row
+// (8*grp + l8)'s squared distance in lane l8 of group grp, which offers
+// (sqdist << 32 | slot).  Lists are read with ld.global.cg: they were written
+// by the preceding union launch.
 template <int R, int CR>
-__device__ __forceinline__ void gather_warp(const RefineArgs& a, const uint32_t* lists, const uint32_t* counts,
-                                            uint32_t lstride, uint32_t q0, uint32_t qstep) {
-    const int lane = threadIdx.x & 31, l8 = lane & 7, grp = lane >> 3;
+__device__ __forceinline__ void gather_list(const RefineArgs& a, const uint32_t* list, uint32_t n, uint32_t start,
+                                            uint32_t step, const uint4 (&qv)[CR], int lane, WarpTopK<R>& tk) {
+    const int l8 = lane & 7, grp = lane >> 3;
     const uint32_t chunks = a.pitch >> 4;
-    for (uint32_t q = q0; q < a.nq; q += qstep) {
-        const uint32_t n = __ldcg(counts + q);
-        const uint32_t* list = lists + uint64_t(q) * lstride;
-        uint4 qv[CR];
-        const uint8_t* qrow = a.queries + uint64_t(q) * a.pitch;
+    uint32_t nx[8];
 #pragma unroll
-        for (int t = 0; t < CR; ++t) {
-            const uint32_t ch = l8 + 8 * t;
-            qv[t] = ch < chunks ? *reinterpret_cast<const uint4*>(qrow + ch * 16) : make_uint4(0, 0, 0, 0);
-        }
-        WarpTopK<R> tk;
-        tk.init(int(a.k));
-        uint32_t nx[8];
+    for (int r = 0; r < 8; ++r) {
+        const uint32_t e = start + grp * 8 + r;
+        nx[r] = e < n ? __ldcg(list + e) : kEmpty;
+    }
+    for (uint32_t base = start; base < n; base += step) {
+        uint32_t sl[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) sl[r] = nx[r];
+        uint4 v[8][CR];
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
-            const uint32_t e = grp * 8 + r;
+#pragma unroll
+            for (int t = 0; t < CR; ++t) {
+                const uint32_t ch = l8 + 8 * t;
+                v[r][t] = (sl[r] != kEmpty && ch < chunks) ? ldg_stream(a.rows + uint64_t(sl[r]) * a.pitch + ch * 16)
+                                                           : make_uint4(0, 0, 0, 0);
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const uint32_t e = base + step + grp * 8 + r;
             nx[r] = e < n ? __ldcg(list + e) : kEmpty;
         }
-        for (uint32_t base = 0; base < n; base += 32) {
-            uint32_t sl[8];
+        uint32_t acc[8];
 #pragma unroll
-            for (int r = 0; r < 8; ++r) sl[r] = nx[r];
-            uint4 v[8][CR];
+        for (int r = 0; r < 8; ++r) {
+            acc[r] = 0;
 #pragma unroll
-            for (int r = 0; r < 8; ++r) {
-#pragma unroll
-                for (int t = 0; t < CR; ++t) {
-                    const uint32_t ch = l8 + 8 * t;
-                    v[r][t] = (sl[r] != kEmpty && ch < chunks)
-                                  ? ldg_stream(a.rows + uint64_t(sl[r]) * a.pitch + ch * 16)
-                                  : make_uint4(0, 0, 0, 0);
-                }
-            }
-#pragma unroll
-            for (int r = 0; r < 8; ++r) {
-                const uint32_t e = base + 32 + grp * 8 + r;
-                nx[r] = e < n ? __ldcg(list + e) : kEmpty;
-            }
-            uint32_t acc[8];
-#pragma unroll
-            for (int r = 0; r < 8; ++r) {
-                acc[r] = 0;
-#pragma unroll
-                for (int t = 0; t < CR; ++t) acc[r] = sad2_16(v[r][t], qv[t], acc[r]);
-            }
-            const bool b2 = l8 & 4, b1 = l8 & 2, b0 = l8 & 1;
-            uint32_t s4[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const uint32_t send = b2 ? acc[i] : acc[i + 4];
-                const uint32_t keep = b2 ? acc[i + 4] : acc[i];
-                s4[i] = keep + __shfl_xor_sync(kFull, send, 4);
-            }
-            uint32_t s2[2];
-#pragma unroll
-            for (int i = 0; i < 2; ++i) {
-                const uint32_t send = b1 ? s4[i] : s4[i + 2];
-                const uint32_t keep = b1 ? s4[i + 2] : s4[i];
-                s2[i] = keep + __shfl_xor_sync(kFull, send, 2);
-            }
-            const uint32_t S = (b0 ? s2[1] : s2[0]) + __shfl_xor_sync(kFull, b0 ? s2[0] : s2[1], 1);
-            uint32_t me = sl[0];
-#pragma unroll
-            for (int r = 1; r < 8; ++r)
-                if (r == l8) me = sl[r];
-            tk.offer(me != kEmpty ? ((uint64_t(S) << 32) | me) : kNone, lane);
+            for (int t = 0; t < CR; ++t) acc[r] = sad2_16(v[r][t], qv[t], acc[r]);
         }
-        write_result<R>(a, q, tk, lane, n);
+        const bool b2 = l8 & 4, b1 = l8 & 2, b0 = l8 & 1;
+        uint32_t s4[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const uint32_t send = b2 ? acc[i] : acc[i + 4];
+            const uint32_t keep = b2 ? acc[i + 4] : acc[i];
+            s4[i] = keep + __shfl_xor_sync(kFull, send, 4);
+        }
+        uint32_t s2[2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const uint32_t send = b1 ? s4[i] : s4[i + 2];
+            const uint32_t keep = b1 ? s4[i + 2] : s4[i];
+            s2[i] = keep + __shfl_xor_sync(kFull, send, 2);
+        }
+        const uint32_t S = (b0 ? s2[1] : s2[0]) + __shfl_xor_sync(kFull, b0 ? s2[0] : s2[1], 1);
+        uint32_t me = sl[0];
+#pragma unroll
+        for (int r = 1; r < 8; ++r)
+            if (r == l8) me = sl[r];
+        tk.offer(me != kEmpty ? ((uint64_t(S) << 32) | me) : kNone, lane);
     }
 }
 
+template <int CR>
+__device__ __forceinline__ void load_query(const RefineArgs& a, uint32_t q, int lane, uint4 (&qv)[CR]) {
+    const uint32_t chunks = a.pitch >> 4;
+    const uint8_t* qrow = a.queries + uint64_t(q) * a.pitch;
+#pragma unroll
+    for (int t = 0; t < CR; ++t) {
+        const uint32_t ch = (lane & 7) + 8 * t;
+        qv[t] = ch < chunks ? *reinterpret_cast<const uint4*>(qrow + ch * 16) : make_uint4(0, 0, 0, 0);
+    }
+}
+
+// K3c for large batches: one WARP per query (persistent grid-stride), no
+// shared memory and no barriers.
 template <int R, int CR, int MINB>
 __global__ void __launch_bounds__(kRefineThreads, MINB) k_gather(RefineArgs a, const uint32_t* __restrict__ lists,
                                                                  const uint32_t* __restrict__ counts,
                                                                  uint32_t lstride) {
-    gather_warp<R, CR>(a, lists, counts, lstride, (blockIdx.x * kRefineThreads + threadIdx.x) >> 5,
-                       gridDim.x * (kRefineThreads / 32));
+    const int lane = threadIdx.x & 31;
+    const uint32_t qstep = gridDim.x * (kRefineThreads / 32);
+    for (uint32_t q = (blockIdx.x * kRefineThreads + threadIdx.x) >> 5; q < a.nq; q += qstep) {
+        const uint32_t n = __ldcg(counts + q);
+        uint4 qv[CR];
+        load_query<CR>(a, q, lane, qv);
+        WarpTopK<R> tk;
+        tk.init(int(a.k));
+        gather_list<R, CR>(a, lists + uint64_t(q) * lstride, n, 0, 32, qv, lane, tk);
+        write_result<R>(a, q, tk, lane, n);
+    }
+}
+
+// K3c for small batches (latency): one CTA per query, the 8 warps split the
+// list and warp 0 merges their top-k lists through shared memory.
+template <int R, int CR>
+__global__ void __launch_bounds__(kRefineThreads) k_gather_cta(RefineArgs a, const uint32_t* __restrict__ lists,
+                                                               const uint32_t* __restrict__ counts, uint32_t lstride) {
+    constexpr int KCAP = 32 * R;
+    constexpr int kWarps = kRefineThreads / 32;
+    __shared__ uint64_t mbuf[kWarps * KCAP];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (uint32_t q = blockIdx.x; q < a.nq; q += gridDim.x) {
+        const uint32_t n = __ldcg(counts + q);
+        uint4 qv[CR];
+        load_query<CR>(a, q, lane, qv);
+        WarpTopK<R> tk;
+        tk.init(int(a.k));
+        gather_list<R, CR>(a, lists + uint64_t(q) * lstride, n, warp * 32, kRefineThreads, qv, lane, tk);
+#pragma unroll
+        for (int r = 0; r < R; ++r) mbuf[warp * KCAP + lane * R + r] = tk.a[r];
+        __syncthreads();
+        if (warp == 0) {
+            WarpTopK<R> fin;
+            fin.init(int(a.k));
+            const uint32_t kr = (a.k + 31) & ~31u;
+            for (int w = 0; w < kWarps; ++w)
+                for (uint32_t i = 0; i < kr; i += 32) fin.offer(mbuf[w * KCAP + i + lane], lane);
+            write_result<R>(a, q, fin, lane, n);
+        }
+        __syncthreads();
+    }
 }
 
 // Candidate-union tap: unique slots -> ids.
@@ -613,6 +604,12 @@ hcg_status refine_dispatch(const RefineArgs& a_in, void* scratch, size_t* scratc
         if (a.mode == kOutCandidates) {
             k_lists_to_ids<<<a.nq, 128, 0, st>>>(a, lists, counts, lstride);
             HCG_RET_IF(check_launch("k_lists_to_ids"));
+            continue;
+        }
+        if (a.nq * 2 < uint32_t(sms) * uint32_t(std::max(g_per_sm, 1)) * 8) {
+            // fewer queries than half the resident warps: spread each query over a CTA (latency)
+            k_gather_cta<R, CR><<<a.nq, kRefineThreads, 0, st>>>(a, lists, counts, lstride);
+            HCG_RET_IF(check_launch("k_gather_cta"));
             continue;
         }
         const uint32_t blocks = std::min<uint32_t>((a.nq + 7) / 8, uint32_t(sms * std::max(g_per_sm, 1)));
