@@ -27,6 +27,10 @@
  *
  *   hcg_miss_bound /   equivalence module: binomial_tail / miss_bound / plan_depth
  *   hcg_plan_depth
+ *   hcg_insert         hc::MulticurvesIndex::insert, batched (multicurves.hpp:79)
+ *   hcg_save/hcg_load  hc::MulticurvesIndex::save / load (multicurves.hpp:96-98)
+ *   hcg_read_vectors / hc::read_vectors / write_vectors (proj/src/vecio.cpp:18-85)
+ *   hcg_write_vectors
  *   hcg_gen_rows /     the counter-based synthetic SIFT-like generator of
  *   hcg_gen_queries    SURVEY.md §8(d) (bench/test data; bit-identical to the oracle)
  *
@@ -66,7 +70,8 @@ typedef enum hcg_status {
     HCG_ENONFINITE = -3,  /* NaN/Inf component (curve.cpp:167)                        */
     HCG_ENOMEM = -4,      /* device allocation failed                                  */
     HCG_ECUDA = -5,       /* CUDA runtime error                                        */
-    HCG_ENODEV = -6       /* no usable sm_100 device                                   */
+    HCG_ENODEV = -6,      /* no usable sm_100 device                                   */
+    HCG_EIO = -7          /* file I/O or format error (reference: std::runtime_error)  */
 } hcg_status;
 
 typedef enum hcg_curve_kind { HCG_ZORDER = 0, HCG_HILBERT = 1 } hcg_curve_kind;
@@ -148,6 +153,29 @@ hcg_status hcg_search_packed(const hcg_index* index, const uint8_t* queries, uin
 hcg_status hcg_merge_packed(const uint64_t* packed, uint32_t parts, uint32_t nq, uint32_t k,
                             uint64_t* out_ids, uint32_t* out_sqdist, uint32_t* out_len, int device,
                             void* stream);
+
+/* Append n rows (ids continue the affine sequence: id_base + s * id_stride for
+ * s = size..size+n-1) and merge their keys into every curve.  The result is
+ * identical to building over the union (SPEC.md:227-235 order independence).
+ * Exclusive with searches on the same index. */
+hcg_status hcg_insert(hcg_index* index, const uint8_t* rows, uint64_t n, void* stream);
+
+/* Little-endian binary persistence (SPEC.md:268 leaves the layout open):
+ * "HCGIDX" header with the scheme, n, ids and view, the descriptor rows, then
+ * per curve its common key prefix and the sorted (suffix key, slot) arrays.
+ * Round-trips bit-exactly (tests/test_gpu_formats.py). */
+hcg_status hcg_save(const hcg_index* index, const char* path);
+hcg_status hcg_load(const char* path, int device, void* stream, hcg_index** out);
+
+/* ---- bvecs / fvecs records (vecio.cpp:18-85): u32 LE dim + payload ---- */
+typedef enum hcg_vector_format { HCG_FVECS = 0, HCG_BVECS = 1 } hcg_vector_format;
+/* *rows_out (n x dim bytes) is malloc'ed; release with hcg_free_buffer.  fvecs
+ * components must be byte values of the view offset + b * scale. */
+hcg_status hcg_read_vectors(const char* path, uint32_t format, float offset, float scale, uint8_t** rows_out,
+                            uint64_t* n_out, uint32_t* dim_out);
+hcg_status hcg_write_vectors(const char* path, uint32_t format, float offset, float scale, const uint8_t* rows,
+                             uint64_t n, uint32_t dim);
+void hcg_free_buffer(void* p);
 
 /* ---- parity taps ---- */
 /* Full-width keys (hcg_key_words words per key, least significant word first,

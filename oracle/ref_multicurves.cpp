@@ -380,3 +380,17 @@ int ref_select_top_k(const std::uint64_t* ids, const double* sq, std::uint64_t n
 }
 
 }  // extern "C"
+
+// ---- vecio round trip through the reference's own reader (vecio.cpp:18-61) ----
+extern "C" int ref_read_vectors(const char* path, int bvecs, float* out, std::uint64_t cap, std::uint64_t* n,
+                                std::uint32_t* dim) {
+    return guard([&] {
+        const auto ds = hc::read_vectors(path, bvecs ? hc::VectorFormat::bvecs : hc::VectorFormat::fvecs);
+        *n = ds.size();
+        *dim = ds.dims;
+        std::uint64_t k = 0;
+        for (const auto& v : ds.vectors)
+            for (float x : v.components)
+                if (k < cap) out[k++] = x;
+    });
+}

@@ -17,6 +17,9 @@ HCG_ENONFINITE = -3
 HCG_ENOMEM = -4
 HCG_ECUDA = -5
 HCG_ENODEV = -6
+HCG_EIO = -7
+HCG_FVECS = 0
+HCG_BVECS = 1
 
 HCG_ZORDER = 0
 HCG_HILBERT = 1
@@ -29,7 +32,8 @@ EXPORTS = [
     "hcg_free", "hcg_size", "hcg_curves", "hcg_key_words", "hcg_device_bytes", "hcg_search",
     "hcg_search_timed", "hcg_search_packed", "hcg_merge_packed", "hcg_keys", "hcg_sorted", "hcg_windows",
     "hcg_candidates", "hcg_brute_force", "hcg_binomial_tail", "hcg_miss_bound",
-    "hcg_plan_depth", "hcg_gen_rows", "hcg_gen_queries",
+    "hcg_plan_depth", "hcg_gen_rows", "hcg_gen_queries", "hcg_insert", "hcg_save", "hcg_load",
+    "hcg_read_vectors", "hcg_write_vectors", "hcg_free_buffer",
 ]
 
 
@@ -54,6 +58,10 @@ class HcgError(RuntimeError):
 
 class HcgInvalidArgument(HcgError, ValueError):
     """Mirrors the reference's std::invalid_argument (curve.cpp:35-59, vecio.cpp:15,78,88,116)."""
+
+
+class HcgIOError(HcgError):
+    """Mirrors the reference's std::runtime_error for I/O (vecio.cpp:20-84)."""
 
 
 _lib = None
@@ -101,9 +109,17 @@ def lib() -> C.CDLL:
     L.hcg_plan_depth.argtypes = [u32, u32, C.c_double]
     L.hcg_gen_rows.argtypes = [u64, u64, u64, vp, C.c_int, vp]
     L.hcg_gen_queries.argtypes = [u64, u64, u64, vp, C.c_int, vp]
+    L.hcg_insert.argtypes = [vp, vp, u64, vp]
+    L.hcg_save.argtypes = [vp, C.c_char_p]
+    L.hcg_load.argtypes = [C.c_char_p, C.c_int, vp, P(vp)]
+    L.hcg_read_vectors.argtypes = [C.c_char_p, u32, C.c_float, C.c_float, P(P(C.c_uint8)), P(u64), P(u32)]
+    L.hcg_write_vectors.argtypes = [C.c_char_p, u32, C.c_float, C.c_float, vp, u64, u32]
+    L.hcg_free_buffer.argtypes = [vp]
+    L.hcg_free_buffer.restype = None
     for name in ("hcg_make_lut", "hcg_default_assignment", "hcg_build", "hcg_free", "hcg_search",
                  "hcg_search_timed", "hcg_search_packed", "hcg_merge_packed", "hcg_keys", "hcg_sorted", "hcg_windows",
-                 "hcg_candidates", "hcg_brute_force", "hcg_gen_rows", "hcg_gen_queries"):
+                 "hcg_candidates", "hcg_brute_force", "hcg_gen_rows", "hcg_gen_queries", "hcg_insert",
+                 "hcg_save", "hcg_load", "hcg_read_vectors", "hcg_write_vectors"):
         getattr(L, name).restype = C.c_int
     del u8
     _lib = L
@@ -116,4 +132,6 @@ def check(rc: int) -> None:
     msg = lib().hcg_last_error().decode(errors="replace")
     if rc in (HCG_EINVAL, HCG_ECAPACITY, HCG_ENONFINITE):
         raise HcgInvalidArgument(rc, msg)
+    if rc == HCG_EIO:
+        raise HcgIOError(rc, msg)
     raise HcgError(rc, msg)

@@ -253,7 +253,66 @@ hcg_status check_device(int device) {
     return HCG_OK;
 }
 
-// Build curve c: K1 keys, prefix detection, K2 stable radix sort, suffix pack.
+// Keys of `count` rows (K1) as SoA words plus their OR / AND over all rows.
+hcg_status keygen_reduce(const hcg_index* ix, uint32_t c, const uint8_t* rows, uint64_t count, Scratch& sc,
+                         uint64_t** soa, std::vector<uint64_t>& oa) {
+    const uint32_t d = ix->off[c + 1] - ix->off[c];
+    const uint32_t W = (d * ix->m + 63) / 64;
+    *soa = sc.alloc<uint64_t>(size_t(W) * count);
+    unsigned long long* or_and = sc.alloc<unsigned long long>(2 * W);
+    if (!*soa || !or_and) return set_error(HCG_ENOMEM, "key buffers");
+    HCG_TRY_CUDA(cudaMemsetAsync(or_and, 0, W * 8, sc.st));
+    HCG_TRY_CUDA(cudaMemsetAsync(or_and + W, 0xFF, W * 8, sc.st));
+    HCG_TRY(keygen_rows(rows, count, ix->pitch, ix->d_assign + ix->off[c], int(d), int(ix->m), int(ix->kind),
+                        ix->d_lut, *soa, int(W), or_and, ix->dmax, sc.st));
+    oa.assign(2 * W, 0);
+    HCG_TRY_CUDA(cudaMemcpyAsync(oa.data(), or_and, 2 * W * 8, cudaMemcpyDeviceToHost, sc.st));
+    HCG_TRY_CUDA(cudaStreamSynchronize(sc.st));
+    return HCG_OK;
+}
+
+// K2: stable LSD radix sort of `count` keys (SoA, W words) by their bits
+// [0, hv] (only the 8-bit digits that vary over `oa`), then pack the sorted
+// suffixes (AoS, ws words) into *keys_out and slot_base + position into
+// *slots_out (both allocated here, owned by the index).
+hcg_status sort_suffix(hcg_index* ix, const uint64_t* soa, uint64_t count, uint32_t W, const std::vector<uint64_t>& oa,
+                       uint32_t hv, uint64_t slot_base, Scratch& sc, uint64_t** keys_out, uint32_t** slots_out) {
+    const int hw = int(hv >> 6), hb = int(hv & 63);
+    const uint64_t below = hb == 63 ? ~0ull : ((2ull << hb) - 1);
+    const uint32_t ws = uint32_t(hw + 1);
+    cudaStream_t st = sc.st;
+    uint64_t* kb = sc.alloc<uint64_t>(count);
+    uint64_t* ka = sc.alloc<uint64_t>(count);
+    uint32_t* va = sc.alloc<uint32_t>(count);
+    uint32_t* vb = sc.alloc<uint32_t>(count);
+    uint32_t* counts = reinterpret_cast<uint32_t*>(sc.alloc<uint8_t>(radix_counts_bytes(count)));
+    if (!kb || !ka || !va || !vb || !counts) return set_error(HCG_ENOMEM, "sort buffers");
+    uint32_t* totals = counts + (radix_counts_bytes(count) / 4 - 256);
+    uint32_t* v = vb;
+    uint32_t* v_alt = va;
+    launch_iota(v, count, 0, st);
+    for (uint32_t w = 0; w <= uint32_t(hw); ++w) {
+        uint64_t vary = oa[w] ^ oa[W + w];
+        if (int(w) == hw) vary &= below;
+        uint32_t dmask = 0;
+        for (int sft = 0; sft < 8; ++sft)
+            if ((vary >> (8 * sft)) & 0xFF) dmask |= 1u << sft;
+        if (!dmask) continue;
+        launch_gather_word(soa + uint64_t(w) * count, v, kb, count, st);
+        uint64_t* k = kb;
+        uint64_t* k_alt = ka;
+        HCG_TRY(radix_sort_pairs(&k, &v, &k_alt, &v_alt, count, dmask, counts, totals, st));
+        kb = k;
+        ka = k_alt;
+    }
+    HCG_TRY(dev_alloc(keys_out, size_t(count) * ws, &ix->bytes));
+    HCG_TRY(dev_alloc(slots_out, count, &ix->bytes));
+    launch_pack_suffix(soa, v, count, int(ws), below, *keys_out, st);
+    launch_offset(v, *slots_out, count, uint32_t(slot_base), st);
+    return check_launch("pack suffix");
+}
+
+// Build curve c over all rows: K1 keys, common-prefix detection, K2 sort.
 hcg_status build_curve(hcg_index* ix, uint32_t c, cudaStream_t st) {
     const uint64_t n = ix->n;
     const uint32_t d = ix->off[c + 1] - ix->off[c];
@@ -268,17 +327,9 @@ hcg_status build_curve(hcg_index* ix, uint32_t c, cudaStream_t st) {
         return HCG_OK;
     }
     Scratch sc(st);
-    uint64_t* keys_soa = sc.alloc<uint64_t>(size_t(W) * n);
-    unsigned long long* or_and = sc.alloc<unsigned long long>(2 * W);
-    if (!keys_soa || !or_and) return set_error(HCG_ENOMEM, "key buffers");
-    HCG_TRY_CUDA(cudaMemsetAsync(or_and, 0, W * 8, st));
-    HCG_TRY_CUDA(cudaMemsetAsync(or_and + W, 0xFF, W * 8, st));
-    HCG_TRY(keygen_rows(ix->rows, n, ix->pitch, ix->d_assign + ix->off[c], int(d), int(ix->m), int(ix->kind),
-                        ix->d_lut, keys_soa, int(W), or_and, ix->dmax, st));
-    std::vector<uint64_t> oa(2 * W);
-    HCG_TRY_CUDA(cudaMemcpyAsync(oa.data(), or_and, 2 * W * 8, cudaMemcpyDeviceToHost, st));
-    HCG_TRY_CUDA(cudaStreamSynchronize(st));
-
+    uint64_t* soa = nullptr;
+    std::vector<uint64_t> oa;
+    HCG_TRY(keygen_reduce(ix, c, ix->rows, n, sc, &soa, oa));
     int hv = 0;
     for (int w = int(W) - 1; w >= 0; --w) {
         const uint64_t vary = oa[w] ^ oa[W + w];
@@ -289,49 +340,131 @@ hcg_status build_curve(hcg_index* ix, uint32_t c, cudaStream_t st) {
     }
     const int hw = hv >> 6, hb = hv & 63;
     const uint64_t above = hb == 63 ? 0ull : (~0ull << (hb + 1));
-    const uint64_t below = hb == 63 ? ~0ull : ((2ull << hb) - 1);
     cv.hv = uint32_t(hv);
     cv.ws = uint32_t(hw + 1);
     for (uint32_t w = 0; w < W; ++w)
         cv.prefix[w] = int(w) > hw ? oa[w] : (int(w) == hw ? (oa[w] & above) : 0ull);
-
-    uint64_t* kb = sc.alloc<uint64_t>(n);
-    uint64_t* ka = sc.alloc<uint64_t>(n);
-    uint32_t* va = sc.alloc<uint32_t>(n);
-    uint32_t* vb = nullptr;
-    uint32_t* counts = reinterpret_cast<uint32_t*>(sc.alloc<uint8_t>(radix_counts_bytes(n)));
-    if (!kb || !ka || !va || !counts) return set_error(HCG_ENOMEM, "sort buffers");
-    HCG_TRY(dev_alloc(&vb, n, &ix->bytes));  // becomes (or swaps into) the resident slots array
-    uint32_t* totals = counts + (radix_counts_bytes(n) / 4 - 256);
-    uint32_t* v = vb;
-    uint32_t* v_alt = va;
-    launch_iota(v, n, st);
-    for (uint32_t w = 0; w <= uint32_t(hw); ++w) {
-        uint64_t vary = oa[w] ^ oa[W + w];
-        if (int(w) == hw) vary &= below;
-        uint32_t dmask = 0;
-        for (int s = 0; s < 8; ++s)
-            if ((vary >> (8 * s)) & 0xFF) dmask |= 1u << s;
-        if (!dmask) continue;
-        launch_gather_word(keys_soa + uint64_t(w) * n, v, kb, n, st);
-        uint64_t* k = kb;
-        uint64_t* k_alt = ka;
-        HCG_TRY(radix_sort_pairs(&k, &v, &k_alt, &v_alt, n, dmask, counts, totals, st));
-        kb = k;
-        ka = k_alt;
-    }
-    HCG_TRY(dev_alloc(&ix->keys[c], size_t(n) * cv.ws, &ix->bytes));
-    launch_pack_suffix(keys_soa, v, n, int(cv.ws), below, ix->keys[c], st);
-    HCG_TRY(check_launch("pack suffix"));
-    if (v == vb) {
-        ix->slots[c] = vb;
-    } else {  // result landed in the scratch buffer: copy into the resident array
-        HCG_TRY_CUDA(cudaMemcpyAsync(vb, v, n * 4, cudaMemcpyDeviceToDevice, st));
-        ix->slots[c] = vb;
-    }
+    HCG_TRY(sort_suffix(ix, soa, n, W, oa, cv.hv, 0, sc, &ix->keys[c], &ix->slots[c]));
     cv.keys = ix->keys[c];
     cv.slots = ix->slots[c];
     HCG_TRY_CUDA(cudaStreamSynchronize(st));
+    return HCG_OK;
+}
+
+void dev_free(void* p, size_t bytes, uint64_t* total) {
+    if (p) {
+        cudaFree(p);
+        *total -= std::min<uint64_t>(*total, bytes);
+    }
+}
+
+// Insert `nb` rows (already appended to ix->rows at slots n_old..) into curve
+// c.  When the new keys share the curve's common prefix, they are sorted on
+// their own and rank-merged into the resident arrays (stable: resident
+// entries first on equal keys, i.e. id order); otherwise the curve is rebuilt.
+hcg_status insert_curve(hcg_index* ix, uint32_t c, uint64_t n_old, uint64_t nb, cudaStream_t st) {
+    CurveDev& cv = ix->curves[c];
+    if (n_old == 0) return build_curve(ix, c, st);
+    const uint32_t W = cv.w;
+    Scratch sc(st);
+    uint64_t* soa = nullptr;
+    std::vector<uint64_t> oa;
+    HCG_TRY(keygen_reduce(ix, c, ix->rows + uint64_t(n_old) * ix->pitch, nb, sc, &soa, oa));
+    const int hw = int(cv.hv >> 6), hb = int(cv.hv & 63);
+    const uint64_t above = hb == 63 ? 0ull : (~0ull << (hb + 1));
+    bool compatible = true;
+    for (uint32_t w = uint32_t(hw); w < W; ++w) {
+        const uint64_t m = int(w) == hw ? above : ~0ull;
+        if ((oa[w] & m) != cv.prefix[w] || (oa[W + w] & m) != cv.prefix[w]) compatible = false;
+    }
+    if (!compatible) {
+        dev_free(ix->keys[c], size_t(n_old) * cv.ws * 8, &ix->bytes);
+        dev_free(ix->slots[c], size_t(n_old) * 4, &ix->bytes);
+        ix->keys[c] = nullptr;
+        ix->slots[c] = nullptr;
+        return build_curve(ix, c, st);
+    }
+    uint64_t* nk = nullptr;
+    uint32_t* ns = nullptr;
+    HCG_TRY(sort_suffix(ix, soa, nb, W, oa, cv.hv, n_old, sc, &nk, &ns));
+    uint64_t* mk = nullptr;
+    uint32_t* ms = nullptr;
+    HCG_TRY(dev_alloc(&mk, size_t(n_old + nb) * cv.ws, &ix->bytes));
+    HCG_TRY(dev_alloc(&ms, n_old + nb, &ix->bytes));
+    launch_rank_merge(ix->keys[c], ix->slots[c], n_old, nk, ns, nb, int(cv.ws), mk, ms, st);
+    HCG_TRY(check_launch("rank merge"));
+    HCG_TRY_CUDA(cudaStreamSynchronize(st));
+    dev_free(ix->keys[c], size_t(n_old) * cv.ws * 8, &ix->bytes);
+    dev_free(ix->slots[c], size_t(n_old) * 4, &ix->bytes);
+    dev_free(nk, size_t(nb) * cv.ws * 8, &ix->bytes);
+    dev_free(ns, size_t(nb) * 4, &ix->bytes);
+    ix->keys[c] = mk;
+    ix->slots[c] = ms;
+    cv.keys = mk;
+    cv.slots = ms;
+    return HCG_OK;
+}
+
+// Upload the curve table and slot pointers (after build / insert / load).
+hcg_status publish_tables(hcg_index* ix, cudaStream_t st) {
+    uint32_t maxws = 1;
+    for (auto& cv : ix->curves) maxws = std::max(maxws, cv.ws);
+    ix->wsmax = pow2_bucket(maxws, 1, 16);
+    if (!ix->d_curves) HCG_TRY(dev_alloc(&ix->d_curves, ix->C, &ix->bytes));
+    if (!ix->d_slot_ptrs) HCG_TRY(dev_alloc(&ix->d_slot_ptrs, ix->C, &ix->bytes));
+    HCG_TRY_CUDA(cudaMemcpyAsync(ix->d_curves, ix->curves.data(), sizeof(CurveDev) * ix->C, cudaMemcpyHostToDevice, st));
+    HCG_TRY_CUDA(cudaMemcpyAsync(ix->d_slot_ptrs, ix->slots.data(), sizeof(uint32_t*) * ix->C, cudaMemcpyHostToDevice,
+                                 st));
+    HCG_TRY_CUDA(cudaStreamSynchronize(st));
+    return HCG_OK;
+}
+
+// Allocate an index for `s` with room for n rows (rows buffer allocated,
+// scheme uploaded); curves are filled by the caller (build / load).
+hcg_status new_index(const hcg_scheme* s, uint64_t n, uint64_t id_base, uint64_t id_stride, int device, cudaStream_t st,
+                     hcg_index** out) {
+    auto* ix = new hcg_index;
+    ix->device = device;
+    ix->d_full = s->d_full;
+    ix->pitch = round16(s->d_full);
+    ix->C = s->curves;
+    ix->m = s->bits_per_dim;
+    ix->kind = s->curve_kind;
+    ix->dist_scale = s->dist_scale;
+    ix->n = n;
+    ix->id_base = id_base;
+    ix->id_stride = id_stride;
+    ix->off.assign(s->assign_off, s->assign_off + s->curves + 1);
+    ix->assign.assign(s->assign, s->assign + ix->off[s->curves]);
+    std::memcpy(ix->lut, s->cell_lut, sizeof(ix->lut));
+    uint32_t maxd = 1;
+    for (uint32_t c = 0; c < ix->C; ++c) maxd = std::max(maxd, ix->off[c + 1] - ix->off[c]);
+    ix->dmax = pow2_bucket(maxd, 8, 128);
+    ix->curves.resize(ix->C);
+    for (uint32_t c = 0; c < ix->C; ++c) {
+        CurveDev& cv = ix->curves[c];
+        std::memset(&cv, 0, sizeof(cv));
+        cv.dims = ix->off[c + 1] - ix->off[c];
+        cv.w = (cv.dims * ix->m + 63) / 64;
+        cv.ws = 1;
+        cv.off = ix->off[c];
+    }
+    ix->keys.assign(ix->C, nullptr);
+    ix->slots.assign(ix->C, nullptr);
+    hcg_status rc = dev_alloc(&ix->rows, size_t(n) * ix->pitch, &ix->bytes);
+    if (rc == HCG_OK) rc = dev_alloc(&ix->d_lut, 256, &ix->bytes);
+    if (rc == HCG_OK) rc = dev_alloc(&ix->d_assign, ix->assign.size(), &ix->bytes);
+    std::vector<uint16_t> asg16(ix->assign.begin(), ix->assign.end());
+    if (rc == HCG_OK &&
+        (cudaMemcpyAsync(ix->d_lut, ix->lut, sizeof(ix->lut), cudaMemcpyHostToDevice, st) != cudaSuccess ||
+         cudaMemcpyAsync(ix->d_assign, asg16.data(), asg16.size() * 2, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+         cudaStreamSynchronize(st) != cudaSuccess))
+        rc = set_error(HCG_ECUDA, "copy scheme");
+    if (rc != HCG_OK) {
+        release(ix);
+        return rc;
+    }
+    *out = ix;
     return HCG_OK;
 }
 
@@ -404,6 +537,27 @@ hcg_status deliver(T* user, const std::vector<T>& v) {
 
 using namespace hcg;
 
+namespace {
+constexpr char kMagic[8] = {'H', 'C', 'G', 'I', 'D', 'X', 0, 1};
+constexpr char kTrailer[8] = {'H', 'C', 'G', 'E', 'N', 'D', 0, 0};
+constexpr uint32_t kFormatVersion = 1;
+
+struct FileCloser {
+    FILE* f = nullptr;
+    ~FileCloser() {
+        if (f) std::fclose(f);
+    }
+};
+template <class T>
+bool put(FILE* f, const T* p, size_t count) {
+    return count == 0 || std::fwrite(p, sizeof(T), count, f) == count;
+}
+template <class T>
+bool get(FILE* f, T* p, size_t count) {
+    return count == 0 || std::fread(p, sizeof(T), count, f) == count;
+}
+}  // namespace
+
 extern "C" {
 
 const char* hcg_last_error(void) { return g_err.c_str(); }
@@ -444,37 +598,14 @@ hcg_status hcg_build(const hcg_scheme* s, const uint8_t* rows, uint64_t n, uint6
     DeviceGuard g(device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
 
-    auto* ix = new hcg_index;
-    ix->device = device;
-    ix->d_full = s->d_full;
-    ix->pitch = round16(s->d_full);
-    ix->C = s->curves;
-    ix->m = s->bits_per_dim;
-    ix->kind = s->curve_kind;
-    ix->dist_scale = s->dist_scale;
-    ix->n = n;
-    ix->id_base = id_base;
-    ix->id_stride = id_stride;
-    ix->off.assign(s->assign_off, s->assign_off + s->curves + 1);
-    ix->assign.assign(s->assign, s->assign + ix->off[s->curves]);
-    std::memcpy(ix->lut, s->cell_lut, sizeof(ix->lut));
-    uint32_t maxd = 1;
-    for (uint32_t c = 0; c < ix->C; ++c) maxd = std::max(maxd, ix->off[c + 1] - ix->off[c]);
-    ix->dmax = pow2_bucket(maxd, 8, 128);
-    ix->curves.resize(ix->C);
-    ix->keys.assign(ix->C, nullptr);
-    ix->slots.assign(ix->C, nullptr);
-
+    hcg_index* ix = nullptr;
+    HCG_TRY(new_index(s, n, id_base, id_stride, device, st, &ix));
     auto fail = [&](hcg_status rc) {
         cudaStreamSynchronize(st);
         release(ix);
         return rc;
     };
     hcg_status rc;
-    if ((rc = dev_alloc(&ix->rows, size_t(n) * ix->pitch, &ix->bytes)) != HCG_OK) return fail(rc);
-    if ((rc = dev_alloc(&ix->d_lut, 256, &ix->bytes)) != HCG_OK) return fail(rc);
-    if ((rc = dev_alloc(&ix->d_assign, ix->assign.size(), &ix->bytes)) != HCG_OK) return fail(rc);
-    std::vector<uint16_t> asg16(ix->assign.begin(), ix->assign.end());
     if (n) {
         if (ix->pitch != ix->d_full && cudaMemsetAsync(ix->rows, 0, size_t(n) * ix->pitch, st) != cudaSuccess)
             return fail(set_error(HCG_ECUDA, "memset rows"));
@@ -482,23 +613,9 @@ hcg_status hcg_build(const hcg_scheme* s, const uint8_t* rows, uint64_t n, uint6
             cudaSuccess)
             return fail(set_error(HCG_ECUDA, std::string("copy rows: ") + cudaGetErrorString(cudaGetLastError())));
     }
-    if (cudaMemcpyAsync(ix->d_lut, ix->lut, sizeof(ix->lut), cudaMemcpyHostToDevice, st) != cudaSuccess ||
-        cudaMemcpyAsync(ix->d_assign, asg16.data(), asg16.size() * 2, cudaMemcpyHostToDevice, st) != cudaSuccess)
-        return fail(set_error(HCG_ECUDA, "copy scheme"));
     for (uint32_t c = 0; c < ix->C; ++c)
         if ((rc = build_curve(ix, c, st)) != HCG_OK) return fail(rc);
-    uint32_t maxws = 1;
-    for (auto& cv : ix->curves) maxws = std::max(maxws, cv.ws);
-    ix->wsmax = pow2_bucket(maxws, 1, 16);
-    if ((rc = dev_alloc(&ix->d_curves, ix->C, &ix->bytes)) != HCG_OK) return fail(rc);
-    if ((rc = dev_alloc(&ix->d_slot_ptrs, ix->C, &ix->bytes)) != HCG_OK) return fail(rc);
-    if (cudaMemcpyAsync(ix->d_curves, ix->curves.data(), sizeof(CurveDev) * ix->C, cudaMemcpyHostToDevice, st) !=
-            cudaSuccess ||
-        cudaMemcpyAsync(ix->d_slot_ptrs, ix->slots.data(), sizeof(uint32_t*) * ix->C, cudaMemcpyHostToDevice, st) !=
-            cudaSuccess)
-        return fail(set_error(HCG_ECUDA, "copy curve table"));
-    if (cudaStreamSynchronize(st) != cudaSuccess)
-        return fail(set_error(HCG_ECUDA, std::string("build: ") + cudaGetErrorString(cudaGetLastError())));
+    if ((rc = publish_tables(ix, st)) != HCG_OK) return fail(rc);
     *out = ix;
     return HCG_OK;
 }
@@ -512,6 +629,153 @@ uint64_t hcg_size(const hcg_index* ix) { return ix ? ix->n : 0; }
 uint32_t hcg_curves(const hcg_index* ix) { return ix ? ix->C : 0; }
 uint32_t hcg_key_words(const hcg_index* ix, uint32_t c) { return ix && c < ix->C ? ix->curves[c].w : 0; }
 uint64_t hcg_device_bytes(const hcg_index* ix) { return ix ? ix->bytes : 0; }
+
+hcg_status hcg_insert(hcg_index* ix, const uint8_t* rows, uint64_t nb, void* stream) {
+    HCG_TRY(check_index(ix));
+    if (nb == 0) return HCG_OK;
+    if (!rows) return set_error(HCG_EINVAL, "null rows");
+    const uint64_t n_old = ix->n, n_new = n_old + nb;
+    if (n_new >= (1ull << 32)) return set_error(HCG_ECAPACITY, "more than 2^32-1 rows in one index");
+    DeviceGuard g(ix->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    uint8_t* nr = nullptr;
+    HCG_TRY(dev_alloc(&nr, size_t(n_new) * ix->pitch, &ix->bytes));
+    if (n_old) HCG_TRY_CUDA(cudaMemcpyAsync(nr, ix->rows, size_t(n_old) * ix->pitch, cudaMemcpyDeviceToDevice, st));
+    if (ix->pitch != ix->d_full) HCG_TRY_CUDA(cudaMemsetAsync(nr + size_t(n_old) * ix->pitch, 0, size_t(nb) * ix->pitch, st));
+    HCG_TRY_CUDA(cudaMemcpy2DAsync(nr + size_t(n_old) * ix->pitch, ix->pitch, rows, ix->d_full, ix->d_full, nb,
+                                   cudaMemcpyDefault, st));
+    HCG_TRY_CUDA(cudaStreamSynchronize(st));
+    dev_free(ix->rows, size_t(std::max<uint64_t>(n_old, 1)) * ix->pitch, &ix->bytes);
+    ix->rows = nr;
+    ix->n = n_new;
+    for (uint32_t c = 0; c < ix->C; ++c) HCG_TRY(insert_curve(ix, c, n_old, nb, st));
+    return publish_tables(ix, st);
+}
+
+
+hcg_status hcg_save(const hcg_index* ix, const char* path) {
+    HCG_TRY(check_index(ix));
+    if (!path) return set_error(HCG_EINVAL, "null path");
+    DeviceGuard g(ix->device);
+    FileCloser fc;
+    fc.f = std::fopen(path, "wb");
+    if (!fc.f) return set_error(HCG_EIO, std::string("cannot open ") + path + " for writing");
+    FILE* f = fc.f;
+    const uint32_t hdr[6] = {kFormatVersion, ix->d_full, ix->C, ix->m, ix->kind, uint32_t(ix->assign.size())};
+    const uint64_t ids[3] = {ix->n, ix->id_base, ix->id_stride};
+    bool ok = put(f, kMagic, 8) && put(f, hdr, 6) && put(f, &ix->dist_scale, 1) && put(f, ids, 3) &&
+              put(f, ix->lut, 256) && put(f, ix->off.data(), ix->off.size()) &&
+              put(f, ix->assign.data(), ix->assign.size());
+    // rows, unpadded, in slices
+    const uint64_t slice = 1 << 20;
+    std::vector<uint8_t> buf;
+    for (uint64_t r = 0; ok && r < ix->n; r += slice) {
+        const uint64_t cnt = std::min(slice, ix->n - r);
+        buf.resize(cnt * ix->d_full);
+        HCG_TRY_CUDA(cudaMemcpy2D(buf.data(), ix->d_full, ix->rows + r * ix->pitch, ix->pitch, ix->d_full, cnt,
+                                  cudaMemcpyDeviceToHost));
+        ok = put(f, buf.data(), buf.size());
+    }
+    for (uint32_t c = 0; ok && c < ix->C; ++c) {
+        const CurveDev& cv = ix->curves[c];
+        const uint32_t ch[5] = {cv.w, cv.ws, cv.hv, cv.dims, cv.off};
+        ok = put(f, ch, 5) && put(f, cv.prefix, kMaxKeyWords);
+        if (ix->n) {
+            std::vector<uint64_t> k(size_t(ix->n) * cv.ws);
+            std::vector<uint32_t> sl(ix->n);
+            HCG_TRY_CUDA(cudaMemcpy(k.data(), ix->keys[c], k.size() * 8, cudaMemcpyDeviceToHost));
+            HCG_TRY_CUDA(cudaMemcpy(sl.data(), ix->slots[c], sl.size() * 4, cudaMemcpyDeviceToHost));
+            ok = ok && put(f, k.data(), k.size()) && put(f, sl.data(), sl.size());
+        }
+    }
+    ok = ok && put(f, kTrailer, 8);
+    if (!ok) return set_error(HCG_EIO, std::string("write failed: ") + path);
+    return HCG_OK;
+}
+
+hcg_status hcg_load(const char* path, int device, void* stream, hcg_index** out) {
+    if (!path || !out) return set_error(HCG_EINVAL, "null argument");
+    *out = nullptr;
+    FileCloser fc;
+    fc.f = std::fopen(path, "rb");
+    if (!fc.f) return set_error(HCG_EIO, std::string("cannot open ") + path);
+    FILE* f = fc.f;
+    char magic[8];
+    uint32_t hdr[6];
+    double scale = 0;
+    uint64_t ids[3];
+    if (!get(f, magic, 8) || std::memcmp(magic, kMagic, 8) != 0) return set_error(HCG_EIO, std::string(path) + ": not an hcg index");
+    if (!get(f, hdr, 6) || hdr[0] != kFormatVersion) return set_error(HCG_EIO, std::string(path) + ": unsupported version");
+    if (!get(f, &scale, 1) || !get(f, ids, 3)) return set_error(HCG_EIO, std::string(path) + ": truncated header");
+    hcg_scheme s{};
+    s.d_full = hdr[1];
+    s.curves = hdr[2];
+    s.bits_per_dim = hdr[3];
+    s.curve_kind = hdr[4];
+    s.dist_scale = scale;
+    if (s.curves == 0 || s.curves > 4096 || hdr[5] > 1u << 20) return set_error(HCG_EIO, std::string(path) + ": corrupt header");
+    std::vector<uint32_t> off(s.curves + 1), asg(hdr[5]);
+    if (!get(f, s.cell_lut, 256) || !get(f, off.data(), off.size()) || !get(f, asg.data(), asg.size()))
+        return set_error(HCG_EIO, std::string(path) + ": truncated scheme");
+    s.assign_off = off.data();
+    s.assign = asg.data();
+    if (off[s.curves] != hdr[5]) return set_error(HCG_EIO, std::string(path) + ": corrupt scheme");
+    HCG_TRY(validate_scheme(&s));
+    HCG_TRY(check_device(device));
+    DeviceGuard g(device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    hcg_index* ix = nullptr;
+    HCG_TRY(new_index(&s, ids[0], ids[1], ids[2], device, st, &ix));
+    auto fail = [&](hcg_status rc) {
+        cudaStreamSynchronize(st);
+        release(ix);
+        return rc;
+    };
+    const uint64_t slice = 1 << 20;
+    std::vector<uint8_t> buf;
+    for (uint64_t r = 0; r < ix->n; r += slice) {
+        const uint64_t cnt = std::min(slice, ix->n - r);
+        buf.resize(cnt * ix->d_full);
+        if (!get(f, buf.data(), buf.size())) return fail(set_error(HCG_EIO, std::string(path) + ": truncated rows"));
+        if (cudaMemcpy2D(ix->rows + r * ix->pitch, ix->pitch, buf.data(), ix->d_full, ix->d_full, cnt,
+                         cudaMemcpyHostToDevice) != cudaSuccess)
+            return fail(set_error(HCG_ECUDA, "upload rows"));
+    }
+    for (uint32_t c = 0; c < ix->C; ++c) {
+        CurveDev& cv = ix->curves[c];
+        std::memset(&cv, 0, sizeof(cv));
+        uint32_t ch[5];
+        if (!get(f, ch, 5) || !get(f, cv.prefix, kMaxKeyWords))
+            return fail(set_error(HCG_EIO, std::string(path) + ": truncated curve header"));
+        cv.w = ch[0];
+        cv.ws = ch[1];
+        cv.hv = ch[2];
+        cv.dims = ch[3];
+        cv.off = ch[4];
+        if (cv.ws < 1 || cv.ws > cv.w || cv.w > kMaxKeyWords || cv.off != off[c] || cv.dims != off[c + 1] - off[c])
+            return fail(set_error(HCG_EIO, std::string(path) + ": corrupt curve header"));
+        if (ix->n) {
+            std::vector<uint64_t> k(size_t(ix->n) * cv.ws);
+            std::vector<uint32_t> sl(ix->n);
+            if (!get(f, k.data(), k.size()) || !get(f, sl.data(), sl.size()))
+                return fail(set_error(HCG_EIO, std::string(path) + ": truncated curve arrays"));
+            hcg_status rc;
+            if ((rc = dev_alloc(&ix->keys[c], k.size(), &ix->bytes)) != HCG_OK) return fail(rc);
+            if ((rc = dev_alloc(&ix->slots[c], sl.size(), &ix->bytes)) != HCG_OK) return fail(rc);
+            if (cudaMemcpy(ix->keys[c], k.data(), k.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess ||
+                cudaMemcpy(ix->slots[c], sl.data(), sl.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess)
+                return fail(set_error(HCG_ECUDA, "upload curve"));
+            cv.keys = ix->keys[c];
+            cv.slots = ix->slots[c];
+        }
+    }
+    char tr[8];
+    if (!get(f, tr, 8) || std::memcmp(tr, kTrailer, 8) != 0) return fail(set_error(HCG_EIO, std::string(path) + ": missing trailer"));
+    hcg_status rc = publish_tables(ix, st);
+    if (rc != HCG_OK) return fail(rc);
+    *out = ix;
+    return HCG_OK;
+}
 
 static hcg_status search_impl(const hcg_index* ix, const uint8_t* queries, uint32_t nq, uint32_t k, uint32_t depth,
                               uint64_t* out_ids, uint32_t* out_sqdist, uint32_t* out_len, uint64_t* out_packed,

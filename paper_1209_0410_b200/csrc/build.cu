@@ -246,9 +246,50 @@ __global__ void __launch_bounds__(kSortThreads) k_downsweep(
     }
 }
 
-__global__ void k_iota(uint32_t* v, uint64_t n) {
+__global__ void k_iota(uint32_t* v, uint64_t n, uint32_t base) {
     const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i < n) v[i] = uint32_t(i);
+    if (i < n) v[i] = base + uint32_t(i);
+}
+
+__global__ void k_offset(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, uint64_t n, uint32_t base) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = base + in[i];
+}
+
+__device__ __forceinline__ int cmp_words(const uint64_t* a, const uint64_t* b, int ws) {
+    for (int w = ws - 1; w >= 0; --w) {
+        const uint64_t x = a[w], y = b[w];
+        if (x != y) return x < y ? -1 : 1;
+    }
+    return 0;
+}
+
+// Stable merge by rank (incremental insert, multicurves.hpp:52):
+// resident entry i lands at i + #(new < key_i), new entry j at j + #(resident <= key_j),
+// so equal keys keep the resident (lower-id) entries first.
+__global__ void k_rank_merge(const uint64_t* __restrict__ ak, const uint32_t* __restrict__ as, uint64_t na,
+                             const uint64_t* __restrict__ bk, const uint32_t* __restrict__ bs, uint64_t nb, int ws,
+                             uint64_t* __restrict__ ck, uint32_t* __restrict__ cs) {
+    const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= na + nb) return;
+    const bool from_a = t < na;
+    const uint64_t i = from_a ? t : t - na;
+    const uint64_t* key = (from_a ? ak : bk) + i * ws;
+    const uint64_t* other = from_a ? bk : ak;
+    uint64_t lo = 0, len = from_a ? nb : na;
+    while (len > 0) {  // from_a: lower_bound in B; else upper_bound in A
+        const uint64_t half = len >> 1, mid = lo + half;
+        const int c = cmp_words(other + mid * ws, key, ws);
+        if (c < 0 || (!from_a && c == 0)) {
+            lo = mid + 1;
+            len -= half + 1;
+        } else {
+            len = half;
+        }
+    }
+    const uint64_t pos = i + lo;
+    for (int w = 0; w < ws; ++w) ck[pos * ws + w] = key[w];
+    cs[pos] = from_a ? as[i] : bs[i];
 }
 
 __global__ void k_gather_word(const uint64_t* __restrict__ src, const uint32_t* __restrict__ perm,
@@ -330,8 +371,15 @@ size_t radix_counts_bytes(uint64_t n) {
     return size_t(tiles) * 256 * 4 + 256 * 4;
 }
 
-void launch_iota(uint32_t* v, uint64_t n, cudaStream_t st) {
-    if (n) k_iota<<<blocks_for(n, 256), 256, 0, st>>>(v, n);
+void launch_iota(uint32_t* v, uint64_t n, uint32_t base, cudaStream_t st) {
+    if (n) k_iota<<<blocks_for(n, 256), 256, 0, st>>>(v, n, base);
+}
+void launch_offset(const uint32_t* in, uint32_t* out, uint64_t n, uint32_t base, cudaStream_t st) {
+    if (n) k_offset<<<blocks_for(n, 256), 256, 0, st>>>(in, out, n, base);
+}
+void launch_rank_merge(const uint64_t* ak, const uint32_t* as, uint64_t na, const uint64_t* bk, const uint32_t* bs,
+                       uint64_t nb, int ws, uint64_t* ck, uint32_t* cs, cudaStream_t st) {
+    if (na + nb) k_rank_merge<<<blocks_for(na + nb, 256), 256, 0, st>>>(ak, as, na, bk, bs, nb, ws, ck, cs);
 }
 void launch_gather_word(const uint64_t* src, const uint32_t* perm, uint64_t* dst, uint64_t n, cudaStream_t st) {
     if (n) k_gather_word<<<blocks_for(n, 256), 256, 0, st>>>(src, perm, dst, n);

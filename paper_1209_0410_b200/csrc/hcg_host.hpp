@@ -22,7 +22,10 @@ hcg_status keygen_rows(const uint8_t* rows, uint64_t n, uint32_t pitch, const ui
 hcg_status radix_sort_pairs(uint64_t** k, uint32_t** v, uint64_t** k_alt, uint32_t** v_alt, uint64_t n,
                             uint32_t digit_mask, uint32_t* counts, uint32_t* totals, cudaStream_t st);
 size_t radix_counts_bytes(uint64_t n);
-void launch_iota(uint32_t* v, uint64_t n, cudaStream_t st);
+void launch_iota(uint32_t* v, uint64_t n, uint32_t base, cudaStream_t st);
+void launch_offset(const uint32_t* in, uint32_t* out, uint64_t n, uint32_t base, cudaStream_t st);
+void launch_rank_merge(const uint64_t* ak, const uint32_t* as, uint64_t na, const uint64_t* bk, const uint32_t* bs,
+                       uint64_t nb, int ws, uint64_t* ck, uint32_t* cs, cudaStream_t st);
 void launch_gather_word(const uint64_t* src, const uint32_t* perm, uint64_t* dst, uint64_t n, cudaStream_t st);
 void launch_pack_suffix(const uint64_t* keys_soa, const uint32_t* perm, uint64_t n, int ws, uint64_t top_mask,
                         uint64_t* out, cudaStream_t st);

@@ -14,6 +14,7 @@ Everything runs on the sm_100a kernels in libhcg.so -- there is no CPU path.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 from typing import NamedTuple
 
@@ -167,13 +168,16 @@ class MulticurvesIndex:
     """
 
     def __init__(self, rows, scheme: ProjectionScheme, view: View = RAW, device: int = 0,
-                 id_base: int = 0, id_stride: int = 1, stream=None):
+                 id_base: int = 0, id_stride: int = 1, stream=None, _handle=None):
         self.scheme = scheme
         self.view = view
         self.device = device
         self.id_base = id_base
         self.id_stride = id_stride
         self._h = None
+        if _handle is not None:  # MulticurvesIndex.load
+            self._h = _handle
+            return
         d = scheme.d_full
         rows = _u8_2d(rows, d) if (rows is not None and len(rows)) else np.zeros((0, d), np.uint8)
         n = rows.shape[0]
@@ -200,6 +204,26 @@ class MulticurvesIndex:
         check(lib().hcg_build(C.byref(s), _ptr(rows), n, id_base, id_stride, device,
                               _stream(stream, rows), C.byref(h)))
         self._h = h
+
+    # -- growth and persistence
+    def insert(self, rows, stream=None) -> None:
+        """multicurves.hpp:79, batched: append rows (ids continue id_base + s*id_stride)."""
+        r = _u8_2d(rows, self.scheme.d_full)
+        check(lib().hcg_insert(self._h, _ptr(r), r.shape[0], _stream(stream, r)))
+
+    def save(self, path: str) -> None:
+        """multicurves.hpp:96-97: little-endian, bit-exact round trip."""
+        check(lib().hcg_save(self._h, os.fsencode(path)))
+
+    @classmethod
+    def load(cls, path: str, scheme: ProjectionScheme, view: View, device: int = 0, id_base: int = 0,
+             id_stride: int = 1) -> "MulticurvesIndex":
+        """multicurves.hpp:98.  The file carries the scheme; `scheme`/`view` are
+        the caller's description of it (for distances and the Python mirror)."""
+        h = C.c_void_p()
+        check(lib().hcg_load(os.fsencode(path), device, None, C.byref(h)))
+        obj = cls(None, scheme, view, device, id_base, id_stride, _handle=h)
+        return obj
 
     # -- lifetime
     def close(self) -> None:
@@ -343,6 +367,34 @@ class MulticurvesIndex:
         return ids, sq, ln
 
 
+def read_vectors(path: str, fmt: str = "bvecs", view: View = RAW) -> np.ndarray:
+    """vecio.cpp:18-61: bvecs / fvecs records -> [n, dim] uint8 rows."""
+    from ._lib import HCG_BVECS, HCG_FVECS
+    buf = C.POINTER(C.c_uint8)()
+    n = C.c_uint64()
+    dim = C.c_uint32()
+    check(lib().hcg_read_vectors(os.fsencode(path), HCG_BVECS if fmt == "bvecs" else HCG_FVECS,
+                                 C.c_float(view.offset), C.c_float(view.scale), C.byref(buf), C.byref(n),
+                                 C.byref(dim)))
+    try:
+        total = n.value * dim.value
+        out = np.ctypeslib.as_array(buf, shape=(max(total, 1),))[:total].copy()
+    finally:
+        lib().hcg_free_buffer(buf)
+    return out.reshape(n.value, dim.value) if n.value else np.zeros((0, dim.value), np.uint8)
+
+
+def write_vectors(path: str, rows, fmt: str = "bvecs", view: View = RAW) -> None:
+    """vecio.cpp:63-85."""
+    from ._lib import HCG_BVECS, HCG_FVECS
+    r = np.ascontiguousarray(rows, dtype=np.uint8)
+    if r.ndim == 1:
+        r = r.reshape(1, -1)
+    check(lib().hcg_write_vectors(os.fsencode(path), HCG_BVECS if fmt == "bvecs" else HCG_FVECS,
+                                  C.c_float(view.offset), C.c_float(view.scale), _ptr(r), r.shape[0],
+                                  r.shape[1] if r.size else 0))
+
+
 def merge_packed(packed, k: int, device: int = 0, stream=None, out=None):
     """Hypershard aggregate: packed [parts, nq, k] -> top-k."""
     parts, nq = int(packed.shape[0]), int(packed.shape[1])
@@ -411,4 +463,5 @@ __all__ = [
     "View", "RAW", "LIFTED", "ProjectionScheme", "default_scheme", "SearchParams", "Neighbor",
     "MulticurvesIndex", "merge_packed", "binomial_tail", "miss_bound", "plan_depth",
     "shard_probe_depth", "gen_rows", "gen_queries", "make_lut", "recall_at", "ZORDER", "HILBERT",
+    "read_vectors", "write_vectors",
 ]

@@ -1,0 +1,70 @@
+"""bvecs / fvecs records (vecio.cpp:18-85): the library's reader
+and writer against the reference's own read_vectors (oracle/_ref) -- same
+payload, same rejection of malformed files (std::runtime_error <-> HcgIOError)."""
+import ctypes as C
+import os
+import struct
+
+import numpy as np
+import pytest
+
+import paper_1209_0410_b200 as H
+from oracle import pyoracle as P
+
+
+def ref_read(path, bvecs):
+    lib = P.ref()
+    lib.ref_read_vectors.argtypes = [C.c_char_p, C.c_int, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64),
+                                     C.POINTER(C.c_uint32)]
+    out = np.zeros(1 << 16, np.float32)
+    n, d = C.c_uint64(), C.c_uint32()
+    rc = lib.ref_read_vectors(os.fsencode(path), int(bvecs), out.ctypes.data, out.size, C.byref(n), C.byref(d))
+    return rc, out[: n.value * d.value].reshape(n.value, d.value) if rc == 0 else None
+
+
+@pytest.mark.parametrize("fmt,view", [("bvecs", H.RAW), ("fvecs", H.RAW), ("fvecs", H.LIFTED)])
+def test_round_trip_and_reference_reader(tmp_path, fmt, view):
+    rows = np.random.default_rng(1).integers(0, 256, (300, 128), dtype=np.uint8)
+    path = str(tmp_path / f"x.{fmt}")
+    H.write_vectors(path, rows, fmt, view)
+    back = H.read_vectors(path, fmt, view)
+    np.testing.assert_array_equal(back, rows)
+    if P.ref_available():
+        rc, f = ref_read(path, fmt == "bvecs")
+        assert rc == 0
+        want = view.floats(rows) if fmt == "fvecs" else rows.astype(np.float32)
+        np.testing.assert_array_equal(f, want)
+
+
+def test_empty_file_is_empty_dataset(tmp_path):
+    p = tmp_path / "e.bvecs"
+    p.write_bytes(b"")
+    assert H.read_vectors(str(p)).shape[0] == 0
+
+
+@pytest.mark.parametrize("payload,why", [
+    (struct.pack("<I", 4) + b"\x01\x02", "truncated bvecs payload"),
+    (struct.pack("<I", 4) + b"\x01\x02\x03\x04" + b"\x01\x00", "truncated record header"),
+    (struct.pack("<I", 0), "zero-dimension record"),
+    (struct.pack("<I", 2) + b"ab" + struct.pack("<I", 3) + b"abc", "inconsistent dimension header"),
+])
+def test_malformed_files_rejected_like_the_reference(tmp_path, payload, why):
+    p = tmp_path / "bad.bvecs"
+    p.write_bytes(payload)
+    with pytest.raises(H.HcgIOError, match=why):
+        H.read_vectors(str(p))
+    if P.ref_available():
+        rc, _ = ref_read(str(p), True)
+        assert rc != 0 and why in P.ref_error()
+
+
+def test_nonfinite_fvecs_rejected(tmp_path):
+    p = tmp_path / "nan.fvecs"
+    p.write_bytes(struct.pack("<I", 2) + struct.pack("<2f", 1.0, float("nan")))
+    with pytest.raises(H.HcgIOError, match="non-finite"):
+        H.read_vectors(str(p), "fvecs")
+
+
+def test_missing_file(tmp_path):
+    with pytest.raises(H.HcgIOError, match="cannot open"):
+        H.read_vectors(str(tmp_path / "nope.bvecs"))

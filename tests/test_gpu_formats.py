@@ -1,0 +1,85 @@
+"""Incremental insert and persistence on the B200 (multicurves.hpp:79,96-98;
+SPEC.md:227-235,268): build(A) + insert(B) equals build(A u B) entry for entry
+(SPEC's order-independence oracle), including the case where B moves a
+curve's common key prefix (rebuild path); save -> load round-trips bit-exactly."""
+import numpy as np
+import pytest
+
+from hcg_testutil import gpu_available
+from oracle import pyoracle as P
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device")]
+
+import paper_1209_0410_b200 as H  # noqa: E402
+
+
+def _same_index(a, b, qs, curves, k=10, depth=200):
+    for c in range(curves):
+        ia, ka = a.subindex(c, with_keys=True)
+        ib, kb = b.subindex(c, with_keys=True)
+        np.testing.assert_array_equal(ia, ib)
+        np.testing.assert_array_equal(ka, kb)
+    ra = a.search_batch(qs, k, depth)
+    rb = b.search_batch(qs, k, depth)
+    for x, y in zip(ra, rb):
+        np.testing.assert_array_equal(x, y)
+
+
+@pytest.mark.parametrize("view,m", [(H.RAW, 8), (H.LIFTED, 16)])
+def test_insert_equals_build_of_union(view, m):
+    rows = P.gen_rows(0, 6000)
+    qs = P.gen_queries(0, 40, 6000)
+    sch = H.default_scheme(128, 8, m)
+    full = H.MulticurvesIndex(rows, sch, view)
+    inc = H.MulticurvesIndex(rows[:4000], sch, view)
+    inc.insert(rows[4000:4001])          # single row (the reference's per-vector insert)
+    inc.insert(rows[4001:5500])
+    inc.insert(rows[5500:])
+    assert inc.size() == 6000
+    _same_index(inc, full, qs, 8)
+    oi = P.Oracle(view.floats(rows), 8, m)
+    ids, dist, ln = oi.search(view.floats(qs), 10, 200)
+    gi, gs, gl = inc.search_batch(qs, 10, 200)
+    np.testing.assert_array_equal(gi, ids)
+
+
+def test_insert_that_moves_the_common_prefix():
+    rng = np.random.default_rng(3)
+    low = rng.integers(0, 40, (3000, 128), dtype=np.uint8)
+    high = rng.integers(200, 256, (500, 128), dtype=np.uint8)
+    both = np.concatenate([low, high])
+    qs = np.concatenate([low[:10], high[:10]])
+    sch = H.default_scheme(128, 8, 16)
+    inc = H.MulticurvesIndex(low, sch, H.LIFTED)
+    inc.insert(high)
+    _same_index(inc, H.MulticurvesIndex(both, sch, H.LIFTED), qs, 8)
+
+
+def test_insert_into_empty_index_equals_build():
+    rows = P.gen_rows(0, 100)
+    sch = H.default_scheme(128, 4, 8)
+    e = H.MulticurvesIndex(rows[:0], sch, H.RAW)
+    e.insert(rows)
+    _same_index(e, H.MulticurvesIndex(rows, sch, H.RAW), rows[:5], 4)
+
+
+@pytest.mark.parametrize("view,m,kind", [(H.RAW, 8, H.HILBERT), (H.LIFTED, 16, H.ZORDER)])
+def test_save_load_round_trip(tmp_path, view, m, kind):
+    rows = np.random.default_rng(4).integers(0, 256, (5000, 100), dtype=np.uint8)
+    qs = rows[:30]
+    sch = H.default_scheme(100, 7, m, kind)
+    a = H.MulticurvesIndex(rows, sch, view)
+    path = str(tmp_path / "idx.hcg")
+    a.save(path)
+    b = H.MulticurvesIndex.load(path, sch, view)
+    assert b.size() == 5000 and b.curves() == 7
+    _same_index(a, b, qs, 7)
+    b.save(str(tmp_path / "again.hcg"))
+    assert open(path, "rb").read() == open(str(tmp_path / "again.hcg"), "rb").read()
+
+
+def test_load_rejects_garbage(tmp_path):
+    p = tmp_path / "bad.hcg"
+    p.write_bytes(b"not an index at all")
+    with pytest.raises(H.HcgIOError):
+        H.MulticurvesIndex.load(str(p), H.default_scheme(128, 8), H.RAW)
