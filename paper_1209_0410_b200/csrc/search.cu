@@ -346,19 +346,21 @@ __device__ __forceinline__ void gather_list(const RefineArgs& a, const uint32_t*
         nx[r] = e < n ? __ldcg(list + e) : kEmpty;
     }
     for (uint32_t base = start; base < n; base += step) {
-        uint32_t sl[8];
-#pragma unroll
-        for (int r = 0; r < 8; ++r) sl[r] = nx[r];
         uint4 v[8][CR];
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
 #pragma unroll
             for (int t = 0; t < CR; ++t) {
                 const uint32_t ch = l8 + 8 * t;
-                v[r][t] = (sl[r] != kEmpty && ch < chunks) ? ldg_stream(a.rows + uint64_t(sl[r]) * a.pitch + ch * 16)
+                v[r][t] = (nx[r] != kEmpty && ch < chunks) ? ldg_stream(a.rows + uint64_t(nx[r]) * a.pitch + ch * 16)
                                                            : make_uint4(0, 0, 0, 0);
             }
         }
+        // this lane's row after the reduce-scatter is row l8 of its group
+        uint32_t me = nx[0];
+#pragma unroll
+        for (int r = 1; r < 8; ++r)
+            if (r == l8) me = nx[r];
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
             const uint32_t e = base + step + grp * 8 + r;
@@ -387,10 +389,6 @@ __device__ __forceinline__ void gather_list(const RefineArgs& a, const uint32_t*
             s2[i] = keep + __shfl_xor_sync(kFull, send, 2);
         }
         const uint32_t S = (b0 ? s2[1] : s2[0]) + __shfl_xor_sync(kFull, b0 ? s2[0] : s2[1], 1);
-        uint32_t me = sl[0];
-#pragma unroll
-        for (int r = 1; r < 8; ++r)
-            if (r == l8) me = sl[r];
         tk.offer(me != kEmpty ? ((uint64_t(S) << 32) | me) : kNone, lane);
     }
 }
@@ -578,8 +576,8 @@ hcg_status refine_dispatch(const RefineArgs& a_in, void* scratch, size_t* scratc
     uint32_t* lists = static_cast<uint32_t*>(scratch);
     uint32_t* counts = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(scratch) + lists_bytes);
     uint32_t* gtab = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(scratch) + lists_bytes + counts_bytes);
-    constexpr int MINB = R <= 2 ? 4 : 2;
-    auto gk = k_gather<R, CR, MINB>;
+    // 4 CTAs/SM: measured best (5-6 spill and lose ~15 %)
+    auto gk = k_gather<R, CR, R <= 2 ? 4 : 2>;
     static bool cfg_u[64] = {};
     if (smem_union) HCG_RET_IF(opt_in_smem(k_union, device, cfg_u));
     int g_per_sm = 1;

@@ -27,3 +27,4 @@ ref = uni + gat
 print(f"depth={D} k={k} U={U.mean():.1f} locate_ms={loc:.3f} union_ms={uni:.3f} gather_ms={gat:.3f} "
       f"refine_ms={ref:.3f} refine_GB/s={bytes_ / ref / 1e6:.0f}", flush=True)
 
+
