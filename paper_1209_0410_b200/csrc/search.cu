@@ -454,6 +454,111 @@ __global__ void __launch_bounds__(kRefineThreads) k_gather_cta(RefineArgs a, con
     }
 }
 
+// K3b (register variant, the default for C x take <= 32 x 256): each thread
+// holds its <= JMAX window ids in registers (coalesced loads, no staging).
+// Round r: every pending id stores (id << 32 | position) into slot h_r(id) of
+// a u64 shared table; after a barrier it reads the slot back -- the same id:
+// the id is resolved, and this copy is its first copy iff the stored position
+// is its own; another id: collision, retried with the next hash.  All copies
+// of an id hit the same slot, so they resolve in the same round.  Ids still
+// colliding after kRegRounds go through an atomicCAS pass on the cleared table
+// (measured: a CAS pass for every round-1 collision instead is 1.6x slower).
+// Kept ids are compacted with one block scan.
+constexpr int kRegRounds = 4;
+
+template <int JMAX>
+__global__ void __launch_bounds__(kRefineThreads) k_union_reg(RefineArgs a, uint32_t* __restrict__ lists,
+                                                              uint32_t* __restrict__ counts, uint32_t lstride,
+                                                              uint32_t tb) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    unsigned long long* tab = reinterpret_cast<unsigned long long*>(smem);  // [1 << tb]
+    const uint32_t** sptr = reinterpret_cast<const uint32_t**>(tab + (size_t(1) << tb));
+    uint32_t* sbeg = reinterpret_cast<uint32_t*>(sptr + a.C);
+    uint32_t* wsum = sbeg + a.C;  // [8] scan scratch
+    const uint32_t T = a.C * a.take;
+    const int tid = threadIdx.x;
+    const uint32_t take = a.take, shift = 32 - tb, tmask = (1u << tb) - 1;
+    for (uint32_t c = tid; c < a.C; c += kRefineThreads) sptr[c] = a.slots[c];
+
+    for (uint32_t q = blockIdx.x; q < a.nq; q += gridDim.x) {
+        __syncthreads();  // previous query done with tab / sbeg
+        for (uint32_t c = tid; c < a.C; c += kRefineThreads) sbeg[c] = a.begins[uint64_t(q) * a.C + c];
+        __syncthreads();
+        uint32_t id[JMAX];
+        uint32_t pending = 0;
+        {
+            uint32_t c = 0, p = tid;
+            while (p >= take && c + 1 < a.C) {
+                p -= take;
+                ++c;
+            }
+#pragma unroll
+            for (int j = 0; j < JMAX; ++j) {
+                const uint32_t i = tid + j * kRefineThreads;
+                id[j] = 0;
+                if (i < T) {
+                    id[j] = __ldg(sptr[c] + sbeg[c] + p);
+                    pending |= 1u << j;
+                }
+                p += kRefineThreads;
+                while (p >= take && c + 1 < a.C) {
+                    p -= take;
+                    ++c;
+                }
+            }
+        }
+        uint32_t keep = 0;
+#pragma unroll 1
+        for (int r = 0; r < kRegRounds; ++r) {
+            const uint32_t mul = 0x9E3779B1u + 0x7F4A7C16u * uint32_t(r) * 2u;  // odd
+#pragma unroll
+            for (int j = 0; j < JMAX; ++j)
+                if ((pending >> j) & 1)
+                    tab[(id[j] * mul) >> shift] = (uint64_t(id[j]) << 32) | uint32_t(tid + j * kRefineThreads);
+            __syncthreads();
+#pragma unroll
+            for (int j = 0; j < JMAX; ++j) {
+                if ((pending >> j) & 1) {
+                    const uint64_t o = tab[(id[j] * mul) >> shift];
+                    if (uint32_t(o >> 32) == id[j]) {
+                        pending &= ~(1u << j);
+                        if (uint32_t(o) == uint32_t(tid + j * kRefineThreads)) keep |= 1u << j;
+                    }
+                }
+            }
+            if (!__syncthreads_or(pending != 0)) break;
+        }
+        if (__syncthreads_or(pending != 0)) {  // rare: CAS set over the cleared table
+            for (uint32_t i = tid; i <= tmask; i += kRefineThreads) tab[i] = ~0ull;
+            __syncthreads();
+#pragma unroll
+            for (int j = 0; j < JMAX; ++j) {
+                if ((pending >> j) & 1) {
+                    const unsigned long long mine = (uint64_t(id[j]) << 32) | uint32_t(tid + j * kRefineThreads);
+                    uint32_t h = hash_slot(id[j]) >> shift;
+                    while (true) {
+                        const unsigned long long prev = atomicCAS(&tab[h], ~0ull, mine);
+                        if (prev == ~0ull) {
+                            keep |= 1u << j;
+                            break;
+                        }
+                        if (uint32_t(prev >> 32) == id[j]) break;
+                        h = (h + 1) & tmask;
+                    }
+                }
+            }
+        }
+        const uint32_t mine = __popc(keep);
+        const uint32_t off = block_excl_scan256_u(mine, wsum);
+        uint32_t* out = lists + uint64_t(q) * lstride + off;
+        uint32_t w = 0;
+#pragma unroll
+        for (int j = 0; j < JMAX; ++j)
+            if ((keep >> j) & 1) out[w++] = id[j];
+        if (tid == kRefineThreads - 1) counts[q] = off + mine;
+    }
+}
+
 // Candidate-union tap: unique slots -> ids.
 __global__ void k_lists_to_ids(RefineArgs a, const uint32_t* __restrict__ lists, const uint32_t* __restrict__ counts,
                                uint32_t lstride) {  // lstride: entries per query list
@@ -547,6 +652,29 @@ size_t union_smem_bytes(uint32_t C, uint32_t T, uint32_t tb) {
 }
 
 
+template <int JMAX>
+hcg_status union_reg_launch(const RefineArgs& a, uint32_t* lists, uint32_t* counts, uint32_t lstride, uint32_t tb,
+                            int device, cudaStream_t st) {
+    auto kern = k_union_reg<JMAX>;
+    const size_t smem = (size_t(8) << tb) + size_t(a.C) * 12 + 64;
+    static bool cfg[64] = {};
+    HCG_RET_IF(opt_in_smem(kern, device, cfg));
+    const uint32_t grid = persistent_grid(reinterpret_cast<const void*>(kern), smem, device, a.nq);
+    kern<<<grid, kRefineThreads, smem, st>>>(a, lists, counts, lstride, tb);
+    return check_launch("k_union_reg");
+}
+
+hcg_status launch_union_reg(const RefineArgs& a, uint32_t* lists, uint32_t* counts, uint32_t lstride, uint32_t tb,
+                            int device, cudaStream_t st) {
+    const uint32_t jn = (a.C * a.take + kRefineThreads - 1) / kRefineThreads;
+    if (jn <= 4) return union_reg_launch<4>(a, lists, counts, lstride, tb, device, st);
+    if (jn <= 8) return union_reg_launch<8>(a, lists, counts, lstride, tb, device, st);
+    if (jn <= 12) return union_reg_launch<12>(a, lists, counts, lstride, tb, device, st);
+    if (jn <= 16) return union_reg_launch<16>(a, lists, counts, lstride, tb, device, st);
+    if (jn <= 24) return union_reg_launch<24>(a, lists, counts, lstride, tb, device, st);
+    return union_reg_launch<32>(a, lists, counts, lstride, tb, device, st);
+}
+
 // Query chunk so the per-call list scratch stays within kListBudget.
 constexpr size_t kListBudget = size_t(2) << 30;
 
@@ -561,6 +689,7 @@ hcg_status refine_dispatch(const RefineArgs& a_in, void* scratch, size_t* scratc
     const uint32_t utb = std::min<uint32_t>(tb + 1, 16);
     const size_t usmem = union_smem_bytes(a_in.C, T, utb);
     const bool smem_union = T <= kUnionMaxT && usmem <= 160 * 1024;
+    const bool reg_union = T <= 32u * kRefineThreads && (size_t(8) << tb) <= 128 * 1024 && !getenv("HCG_UNION_SMEM");
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     const uint32_t chunk = uint32_t(std::max<size_t>(1, std::min<size_t>(a_in.nq, kListBudget / (size_t(lstride) * 4))));
@@ -591,7 +720,9 @@ hcg_status refine_dispatch(const RefineArgs& a_in, void* scratch, size_t* scratc
         if (a.out_sqdist) a.out_sqdist += uint64_t(q0) * a_in.k;
         if (a.out_len) a.out_len += q0;
         if (a.out_packed) a.out_packed += uint64_t(q0) * a_in.k;
-        if (smem_union) {
+        if (reg_union) {
+            HCG_RET_IF(launch_union_reg(a, lists, counts, lstride, tb, device, st));
+        } else if (smem_union) {
             const uint32_t ugrid = persistent_grid(reinterpret_cast<const void*>(k_union), usmem, device, a.nq);
             k_union<<<ugrid, kRefineThreads, usmem, st>>>(a, lists, counts, lstride, utb);
         } else {

@@ -28,3 +28,14 @@ print(f"depth={D} k={k} U={U.mean():.1f} locate_ms={loc:.3f} union_ms={uni:.3f} 
       f"refine_ms={ref:.3f} refine_GB/s={bytes_ / ref / 1e6:.0f}", flush=True)
 
 
+
+if os.environ.get("UNION_AB"):
+    for v in ("reg", "smem", "reg", "smem"):
+        if v == "smem":
+            os.environ["HCG_UNION_SMEM"] = "1"
+        else:
+            os.environ.pop("HCG_UNION_SMEM", None)
+        for b in range(2):
+            ix.search_timed(qs[b], k, D, out=out)
+        ms = sorted(ix.search_timed(qs[b % 4], k, D, out=out)[1] for b in range(6))[3]
+        print(f"union={v} union_ms={ms:.3f}", flush=True)
