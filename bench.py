@@ -470,8 +470,9 @@ def run_reference(a):
 
 
 def main():
-    # one JSON line on rank 0's stdout: keep NCCL's banner out of it
-    os.environ.setdefault("NCCL_DEBUG", "WARN")
+    # one JSON line on rank 0's stdout: keep NCCL's version banner out of it
+    if os.environ.get("NCCL_DEBUG", "").upper() in ("", "VERSION"):
+        os.environ["NCCL_DEBUG"] = "WARN"
     a = parse()
     if a.impl == "reference":
         run_reference(a)
