@@ -246,24 +246,27 @@ def run_ours(a):
     time.sleep(0.3)
     ms_total = timed(step)
 
-    # e2e: pinned host queries in, host results out, through the public API.
+    # e2e: pinned host queries in, pinned host results out, every step, through
+    # the public API (HostPipeline: H2D of step b+1 and D2H of step b overlap
+    # the search of step b; each step's copies stay inside the timed region).
+    from paper_1209_0410_b200.pipeline import HostPipeline
     host_batches = [bt.cpu().pin_memory() for bt in batches]
-    host_out = (torch.empty((Q, k), dtype=torch.uint64).pin_memory(),
-                torch.empty((Q, k), dtype=torch.uint32).pin_memory(),
-                torch.empty((Q,), dtype=torch.uint32).pin_memory())
-    dq = torch.empty((Q, 128), dtype=torch.uint8, device=dev)
-
-    def step_e2e(b):
-        if world == 1:
-            sidx.local.search_batch(host_batches[b], k, shard_depth, out=host_out)  # library stages H2D/D2H
-        else:
-            dq.copy_(host_batches[b], non_blocking=True)
-            r = sidx.search(dq, k, shard_depth, out=out)
-            for h, d_ in zip(host_out, r):
-                h.copy_(d_, non_blocking=True)
-            stream.synchronize()
-
-    ms_e2e = timed(step_e2e)
+    host_outs = [(torch.empty((Q, k), dtype=torch.uint64).pin_memory(),
+                  torch.empty((Q, k), dtype=torch.uint32).pin_memory(),
+                  torch.empty((Q,), dtype=torch.uint32).pin_memory()) for _ in range(2)]
+    pipe = HostPipeline(lambda q, out: sidx.search(q, k, shard_depth, out=out), k, Q, device=local)
+    pipe.run(host_batches[:a.warmup], [host_outs[b % 2] for b in range(a.warmup)])
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    pipe.run(host_batches[a.warmup:], [host_outs[b % 2] for b in range(a.steps)], e0, e1)
+    ms_e2e = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms_e2e], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_e2e = float(t.item())
     clocks.stop()
     h2d = Q * 128
     d2h = Q * k * 8 + Q * k * 4 + Q * 4
@@ -396,7 +399,7 @@ def run_ours(a):
             "clocks": clocks.summary(),
             "latency": lat,
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -466,13 +469,28 @@ def run_reference(a):
                                    f"multicurves.hpp restatement, query-parallel on {threads} threads"},
         "e2e": {"value": round(value, 1), "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
+
+
+_JSON_OUT = None
+
+
+def emit(line: dict) -> None:
+    """The one JSON line on the original stdout (everything else -- NCCL's
+    version banner included -- was redirected to stderr in main())."""
+    out = _JSON_OUT or sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
 
 
 def main():
-    # one JSON line on rank 0's stdout: keep NCCL's version banner out of it
-    if os.environ.get("NCCL_DEBUG", "").upper() in ("", "VERSION"):
-        os.environ["NCCL_DEBUG"] = "WARN"
+    global _JSON_OUT
+    # One JSON line on stdout: native libraries (NCCL prints its version with
+    # printf at communicator init) write to fd 1 directly, so move fd 1 to
+    # stderr for the run and keep a private handle on the real stdout.
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     a = parse()
     if a.impl == "reference":
         run_reference(a)

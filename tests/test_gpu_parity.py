@@ -234,3 +234,22 @@ def test_error_behaviour():
         gi.search_batch(rows[:2, :64], 10, 10)  # dimension mismatch
     with pytest.raises(ValueError):
         H.MulticurvesIndex(rows, H.default_scheme(128, 1, 16), H.RAW)  # 2048-bit key > capacity
+
+
+def test_host_pipeline_matches_direct_search():
+    """pipeline.HostPipeline (overlapped H2D / search / D2H) returns exactly the
+    per-batch results of search_batch."""
+    import torch
+    from paper_1209_0410_b200.pipeline import HostPipeline
+    rows = P.gen_rows(0, 20000)
+    gi = H.MulticurvesIndex(rows, H.default_scheme(128, 8, 16), H.LIFTED)
+    batches = [torch.from_numpy(P.gen_queries(b * 500, 500 - 37 * (b % 3), 20000)).pin_memory() for b in range(6)]
+    outs = [(torch.empty((len(q), 10), dtype=torch.uint64).pin_memory(),
+             torch.empty((len(q), 10), dtype=torch.uint32).pin_memory(),
+             torch.empty((len(q),), dtype=torch.uint32).pin_memory()) for q in batches]
+    HostPipeline(lambda q, out: gi.search_batch(q, 10, 350, out=out), 10, 500).run(batches, outs)
+    for q, (ids, sq, ln) in zip(batches, outs):
+        wi, ws, wl = gi.search_batch(q.numpy(), 10, 350)
+        np.testing.assert_array_equal(ids.numpy(), wi)
+        np.testing.assert_array_equal(sq.numpy(), ws)
+        np.testing.assert_array_equal(ln.numpy(), wl)
