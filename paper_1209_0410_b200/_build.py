@@ -38,7 +38,13 @@ def _stale(target: str, deps: list[str]) -> bool:
 
 
 def build(verbose: bool = False, ptxas_info: bool = False) -> str:
-    """Compile every CUDA/C++ source and link libhcg.so; returns its path."""
+    """Compile every CUDA/C++ source and link libhcg.so; returns its path.
+    HCG_DEBUG_BOUNDS=1 in the environment compiles the device bounds checks in
+    (objects go to csrc/build-debug/ so the two builds do not mix)."""
+    global OBJ
+    debug = os.environ.get("HCG_DEBUG_BOUNDS") == "1"
+    if debug:
+        OBJ = os.path.join(CSRC, "build-debug")
     os.makedirs(OBJ, exist_ok=True)
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "hcg.h")]
     jobs = []
@@ -46,7 +52,7 @@ def build(verbose: bool = False, ptxas_info: bool = False) -> str:
         s = os.path.join(CSRC, src)
         o = os.path.join(OBJ, src + ".o")
         if _stale(o, [s] + hdrs) or ptxas_info:
-            flags = list(NVCC_FLAGS)
+            flags = list(NVCC_FLAGS) + (["-DHCG_DEBUG_BOUNDS"] if debug else [])
             if ptxas_info and src.endswith(".cu"):
                 flags += ["-Xptxas", "-v"]
             if src.endswith(".cpp"):
@@ -63,10 +69,14 @@ def build(verbose: bool = False, ptxas_info: bool = False) -> str:
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         list(ex.map(run, jobs))
     objs = [os.path.join(OBJ, s + ".o") for s in CU + CPP]
-    if _stale(LIB, objs):
+    stamp = LIB + ".flavor"
+    flavor = "debug" if debug else "release"
+    if _stale(LIB, objs) or not os.path.exists(stamp) or open(stamp).read() != flavor:
         tmp = LIB + ".tmp"
         run([_nvcc(), "-shared"] + ARCH + ["-cudart", "static", "-o", tmp] + objs)
         os.replace(tmp, LIB)
+        with open(stamp, "w") as f:
+            f.write(flavor)
     return LIB
 
 

@@ -510,6 +510,7 @@ RefineArgs refine_args(const hcg_index* ix, const uint8_t* dq, uint32_t nq, uint
     a.k = k;
     a.id_base = ix->id_base;
     a.id_stride = ix->id_stride;
+    a.n_rows = ix->n;
     return a;
 }
 

@@ -241,6 +241,7 @@ __global__ void __launch_bounds__(kSortThreads) k_downsweep(
         const uint64_t key = skeys[i];
         const uint32_t d = uint32_t((key >> shift) & 255);
         const uint64_t g = uint64_t(gbase[d]) + (i - tile_off[d]);
+        HCG_DASSERT(g < n);
         kout[g] = key;
         vout[g] = svals[i];
     }
@@ -288,6 +289,7 @@ __global__ void k_rank_merge(const uint64_t* __restrict__ ak, const uint32_t* __
         }
     }
     const uint64_t pos = i + lo;
+    HCG_DASSERT(pos < na + nb);
     for (int w = 0; w < ws; ++w) ck[pos * ws + w] = key[w];
     cs[pos] = from_a ? as[i] : bs[i];
 }

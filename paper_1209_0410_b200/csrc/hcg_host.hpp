@@ -70,6 +70,7 @@ struct RefineArgs {
     uint32_t cap;          // kOutCandidates
     unsigned long long* prof;  // unused (kept zero)
     cudaEvent_t ev_mid;        // optional: recorded between the union and gather launches
+    uint64_t n_rows;           // rows in the index (bounds checks)
 };
 // Scratch bytes the refine launch needs (global hash tables when the table
 // does not fit in shared memory); query with scratch == nullptr first.

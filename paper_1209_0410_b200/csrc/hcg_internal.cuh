@@ -11,6 +11,25 @@
 #error "this library targets sm_100a (B200) only"
 #endif
 
+// Device bounds checks, compiled in with -DHCG_DEBUG_BOUNDS (HCG_DEBUG_BOUNDS=1
+// at build time); the normal build compiles them out.  compute-sanitizer is
+// unavailable on the GPU pool, so the -m gpu suite is also run against this
+// build (tools/debug_bounds.sh).
+#ifdef HCG_DEBUG_BOUNDS
+#include <cstdio>
+#define HCG_DASSERT(c)                                                                        \
+    do {                                                                                      \
+        if (!(c)) {                                                                           \
+            printf("hcg bounds check failed: %s (%s:%d)\n", #c, __FILE__, __LINE__);          \
+            __trap();                                                                         \
+        }                                                                                     \
+    } while (0)
+#else
+#define HCG_DASSERT(c) \
+    do {               \
+    } while (0)
+#endif
+
 namespace hcg {
 
 constexpr int kMaxKeyWords = HCG_MAX_KEY_BITS / 64;  // 16

@@ -111,6 +111,7 @@ __global__ void __launch_bounds__(128) k_locate(LocateArgs a) {
     const uint64_t below_n = take / 2;
     uint64_t begin = rank >= below_n ? rank - below_n : 0;
     if (begin + take > a.n) begin = a.n - take;
+    HCG_DASSERT(begin + take <= a.n && rank <= a.n);
     a.out_begin[t] = uint32_t(begin);
     if (a.out_rank) a.out_rank[t] = rank;
 }
@@ -346,6 +347,8 @@ __device__ __forceinline__ void gather_list(const RefineArgs& a, const uint32_t*
         nx[r] = e < n ? __ldcg(list + e) : kEmpty;
     }
     for (uint32_t base = start; base < n; base += step) {
+#pragma unroll
+        for (int r = 0; r < 8; ++r) HCG_DASSERT(nx[r] == kEmpty || nx[r] < a.n_rows);
         uint4 v[8][CR];
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
@@ -555,6 +558,7 @@ __global__ void __launch_bounds__(kRefineThreads) k_union_reg(RefineArgs a, uint
 #pragma unroll
         for (int j = 0; j < JMAX; ++j)
             if ((keep >> j) & 1) out[w++] = id[j];
+        HCG_DASSERT(off + mine <= T && off + mine <= lstride);
         if (tid == kRefineThreads - 1) counts[q] = off + mine;
     }
 }
@@ -615,7 +619,10 @@ __global__ void __launch_bounds__(kRefineThreads) k_union_cas(RefineArgs a, uint
                     uint32_t base = 0;
                     if (lane == leader) base = atomicAdd(&cnt, uint32_t(__popc(b)));
                     base = __shfl_sync(kFull, base, leader);
-                    if (fresh) out[base + __popc(b & lt)] = s;
+                    if (fresh) {
+                        HCG_DASSERT(base + __popc(b & lt) < lstride && s < a.n_rows);
+                        out[base + __popc(b & lt)] = s;
+                    }
                 }
             }
         }
@@ -792,6 +799,7 @@ __global__ void __launch_bounds__(256) k_merge(const uint64_t* __restrict__ pack
         if (e < k) {
             const uint64_t x = tk.a[r];
             const bool none = x == kNone;
+            HCG_DASSERT(e < k && q < nq);
             out_ids[uint64_t(q) * k + e] = none ? ~0ull : (x & 0xFFFFFFFFull);
             out_sq[uint64_t(q) * k + e] = none ? 0xFFFFFFFFu : uint32_t(x >> 32);
             cnt += none ? 0 : 1;
