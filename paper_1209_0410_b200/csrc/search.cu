@@ -489,7 +489,21 @@ __global__ void __launch_bounds__(kRefineThreads) k_union_reg(RefineArgs a, uint
         __syncthreads();
         uint32_t id[JMAX];
         uint32_t pending = 0;
-        {
+        if (kRefineThreads % a.C == 0) {
+            // fixed curve per thread: position (c, p0 + j * step), no walking
+            const uint32_t c = tid % a.C, step = kRefineThreads / a.C;
+            const uint32_t* src = sptr[c] + sbeg[c];
+            uint32_t p = tid / a.C;
+#pragma unroll
+            for (int j = 0; j < JMAX; ++j) {
+                id[j] = 0;
+                if (p < take) {
+                    id[j] = __ldg(src + p);
+                    pending |= 1u << j;
+                }
+                p += step;
+            }
+        } else {
             uint32_t c = 0, p = tid;
             while (p >= take && c + 1 < a.C) {
                 p -= take;
@@ -673,7 +687,9 @@ hcg_status union_reg_launch(const RefineArgs& a, uint32_t* lists, uint32_t* coun
 
 hcg_status launch_union_reg(const RefineArgs& a, uint32_t* lists, uint32_t* counts, uint32_t lstride, uint32_t tb,
                             int device, cudaStream_t st) {
-    const uint32_t jn = (a.C * a.take + kRefineThreads - 1) / kRefineThreads;
+    const uint32_t jn = kRefineThreads % a.C == 0 ? (a.take + kRefineThreads / a.C - 1) / (kRefineThreads / a.C)
+                                                : (a.C * a.take + kRefineThreads - 1) / kRefineThreads;
+    if (jn > 32) return set_error(HCG_ECAPACITY, "union: more than 32 ids per thread");
     if (jn <= 4) return union_reg_launch<4>(a, lists, counts, lstride, tb, device, st);
     if (jn <= 8) return union_reg_launch<8>(a, lists, counts, lstride, tb, device, st);
     if (jn <= 12) return union_reg_launch<12>(a, lists, counts, lstride, tb, device, st);
