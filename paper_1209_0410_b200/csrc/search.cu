@@ -186,6 +186,26 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 
+// Exclusive scan of one value per thread over an NT-thread block (ends with a barrier).
+template <int NT>
+__device__ __forceinline__ uint32_t block_excl_scan_u(uint32_t v, uint32_t* wsum) {
+    constexpr int kW = NT / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t inc = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t t = __shfl_up_sync(kFull, inc, off);
+        if (lane >= off) inc += t;
+    }
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    uint32_t before = 0;
+#pragma unroll
+    for (int w = 0; w < kW; ++w) before += w < warp ? wsum[w] : 0u;
+    __syncthreads();
+    return before + inc - v;
+}
+
 // Exclusive scan of one value per thread over a 256-thread block (ends with a barrier).
 __device__ __forceinline__ uint32_t block_excl_scan256_u(uint32_t v, uint32_t* wsum) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -469,29 +489,28 @@ __global__ void __launch_bounds__(kRefineThreads) k_gather_cta(RefineArgs a, con
 // Kept ids are compacted with one block scan.
 constexpr int kRegRounds = 4;
 
-template <int JMAX>
-__global__ void __launch_bounds__(kRefineThreads) k_union_reg(RefineArgs a, uint32_t* __restrict__ lists,
-                                                              uint32_t* __restrict__ counts, uint32_t lstride,
-                                                              uint32_t tb) {
+template <int JMAX, int NT>
+__global__ void __launch_bounds__(NT) k_union_reg(RefineArgs a, uint32_t* __restrict__ lists,
+                                                  uint32_t* __restrict__ counts, uint32_t lstride, uint32_t tb) {
     extern __shared__ __align__(16) unsigned char smem[];
     unsigned long long* tab = reinterpret_cast<unsigned long long*>(smem);  // [1 << tb]
     const uint32_t** sptr = reinterpret_cast<const uint32_t**>(tab + (size_t(1) << tb));
     uint32_t* sbeg = reinterpret_cast<uint32_t*>(sptr + a.C);
-    uint32_t* wsum = sbeg + a.C;  // [8] scan scratch
+    uint32_t* wsum = sbeg + a.C;  // [NT/32] scan scratch
     const uint32_t T = a.C * a.take;
     const int tid = threadIdx.x;
     const uint32_t take = a.take, shift = 32 - tb, tmask = (1u << tb) - 1;
-    for (uint32_t c = tid; c < a.C; c += kRefineThreads) sptr[c] = a.slots[c];
+    for (uint32_t c = tid; c < a.C; c += NT) sptr[c] = a.slots[c];
 
     for (uint32_t q = blockIdx.x; q < a.nq; q += gridDim.x) {
         __syncthreads();  // previous query done with tab / sbeg
-        for (uint32_t c = tid; c < a.C; c += kRefineThreads) sbeg[c] = a.begins[uint64_t(q) * a.C + c];
+        for (uint32_t c = tid; c < a.C; c += NT) sbeg[c] = a.begins[uint64_t(q) * a.C + c];
         __syncthreads();
         uint32_t id[JMAX];
         uint32_t pending = 0;
-        if (kRefineThreads % a.C == 0) {
+        if (NT % a.C == 0) {
             // fixed curve per thread: position (c, p0 + j * step), no walking
-            const uint32_t c = tid % a.C, step = kRefineThreads / a.C;
+            const uint32_t c = tid % a.C, step = NT / a.C;
             const uint32_t* src = sptr[c] + sbeg[c];
             uint32_t p = tid / a.C;
 #pragma unroll
@@ -511,13 +530,13 @@ __global__ void __launch_bounds__(kRefineThreads) k_union_reg(RefineArgs a, uint
             }
 #pragma unroll
             for (int j = 0; j < JMAX; ++j) {
-                const uint32_t i = tid + j * kRefineThreads;
+                const uint32_t i = tid + j * NT;
                 id[j] = 0;
                 if (i < T) {
                     id[j] = __ldg(sptr[c] + sbeg[c] + p);
                     pending |= 1u << j;
                 }
-                p += kRefineThreads;
+                p += NT;
                 while (p >= take && c + 1 < a.C) {
                     p -= take;
                     ++c;
@@ -531,7 +550,7 @@ __global__ void __launch_bounds__(kRefineThreads) k_union_reg(RefineArgs a, uint
 #pragma unroll
             for (int j = 0; j < JMAX; ++j)
                 if ((pending >> j) & 1)
-                    tab[(id[j] * mul) >> shift] = (uint64_t(id[j]) << 32) | uint32_t(tid + j * kRefineThreads);
+                    tab[(id[j] * mul) >> shift] = (uint64_t(id[j]) << 32) | uint32_t(tid + j * NT);
             __syncthreads();
 #pragma unroll
             for (int j = 0; j < JMAX; ++j) {
@@ -539,19 +558,19 @@ __global__ void __launch_bounds__(kRefineThreads) k_union_reg(RefineArgs a, uint
                     const uint64_t o = tab[(id[j] * mul) >> shift];
                     if (uint32_t(o >> 32) == id[j]) {
                         pending &= ~(1u << j);
-                        if (uint32_t(o) == uint32_t(tid + j * kRefineThreads)) keep |= 1u << j;
+                        if (uint32_t(o) == uint32_t(tid + j * NT)) keep |= 1u << j;
                     }
                 }
             }
             if (!__syncthreads_or(pending != 0)) break;
         }
         if (__syncthreads_or(pending != 0)) {  // rare: CAS set over the cleared table
-            for (uint32_t i = tid; i <= tmask; i += kRefineThreads) tab[i] = ~0ull;
+            for (uint32_t i = tid; i <= tmask; i += NT) tab[i] = ~0ull;
             __syncthreads();
 #pragma unroll
             for (int j = 0; j < JMAX; ++j) {
                 if ((pending >> j) & 1) {
-                    const unsigned long long mine = (uint64_t(id[j]) << 32) | uint32_t(tid + j * kRefineThreads);
+                    const unsigned long long mine = (uint64_t(id[j]) << 32) | uint32_t(tid + j * NT);
                     uint32_t h = hash_slot(id[j]) >> shift;
                     while (true) {
                         const unsigned long long prev = atomicCAS(&tab[h], ~0ull, mine);
@@ -566,14 +585,14 @@ __global__ void __launch_bounds__(kRefineThreads) k_union_reg(RefineArgs a, uint
             }
         }
         const uint32_t mine = __popc(keep);
-        const uint32_t off = block_excl_scan256_u(mine, wsum);
+        const uint32_t off = block_excl_scan_u<NT>(mine, wsum);
         uint32_t* out = lists + uint64_t(q) * lstride + off;
         uint32_t w = 0;
 #pragma unroll
         for (int j = 0; j < JMAX; ++j)
             if ((keep >> j) & 1) out[w++] = id[j];
         HCG_DASSERT(off + mine <= T && off + mine <= lstride);
-        if (tid == kRefineThreads - 1) counts[q] = off + mine;
+        if (tid == NT - 1) counts[q] = off + mine;
     }
 }
 
@@ -673,29 +692,38 @@ size_t union_smem_bytes(uint32_t C, uint32_t T, uint32_t tb) {
 }
 
 
-template <int JMAX>
+template <int JMAX, int NT>
 hcg_status union_reg_launch(const RefineArgs& a, uint32_t* lists, uint32_t* counts, uint32_t lstride, uint32_t tb,
                             int device, cudaStream_t st) {
-    auto kern = k_union_reg<JMAX>;
-    const size_t smem = (size_t(8) << tb) + size_t(a.C) * 12 + 64;
+    auto kern = k_union_reg<JMAX, NT>;
+    const size_t smem = (size_t(8) << tb) + size_t(a.C) * 12 + 4 * (NT / 32) + 64;
     static bool cfg[64] = {};
     HCG_RET_IF(opt_in_smem(kern, device, cfg));
-    const uint32_t grid = persistent_grid(reinterpret_cast<const void*>(kern), smem, device, a.nq);
-    kern<<<grid, kRefineThreads, smem, st>>>(a, lists, counts, lstride, tb);
+    int sms = 148, per_sm = 1;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem);
+    const uint32_t grid = std::min<uint32_t>(a.nq, uint32_t(sms * std::max(per_sm, 1)));
+    kern<<<grid, NT, smem, st>>>(a, lists, counts, lstride, tb);
     return check_launch("k_union_reg");
 }
 
+template <int NT>
+hcg_status union_reg_dispatch(const RefineArgs& a, uint32_t* lists, uint32_t* counts, uint32_t lstride, uint32_t tb,
+                              int device, cudaStream_t st) {
+    const uint32_t jn = NT % a.C == 0 ? (a.take + NT / a.C - 1) / (NT / a.C) : (a.C * a.take + NT - 1) / NT;
+    if (jn > 32) return set_error(HCG_ECAPACITY, "union: more than 32 ids per thread");
+    if (jn <= 4) return union_reg_launch<4, NT>(a, lists, counts, lstride, tb, device, st);
+    if (jn <= 8) return union_reg_launch<8, NT>(a, lists, counts, lstride, tb, device, st);
+    if (jn <= 12) return union_reg_launch<12, NT>(a, lists, counts, lstride, tb, device, st);
+    if (jn <= 16) return union_reg_launch<16, NT>(a, lists, counts, lstride, tb, device, st);
+    if (jn <= 24) return union_reg_launch<24, NT>(a, lists, counts, lstride, tb, device, st);
+    return union_reg_launch<32, NT>(a, lists, counts, lstride, tb, device, st);
+}
+
+// 256-thread CTAs measured best (128: +15 %, 512: +18 %, 1024: +75 % union time).
 hcg_status launch_union_reg(const RefineArgs& a, uint32_t* lists, uint32_t* counts, uint32_t lstride, uint32_t tb,
                             int device, cudaStream_t st) {
-    const uint32_t jn = kRefineThreads % a.C == 0 ? (a.take + kRefineThreads / a.C - 1) / (kRefineThreads / a.C)
-                                                : (a.C * a.take + kRefineThreads - 1) / kRefineThreads;
-    if (jn > 32) return set_error(HCG_ECAPACITY, "union: more than 32 ids per thread");
-    if (jn <= 4) return union_reg_launch<4>(a, lists, counts, lstride, tb, device, st);
-    if (jn <= 8) return union_reg_launch<8>(a, lists, counts, lstride, tb, device, st);
-    if (jn <= 12) return union_reg_launch<12>(a, lists, counts, lstride, tb, device, st);
-    if (jn <= 16) return union_reg_launch<16>(a, lists, counts, lstride, tb, device, st);
-    if (jn <= 24) return union_reg_launch<24>(a, lists, counts, lstride, tb, device, st);
-    return union_reg_launch<32>(a, lists, counts, lstride, tb, device, st);
+    return union_reg_dispatch<256>(a, lists, counts, lstride, tb, device, st);
 }
 
 // Query chunk so the per-call list scratch stays within kListBudget.
@@ -712,7 +740,7 @@ hcg_status refine_dispatch(const RefineArgs& a_in, void* scratch, size_t* scratc
     const uint32_t utb = std::min<uint32_t>(tb + 1, 16);
     const size_t usmem = union_smem_bytes(a_in.C, T, utb);
     const bool smem_union = T <= kUnionMaxT && usmem <= 160 * 1024;
-    const bool reg_union = T <= 32u * kRefineThreads && (size_t(8) << tb) <= 128 * 1024 && !getenv("HCG_UNION_SMEM");
+    const bool reg_union = T <= 32u * 256 && (size_t(8) << tb) <= 128 * 1024 && !getenv("HCG_UNION_SMEM");
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     const uint32_t chunk = uint32_t(std::max<size_t>(1, std::min<size_t>(a_in.nq, kListBudget / (size_t(lstride) * 4))));
