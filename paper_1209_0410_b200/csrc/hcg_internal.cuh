@@ -178,10 +178,11 @@ struct WarpTopK {
             if (!p_lt) a[r] = p;
             else if (a[r] > x) a[r] = x;
         }
-        uint64_t mine = a[0];
+        // arithmetic select: a runtime-indexed a[thr_reg] would spill the
+        // list to local memory
+        uint64_t mine = 0;
 #pragma unroll
-        for (int r = 1; r < R; ++r)
-            if (r == thr_reg) mine = a[r];
+        for (int r = 0; r < R; ++r) mine |= a[r] & (0ull - uint64_t(r == thr_reg));
         thr = __shfl_sync(kFull, mine, thr_lane);
     }
 

@@ -757,7 +757,7 @@ hcg_status refine_dispatch(const RefineArgs& a_in, void* scratch, size_t* scratc
     uint32_t* counts = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(scratch) + lists_bytes);
     uint32_t* gtab = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(scratch) + lists_bytes + counts_bytes);
     // 4 CTAs/SM: measured best (5-6 spill and lose ~15 %)
-    auto gk = k_gather<R, CR, R <= 2 ? 4 : 2>;
+    auto gk = k_gather<R, CR, R <= 4 ? 4 : 2>;
     static bool cfg_u[64] = {};
     if (smem_union) HCG_RET_IF(opt_in_smem(k_union, device, cfg_u));
     int g_per_sm = 1;

@@ -40,3 +40,4 @@ if os.environ.get("UNION_AB"):
         ms = sorted(ix.search_timed(qs[b % 4], k, D, out=out)[1] for b in range(6))[3]
         print(f"union={v} union_ms={ms:.3f}", flush=True)
 
+
