@@ -41,13 +41,32 @@ __device__ __forceinline__ unsigned lanemask_lt_s() {
 }
 
 // ----------------------------------------------------------------- K3a ----
-template <int DMAX, int WSMAX>
+// -1 / 0 / 1: the stored suffix key at e vs the query suffix qs (ws words,
+// most significant first).
+template <int WSMAX>
+__device__ __forceinline__ int suffix_cmp(const uint64_t* e, const uint64_t (&qs)[WSMAX], int ws) {
+    int o = 0;
+#pragma unroll
+    for (int w = WSMAX - 1; w >= 0; --w) {
+        if (o == 0 && w < ws) {
+            const uint64_t ev = __ldg(e + w);
+            o = ev < qs[w] ? -1 : (ev > qs[w] ? 1 : 0);
+        }
+    }
+    return o;
+}
+
+// COOP: one WARP per (query, curve) and a 32-ary lower_bound (each round the
+// lanes probe 32 splitters and a ballot narrows the range 33x: ~5 dependent
+// loads at 10M instead of 24) -- the small-batch latency path.
+template <int DMAX, int WSMAX, bool COOP>
 __global__ void __launch_bounds__(128) k_locate(LocateArgs a) {
     constexpr int WMAX = DMAX / 2 > kMaxKeyWords ? kMaxKeyWords : (DMAX / 2 < 1 ? 1 : DMAX / 2);
     __shared__ uint32_t lut[256];
     for (int i = threadIdx.x; i < 256; i += blockDim.x) lut[i] = a.lut[i];
     __syncthreads();
-    const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t t = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> (COOP ? 5 : 0);
+    const int lane = threadIdx.x & 31;
     if (t >= uint64_t(a.nq) * a.C) return;
     const uint32_t q = uint32_t(t / a.C), c = uint32_t(t % a.C);
     const CurveDev& cv = a.curves[c];
@@ -85,24 +104,33 @@ __global__ void __launch_bounds__(128) k_locate(LocateArgs a) {
 #pragma unroll
         for (int w = 0; w < WSMAX; ++w) qs[w] = w < ws ? (key[w < WMAX ? w : 0] & (w == ws - 1 ? below : ~0ull)) : 0ull;
         const uint64_t* keys = cv.keys;
-        uint64_t lo = 0, len = a.n;
-        while (len > 0) {
-            const uint64_t half = len >> 1;
-            const uint64_t mid = lo + half;
-            const uint64_t* e = keys + mid * ws;
-            int o = 0;
-#pragma unroll
-            for (int w = WSMAX - 1; w >= 0; --w) {
-                if (o == 0 && w < ws) {
-                    const uint64_t ev = __ldg(e + w);
-                    o = ev < qs[w] ? -1 : (ev > qs[w] ? 1 : 0);
-                }
+        const uint32_t wsu = uint32_t(ws);
+        uint64_t lo = 0;
+        if (COOP) {
+            uint64_t hi = a.n;  // the answer lies in [lo, hi]
+            while (hi - lo > 32) {
+                const uint64_t len = hi - lo;
+                const uint64_t sp = lo + ((uint64_t(lane) + 1) * len) / 33;  // strictly increasing, < hi
+                const unsigned b = __ballot_sync(kFull, suffix_cmp<WSMAX>(keys + sp * wsu, qs, ws) < 0);
+                const int cnt = __popc(b);
+                const uint64_t s_lo = __shfl_sync(kFull, sp, cnt > 0 ? cnt - 1 : 0);
+                const uint64_t s_hi = __shfl_sync(kFull, sp, cnt < 32 ? cnt : 31);
+                if (cnt > 0) lo = s_lo + 1;
+                if (cnt < 32) hi = s_hi;
             }
-            if (o < 0) {
-                lo = mid + 1;
-                len -= half + 1;
-            } else {
-                len = half;
+            const bool less = lo + lane < hi && suffix_cmp<WSMAX>(keys + (lo + lane) * wsu, qs, ws) < 0;
+            lo += __popc(__ballot_sync(kFull, less));
+        } else {
+            uint64_t len = a.n;
+            while (len > 0) {
+                const uint64_t half = len >> 1;
+                const uint64_t mid = lo + half;
+                if (suffix_cmp<WSMAX>(keys + mid * wsu, qs, ws) < 0) {
+                    lo = mid + 1;
+                    len -= half + 1;
+                } else {
+                    len = half;
+                }
             }
         }
         rank = lo;
@@ -112,14 +140,19 @@ __global__ void __launch_bounds__(128) k_locate(LocateArgs a) {
     uint64_t begin = rank >= below_n ? rank - below_n : 0;
     if (begin + take > a.n) begin = a.n - take;
     HCG_DASSERT(begin + take <= a.n && rank <= a.n);
-    a.out_begin[t] = uint32_t(begin);
-    if (a.out_rank) a.out_rank[t] = rank;
+    if (!COOP || lane == 0) {
+        a.out_begin[t] = uint32_t(begin);
+        if (a.out_rank) a.out_rank[t] = rank;
+    }
 }
 
 template <int DMAX, int WSMAX>
 static void locate_launch(const LocateArgs& a, cudaStream_t st) {
     const uint64_t total = uint64_t(a.nq) * a.C;
-    k_locate<DMAX, WSMAX><<<unsigned((total + 127) / 128), 128, 0, st>>>(a);
+    if (total <= 1024)  // small batches: a warp per (query, curve), ~5 dependent loads
+        k_locate<DMAX, WSMAX, true><<<unsigned((total * 32 + 127) / 128), 128, 0, st>>>(a);
+    else
+        k_locate<DMAX, WSMAX, false><<<unsigned((total + 127) / 128), 128, 0, st>>>(a);
 }
 
 template <int DMAX>
@@ -448,11 +481,11 @@ __global__ void __launch_bounds__(kRefineThreads, MINB) k_gather(RefineArgs a, c
 
 // K3c for small batches (latency): one CTA per query, the 8 warps split the
 // list and warp 0 merges their top-k lists through shared memory.
-template <int R, int CR>
-__global__ void __launch_bounds__(kRefineThreads) k_gather_cta(RefineArgs a, const uint32_t* __restrict__ lists,
-                                                               const uint32_t* __restrict__ counts, uint32_t lstride) {
+template <int R, int CR, int NW>
+__global__ void __launch_bounds__(NW * 32) k_gather_cta(RefineArgs a, const uint32_t* __restrict__ lists,
+                                                        const uint32_t* __restrict__ counts, uint32_t lstride) {
     constexpr int KCAP = 32 * R;
-    constexpr int kWarps = kRefineThreads / 32;
+    constexpr int kWarps = NW;
     __shared__ uint64_t mbuf[kWarps * KCAP];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (uint32_t q = blockIdx.x; q < a.nq; q += gridDim.x) {
@@ -461,7 +494,7 @@ __global__ void __launch_bounds__(kRefineThreads) k_gather_cta(RefineArgs a, con
         load_query<CR>(a, q, lane, qv);
         WarpTopK<R> tk;
         tk.init(int(a.k));
-        gather_list<R, CR>(a, lists + uint64_t(q) * lstride, n, warp * 32, kRefineThreads, qv, lane, tk);
+        gather_list<R, CR>(a, lists + uint64_t(q) * lstride, n, warp * 32, NW * 32, qv, lane, tk);
 #pragma unroll
         for (int r = 0; r < R; ++r) mbuf[warp * KCAP + lane * R + r] = tk.a[r];
         __syncthreads();
@@ -788,7 +821,14 @@ hcg_status refine_dispatch(const RefineArgs& a_in, void* scratch, size_t* scratc
         }
         if (a.nq * 2 < uint32_t(sms) * uint32_t(std::max(g_per_sm, 1)) * 8) {
             // fewer queries than half the resident warps: spread each query over a CTA (latency)
-            k_gather_cta<R, CR><<<a.nq, kRefineThreads, 0, st>>>(a, lists, counts, lstride);
+            bool wide = false;
+            if constexpr (R <= 2) {
+                if (a.nq <= uint32_t(sms)) {  // very small batches: 32 warps per query
+                    k_gather_cta<R, CR, 32><<<a.nq, 1024, 0, st>>>(a, lists, counts, lstride);
+                    wide = true;
+                }
+            }
+            if (!wide) k_gather_cta<R, CR, 8><<<a.nq, kRefineThreads, 0, st>>>(a, lists, counts, lstride);
             HCG_RET_IF(check_launch("k_gather_cta"));
             continue;
         }
