@@ -188,3 +188,68 @@ def spin_idle(clock):
         if d > 200e-6:
             time.sleep(min(d, 1e-3) - 100e-6)
     return idle
+
+
+class ShardedBackend:
+    """Multi-GPU serving (configs[4]): rank 0 runs the controller; every
+    dispatch broadcasts (first, count) to the other ranks, all ranks run the
+    sharded search of that batch (whose NCCL all-gather keeps them in
+    lockstep), and rank 0 observes completion.  One batch in flight across the
+    group (slots=1): the collectives of consecutive batches stay ordered."""
+
+    STOP = -1
+
+    def __init__(self, search_fn, queries, k: int, max_batch: int = 8192):
+        import torch
+        self.torch = torch
+        self.search_fn = search_fn  # search_fn(queries_slice, out)
+        self.queries = queries
+        dev = queries.device
+        self.cmd = torch.zeros(2, dtype=torch.int64, device=dev)
+        self.out = (torch.empty((max_batch, k), dtype=torch.uint64, device=dev),
+                    torch.empty((max_batch, k), dtype=torch.uint32, device=dev),
+                    torch.empty((max_batch,), dtype=torch.uint32, device=dev))
+        self.start = None
+        self.clock = None
+
+    def _run_batch(self, first: int, count: int):
+        out = tuple(o[:count] for o in self.out)
+        self.search_fn(self.queries[first:first + count], out)
+
+    def begin(self):
+        torch = self.torch
+        torch.cuda.synchronize()
+        self.start = torch.cuda.Event(enable_timing=True)
+        self.start.record()
+        self.start.synchronize()
+        self.clock = _WallClock()
+        return self.clock
+
+    def launch(self, first: int, count: int, slot: int):
+        import torch.distributed as dist
+        self.cmd[0], self.cmd[1] = first, count
+        dist.broadcast(self.cmd, 0)
+        self._run_batch(first, count)
+        ev = self.torch.cuda.Event(enable_timing=True)
+        ev.record()
+        return ev
+
+    def poll(self, ev):
+        if not ev.query():
+            return None
+        return self.start.elapsed_time(ev) * 1e-3
+
+    def stop(self):
+        import torch.distributed as dist
+        self.cmd[0], self.cmd[1] = self.STOP, 0
+        dist.broadcast(self.cmd, 0)
+
+    def follow(self):
+        """Non-zero ranks: run every broadcast batch until the stop command."""
+        import torch.distributed as dist
+        while True:
+            dist.broadcast(self.cmd, 0)
+            first, count = (int(x) for x in self.cmd.tolist())
+            if first == self.STOP:
+                break
+            self._run_batch(first, count)
