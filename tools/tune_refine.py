@@ -41,3 +41,4 @@ if os.environ.get("UNION_AB"):
         print(f"union={v} union_ms={ms:.3f}", flush=True)
 
 
+
