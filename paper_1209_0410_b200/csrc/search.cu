@@ -59,8 +59,8 @@ __device__ __forceinline__ int suffix_cmp(const uint64_t* e, const uint64_t (&qs
 // COOP: one WARP per (query, curve) and a 32-ary lower_bound (each round the
 // lanes probe 32 splitters and a ballot narrows the range 33x: ~5 dependent
 // loads at 10M instead of 24) -- the small-batch latency path.
-template <int DMAX, int WSMAX, bool COOP>
-__global__ void __launch_bounds__(128) k_locate(LocateArgs a) {
+template <int DMAX, int WSMAX, bool COOP, int MINB = 1>
+__global__ void __launch_bounds__(128, MINB) k_locate(LocateArgs a) {
     constexpr int WMAX = DMAX / 2 > kMaxKeyWords ? kMaxKeyWords : (DMAX / 2 < 1 ? 1 : DMAX / 2);
     __shared__ uint32_t lut[256];
     for (int i = threadIdx.x; i < 256; i += blockDim.x) lut[i] = a.lut[i];
@@ -151,8 +151,8 @@ static void locate_launch(const LocateArgs& a, cudaStream_t st) {
     const uint64_t total = uint64_t(a.nq) * a.C;
     if (total <= 1024)  // small batches: a warp per (query, curve), ~5 dependent loads
         k_locate<DMAX, WSMAX, true><<<unsigned((total * 32 + 127) / 128), 128, 0, st>>>(a);
-    else
-        k_locate<DMAX, WSMAX, false><<<unsigned((total + 127) / 128), 128, 0, st>>>(a);
+    else  // 8 CTAs/SM: measured 3 % faster than the 88-register default
+        k_locate<DMAX, WSMAX, false, (DMAX <= 16 ? 8 : 1)><<<unsigned((total + 127) / 128), 128, 0, st>>>(a);
 }
 
 template <int DMAX>

@@ -42,3 +42,4 @@ if os.environ.get("UNION_AB"):
 
 
 
+
