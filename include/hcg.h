@@ -76,10 +76,18 @@ typedef enum hcg_status {
 
 typedef enum hcg_curve_kind { HCG_ZORDER = 0, HCG_HILBERT = 1 } hcg_curve_kind;
 
+/* Element type of the descriptors.  HCG_U8: bytes (bvecs) seen through the
+ * scheme's view (cell_lut, dist_scale), distances exact integers.  HCG_F32:
+ * the reference's float components as-is (fvecs): quantized on the device by
+ * float_to_ordinal >> (32 - m) (curve.cpp:166-174), squared distances
+ * accumulated in double (vecio.cpp:87-95; same terms, tree order: within
+ * 1e-15 relative of the reference), searched with hcg_search_f32. */
+typedef enum hcg_dtype { HCG_U8 = 0, HCG_F32 = 1 } hcg_dtype;
+
 #define HCG_MAX_KEY_BITS 1024  /* HC_MAX_KEY_BITS, keys.hpp:15-23 */
 #define HCG_MAX_CURVE_DIMS 128 /* dims feeding one curve          */
 #define HCG_MAX_K 256          /* largest k of the warp top-k      */
-#define HCG_MAX_ROW_BYTES 512  /* descriptor length (bytes)        */
+#define HCG_MAX_ROW_BYTES 512  /* descriptor length (bytes): 512 u8 / 128 f32 */
 
 /* ProjectionScheme (multicurves.hpp:18-32) plus the view of the bytes. */
 typedef struct hcg_scheme {
@@ -89,8 +97,9 @@ typedef struct hcg_scheme {
     uint32_t curve_kind;        /* hcg_curve_kind                                  */
     const uint32_t* assign_off; /* curves+1 offsets into assign                    */
     const uint32_t* assign;     /* assign[assign_off[c] + s] = input dim of slot s */
-    uint32_t cell_lut[256];     /* quantized cell of each byte value (m bits)      */
-    double dist_scale;          /* view scale: distance = sqrt(sqdist) * dist_scale */
+    uint32_t cell_lut[256];     /* HCG_U8: quantized cell of each byte value        */
+    double dist_scale;          /* HCG_U8 view scale: distance = sqrt(sqdist)*scale */
+    uint32_t dtype;             /* an hcg_dtype; 0 = HCG_U8                        */
 } hcg_scheme;
 
 typedef struct hcg_index hcg_index;
@@ -109,7 +118,8 @@ hcg_status hcg_make_lut(float offset, float scale, uint32_t bits_per_dim, uint32
 hcg_status hcg_default_assignment(uint32_t d_full, uint32_t curves, uint32_t* assign_off,
                                   uint32_t* assign);
 
-/* Build an index over n descriptors (rows: n x d_full bytes).  The id of row s
+/* Build an index over n descriptors (rows: n x d_full elements of the scheme's
+ * dtype; every `rows` / `queries` pointer below is d_full elements per row).  The id of row s
  * is id_base + s * id_stride (the dataset's ids 0..n-1 are base 0, stride 1; a
  * shard of `id mod G` partitioning is base r, stride G).  The index copies the
  * rows into HBM and owns all device memory. */
@@ -123,6 +133,7 @@ uint32_t hcg_curves(const hcg_index* index);
 uint32_t hcg_key_words(const hcg_index* index, uint32_t curve);
 /* Device bytes owned by the index. */
 uint64_t hcg_device_bytes(const hcg_index* index);
+uint32_t hcg_index_dtype(const hcg_index* index); /* hcg_dtype of the rows */
 
 /* Batched search: for each of nq queries (nq x d_full bytes) the top-k of the
  * deduplicated union of every curve's probe-depth window, ordered by
@@ -141,6 +152,13 @@ hcg_status hcg_search(const hcg_index* index, const uint8_t* queries, uint32_t n
 hcg_status hcg_search_timed(const hcg_index* index, const uint8_t* queries, uint32_t nq, uint32_t k,
                             uint32_t depth, uint64_t* out_ids, uint32_t* out_sqdist,
                             uint32_t* out_len, float* ms_out, void* stream);
+
+/* hcg_search for an HCG_F32 index: queries are nq x d_full floats, out_sqdist
+ * are the reference's squared distances in double (distance = sqrt).  Fails
+ * with HCG_ENONFINITE on a NaN/Inf query component (curve.cpp:167). */
+hcg_status hcg_search_f32(const hcg_index* index, const float* queries, uint32_t nq, uint32_t k,
+                          uint32_t depth, uint64_t* out_ids, double* out_sqdist, uint32_t* out_len,
+                          void* stream);
 
 /* Per-shard search writing packed (sqdist << 32 | id) u64 per result, nq x k,
  * padding UINT64_MAX; requires ids < 2^32.  Input to hcg_merge_packed. */
@@ -168,9 +186,11 @@ hcg_status hcg_save(const hcg_index* index, const char* path);
 hcg_status hcg_load(const char* path, int device, void* stream, hcg_index** out);
 
 /* ---- bvecs / fvecs records (vecio.cpp:18-85): u32 LE dim + payload ---- */
-typedef enum hcg_vector_format { HCG_FVECS = 0, HCG_BVECS = 1 } hcg_vector_format;
-/* *rows_out (n x dim bytes) is malloc'ed; release with hcg_free_buffer.  fvecs
- * components must be byte values of the view offset + b * scale. */
+typedef enum hcg_vector_format { HCG_FVECS = 0, HCG_BVECS = 1, HCG_FVECS_F32 = 2 } hcg_vector_format;
+/* *rows_out is malloc'ed; release with hcg_free_buffer.  HCG_BVECS / HCG_FVECS:
+ * n x dim bytes, fvecs components must be byte values of the view
+ * offset + b * scale.  HCG_FVECS_F32: n x dim floats as stored (offset and
+ * scale unused), the rows of an HCG_F32 index. */
 hcg_status hcg_read_vectors(const char* path, uint32_t format, float offset, float scale, uint8_t** rows_out,
                             uint64_t* n_out, uint32_t* dim_out);
 hcg_status hcg_write_vectors(const char* path, uint32_t format, float offset, float scale, const uint8_t* rows,
@@ -200,6 +220,11 @@ hcg_status hcg_candidates(const hcg_index* index, const uint8_t* queries, uint32
 hcg_status hcg_brute_force(const hcg_index* index, const uint8_t* queries, uint32_t nq, uint32_t k,
                            uint64_t* out_ids, uint32_t* out_sqdist, uint32_t* out_len,
                            void* stream);
+/* hcg_brute_force for an HCG_F32 index (double squared distances; +inf and
+ * id UINT64_MAX pad lists shorter than k). */
+hcg_status hcg_brute_force_f32(const hcg_index* index, const float* queries, uint32_t nq, uint32_t k,
+                               uint64_t* out_ids, double* out_sqdist, uint32_t* out_len,
+                               void* stream);
 
 /* ---- probe-depth planner (equivalence module, host math) ---- */
 /* P[Bin(trials, p) > phi]. */

@@ -20,11 +20,14 @@ HCG_ENODEV = -6
 HCG_EIO = -7
 HCG_FVECS = 0
 HCG_BVECS = 1
+HCG_FVECS_F32 = 2
 
 HCG_ZORDER = 0
 HCG_HILBERT = 1
 HCG_MAX_K = 256
 HCG_MAX_KEY_BITS = 1024
+HCG_U8 = 0
+HCG_F32 = 1
 
 # Every symbol include/hcg.h declares (checked by tests/test_abi.py).
 EXPORTS = [
@@ -32,7 +35,7 @@ EXPORTS = [
     "hcg_free", "hcg_size", "hcg_curves", "hcg_key_words", "hcg_device_bytes", "hcg_search",
     "hcg_search_timed", "hcg_search_packed", "hcg_merge_packed", "hcg_keys", "hcg_sorted", "hcg_windows",
     "hcg_candidates", "hcg_brute_force", "hcg_binomial_tail", "hcg_miss_bound",
-    "hcg_plan_depth", "hcg_gen_rows", "hcg_gen_queries", "hcg_insert", "hcg_save", "hcg_load",
+    "hcg_search_f32", "hcg_brute_force_f32", "hcg_index_dtype", "hcg_plan_depth", "hcg_gen_rows", "hcg_gen_queries", "hcg_insert", "hcg_save", "hcg_load",
     "hcg_read_vectors", "hcg_write_vectors", "hcg_free_buffer",
 ]
 
@@ -47,6 +50,7 @@ class HcgScheme(C.Structure):
         ("assign", C.POINTER(C.c_uint32)),
         ("cell_lut", C.c_uint32 * 256),
         ("dist_scale", C.c_double),
+        ("dtype", C.c_uint32),
     ]
 
 
@@ -92,6 +96,8 @@ def lib() -> C.CDLL:
     L.hcg_key_words.argtypes = [vp, u32]
     L.hcg_device_bytes.restype = u64
     L.hcg_device_bytes.argtypes = [vp]
+    L.hcg_index_dtype.restype = u32
+    L.hcg_index_dtype.argtypes = [vp]
     L.hcg_search.argtypes = [vp, vp, u32, u32, u32, vp, vp, vp, vp]
     L.hcg_search_timed.argtypes = [vp, vp, u32, u32, u32, vp, vp, vp, P(C.c_float), vp]
     L.hcg_search_packed.argtypes = [vp, vp, u32, u32, u32, vp, vp]
@@ -101,6 +107,8 @@ def lib() -> C.CDLL:
     L.hcg_windows.argtypes = [vp, vp, u32, u32, vp, vp, vp, vp]
     L.hcg_candidates.argtypes = [vp, vp, u32, u32, vp, u32, vp, vp]
     L.hcg_brute_force.argtypes = [vp, vp, u32, u32, vp, vp, vp, vp]
+    L.hcg_search_f32.argtypes = [vp, vp, u32, u32, u32, vp, vp, vp, vp]
+    L.hcg_brute_force_f32.argtypes = [vp, vp, u32, u32, vp, vp, vp, vp]
     L.hcg_binomial_tail.restype = C.c_double
     L.hcg_binomial_tail.argtypes = [u32, C.c_double, u32]
     L.hcg_miss_bound.restype = C.c_double
@@ -118,7 +126,7 @@ def lib() -> C.CDLL:
     L.hcg_free_buffer.restype = None
     for name in ("hcg_make_lut", "hcg_default_assignment", "hcg_build", "hcg_free", "hcg_search",
                  "hcg_search_timed", "hcg_search_packed", "hcg_merge_packed", "hcg_keys", "hcg_sorted", "hcg_windows",
-                 "hcg_candidates", "hcg_brute_force", "hcg_gen_rows", "hcg_gen_queries", "hcg_insert",
+                 "hcg_candidates", "hcg_brute_force", "hcg_search_f32", "hcg_brute_force_f32", "hcg_gen_rows", "hcg_gen_queries", "hcg_insert",
                  "hcg_save", "hcg_load", "hcg_read_vectors", "hcg_write_vectors"):
         getattr(L, name).restype = C.c_int
     del u8

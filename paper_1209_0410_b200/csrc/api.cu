@@ -17,6 +17,7 @@
 struct hcg_index {
     int device = 0;
     uint32_t d_full = 0, pitch = 0, C = 0, m = 0, kind = 0;
+    uint32_t dtype = HCG_U8, row_bytes = 0;  // row_bytes = d_full * element size
     double dist_scale = 1.0;
     uint64_t n = 0, id_base = 0, id_stride = 1;
     std::vector<uint32_t> off, assign;
@@ -211,8 +212,10 @@ hcg_status dev_alloc(T** p, size_t count, uint64_t* bytes) {
 
 hcg_status validate_scheme(const hcg_scheme* s) {
     if (!s) return set_error(HCG_EINVAL, "null scheme");
-    if (s->d_full < 1 || s->d_full > HCG_MAX_ROW_BYTES)
-        return set_error(HCG_ECAPACITY, "d_full must be in [1, " + std::to_string(HCG_MAX_ROW_BYTES) + "]");
+    if (s->dtype > HCG_F32) return set_error(HCG_EINVAL, "unknown descriptor dtype");
+    const uint32_t esize = s->dtype == HCG_F32 ? 4 : 1;
+    if (s->d_full < 1 || uint64_t(s->d_full) * esize > HCG_MAX_ROW_BYTES)
+        return set_error(HCG_ECAPACITY, "d_full must be in [1, " + std::to_string(HCG_MAX_ROW_BYTES / esize) + "]");
     if (s->curves < 1 || s->curves > s->d_full) return set_error(HCG_EINVAL, "curves must be in [1, d_full]");
     if (s->bits_per_dim < 1 || s->bits_per_dim > 32) return set_error(HCG_EINVAL, "bits_per_dim out of range [1,32]");
     if (s->curve_kind > 1) return set_error(HCG_EINVAL, "unknown curve kind");
@@ -234,6 +237,7 @@ hcg_status validate_scheme(const hcg_scheme* s) {
     }
     for (bool cv : covered)
         if (!cv) return set_error(HCG_EINVAL, "input dimension not covered by any curve");
+    if (s->dtype == HCG_F32) return HCG_OK;  // cells computed on the device; the table is unused
     const uint64_t lim = s->bits_per_dim == 32 ? (1ull << 32) : (1ull << s->bits_per_dim);
     for (int b = 0; b < 256; ++b)
         if (s->cell_lut[b] >= lim) return set_error(HCG_EINVAL, "cell_lut entry exceeds 2^m");
@@ -259,15 +263,20 @@ hcg_status keygen_reduce(const hcg_index* ix, uint32_t c, const uint8_t* rows, u
     const uint32_t d = ix->off[c + 1] - ix->off[c];
     const uint32_t W = (d * ix->m + 63) / 64;
     *soa = sc.alloc<uint64_t>(size_t(W) * count);
-    unsigned long long* or_and = sc.alloc<unsigned long long>(2 * W);
+    unsigned long long* or_and = sc.alloc<unsigned long long>(2 * W + 1);  // + the non-finite flag
     if (!*soa || !or_and) return set_error(HCG_ENOMEM, "key buffers");
     HCG_TRY_CUDA(cudaMemsetAsync(or_and, 0, W * 8, sc.st));
     HCG_TRY_CUDA(cudaMemsetAsync(or_and + W, 0xFF, W * 8, sc.st));
+    HCG_TRY_CUDA(cudaMemsetAsync(or_and + 2 * W, 0, 8, sc.st));
     HCG_TRY(keygen_rows(rows, count, ix->pitch, ix->d_assign + ix->off[c], int(d), int(ix->m), int(ix->kind),
-                        ix->d_lut, *soa, int(W), or_and, ix->dmax, sc.st));
-    oa.assign(2 * W, 0);
-    HCG_TRY_CUDA(cudaMemcpyAsync(oa.data(), or_and, 2 * W * 8, cudaMemcpyDeviceToHost, sc.st));
+                        ix->d_lut, *soa, int(W), or_and, ix->dmax, int(ix->dtype),
+                        reinterpret_cast<unsigned*>(or_and + 2 * W), sc.st));
+    oa.assign(2 * W + 1, 0);
+    HCG_TRY_CUDA(cudaMemcpyAsync(oa.data(), or_and, (2 * W + 1) * 8, cudaMemcpyDeviceToHost, sc.st));
     HCG_TRY_CUDA(cudaStreamSynchronize(sc.st));
+    const bool bad = oa[2 * W] != 0;
+    oa.resize(2 * W);
+    if (bad) return set_error(HCG_ENONFINITE, "non-finite component");
     return HCG_OK;
 }
 
@@ -426,7 +435,9 @@ hcg_status new_index(const hcg_scheme* s, uint64_t n, uint64_t id_base, uint64_t
     auto* ix = new hcg_index;
     ix->device = device;
     ix->d_full = s->d_full;
-    ix->pitch = round16(s->d_full);
+    ix->dtype = s->dtype;
+    ix->row_bytes = s->d_full * (s->dtype == HCG_F32 ? 4 : 1);
+    ix->pitch = round16(ix->row_bytes);
     ix->C = s->curves;
     ix->m = s->bits_per_dim;
     ix->kind = s->curve_kind;
@@ -468,6 +479,14 @@ hcg_status new_index(const hcg_scheme* s, uint64_t n, uint64_t id_base, uint64_t
     return HCG_OK;
 }
 
+// +inf distances for empty f32 result lists.
+hcg_status fill_inf(double* p, size_t count, cudaStream_t st) {
+    if (!count) return HCG_OK;
+    const std::vector<double> h(count, HUGE_VAL);
+    HCG_TRY_CUDA(cudaMemcpyAsync(p, h.data(), count * 8, cudaMemcpyHostToDevice, st));
+    return cudaStreamSynchronize(st) == cudaSuccess ? HCG_OK : set_error(HCG_ECUDA, "fill");
+}
+
 hcg_status check_search_args(const hcg_index* ix, uint32_t k, uint32_t depth) {
     HCG_TRY(check_index(ix));
     if (k < 1) return set_error(HCG_EINVAL, "k must be >= 1");
@@ -476,9 +495,33 @@ hcg_status check_search_args(const hcg_index* ix, uint32_t k, uint32_t depth) {
     return HCG_OK;
 }
 
+// Non-finite query flag (f32 indexes): cleared before locate, checked by
+// check_queries() after it (the reference throws on NaN / Inf components).
+struct QueryFlag {
+    unsigned* dev = nullptr;
+};
+
+hcg_status make_flag(const hcg_index* ix, Scratch& sc, QueryFlag* f) {
+    if (ix->dtype != HCG_F32) return HCG_OK;
+    f->dev = sc.alloc<unsigned>(1);
+    if (!f->dev) return set_error(HCG_ENOMEM, "flag");
+    HCG_TRY_CUDA(cudaMemsetAsync(f->dev, 0, 4, sc.st));
+    return HCG_OK;
+}
+
+hcg_status check_flag(const QueryFlag& f, cudaStream_t st) {
+    if (!f.dev) return HCG_OK;
+    unsigned h = 0;
+    HCG_TRY_CUDA(cudaMemcpyAsync(&h, f.dev, 4, cudaMemcpyDeviceToHost, st));
+    HCG_TRY_CUDA(cudaStreamSynchronize(st));
+    return h ? set_error(HCG_ENONFINITE, "non-finite query component") : HCG_OK;
+}
+
 hcg_status locate(const hcg_index* ix, Scratch& sc, const uint8_t* dq, uint32_t nq, uint32_t depth,
-                  uint32_t* begins, uint64_t* ranks) {
+                  uint32_t* begins, uint64_t* ranks, const QueryFlag& flag) {
     LocateArgs a{};
+    a.dtype = int(ix->dtype);
+    a.bad = flag.dev;
     a.queries = dq;
     a.nq = nq;
     a.pitch = ix->pitch;
@@ -511,6 +554,7 @@ RefineArgs refine_args(const hcg_index* ix, const uint8_t* dq, uint32_t nq, uint
     a.id_base = ix->id_base;
     a.id_stride = ix->id_stride;
     a.n_rows = ix->n;
+    a.dtype = int(ix->dtype);
     return a;
 }
 
@@ -541,7 +585,7 @@ using namespace hcg;
 namespace {
 constexpr char kMagic[8] = {'H', 'C', 'G', 'I', 'D', 'X', 0, 1};
 constexpr char kTrailer[8] = {'H', 'C', 'G', 'E', 'N', 'D', 0, 0};
-constexpr uint32_t kFormatVersion = 1;
+constexpr uint32_t kFormatVersion = 2;  // 2: + descriptor dtype
 
 struct FileCloser {
     FILE* f = nullptr;
@@ -608,9 +652,9 @@ hcg_status hcg_build(const hcg_scheme* s, const uint8_t* rows, uint64_t n, uint6
     };
     hcg_status rc;
     if (n) {
-        if (ix->pitch != ix->d_full && cudaMemsetAsync(ix->rows, 0, size_t(n) * ix->pitch, st) != cudaSuccess)
+        if (ix->pitch != ix->row_bytes && cudaMemsetAsync(ix->rows, 0, size_t(n) * ix->pitch, st) != cudaSuccess)
             return fail(set_error(HCG_ECUDA, "memset rows"));
-        if (cudaMemcpy2DAsync(ix->rows, ix->pitch, rows, ix->d_full, ix->d_full, n, cudaMemcpyDefault, st) !=
+        if (cudaMemcpy2DAsync(ix->rows, ix->pitch, rows, ix->row_bytes, ix->row_bytes, n, cudaMemcpyDefault, st) !=
             cudaSuccess)
             return fail(set_error(HCG_ECUDA, std::string("copy rows: ") + cudaGetErrorString(cudaGetLastError())));
     }
@@ -630,6 +674,7 @@ uint64_t hcg_size(const hcg_index* ix) { return ix ? ix->n : 0; }
 uint32_t hcg_curves(const hcg_index* ix) { return ix ? ix->C : 0; }
 uint32_t hcg_key_words(const hcg_index* ix, uint32_t c) { return ix && c < ix->C ? ix->curves[c].w : 0; }
 uint64_t hcg_device_bytes(const hcg_index* ix) { return ix ? ix->bytes : 0; }
+uint32_t hcg_index_dtype(const hcg_index* ix) { return ix ? ix->dtype : 0; }
 
 hcg_status hcg_insert(hcg_index* ix, const uint8_t* rows, uint64_t nb, void* stream) {
     HCG_TRY(check_index(ix));
@@ -642,10 +687,27 @@ hcg_status hcg_insert(hcg_index* ix, const uint8_t* rows, uint64_t nb, void* str
     uint8_t* nr = nullptr;
     HCG_TRY(dev_alloc(&nr, size_t(n_new) * ix->pitch, &ix->bytes));
     if (n_old) HCG_TRY_CUDA(cudaMemcpyAsync(nr, ix->rows, size_t(n_old) * ix->pitch, cudaMemcpyDeviceToDevice, st));
-    if (ix->pitch != ix->d_full) HCG_TRY_CUDA(cudaMemsetAsync(nr + size_t(n_old) * ix->pitch, 0, size_t(nb) * ix->pitch, st));
-    HCG_TRY_CUDA(cudaMemcpy2DAsync(nr + size_t(n_old) * ix->pitch, ix->pitch, rows, ix->d_full, ix->d_full, nb,
+    if (ix->pitch != ix->row_bytes)
+        HCG_TRY_CUDA(cudaMemsetAsync(nr + size_t(n_old) * ix->pitch, 0, size_t(nb) * ix->pitch, st));
+    HCG_TRY_CUDA(cudaMemcpy2DAsync(nr + size_t(n_old) * ix->pitch, ix->pitch, rows, ix->row_bytes, ix->row_bytes, nb,
                                    cudaMemcpyDefault, st));
     HCG_TRY_CUDA(cudaStreamSynchronize(st));
+    if (ix->dtype == HCG_F32) {  // reject NaN / Inf before the index changes (curve.cpp:167)
+        Scratch sc(st);
+        unsigned* bad = sc.alloc<unsigned>(1);
+        unsigned h = 0;
+        hcg_status rc = bad ? HCG_OK : set_error(HCG_ENOMEM, "flag");
+        if (rc == HCG_OK && (cudaMemsetAsync(bad, 0, 4, st) != cudaSuccess)) rc = set_error(HCG_ECUDA, "memset");
+        if (rc == HCG_OK) launch_check_finite(nr + size_t(n_old) * ix->pitch, nb, ix->pitch, ix->d_full, bad, st);
+        if (rc == HCG_OK && (cudaMemcpyAsync(&h, bad, 4, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+                             cudaStreamSynchronize(st) != cudaSuccess))
+            rc = set_error(HCG_ECUDA, "finite check");
+        if (rc == HCG_OK && h) rc = set_error(HCG_ENONFINITE, "non-finite component");
+        if (rc != HCG_OK) {
+            dev_free(nr, size_t(n_new) * ix->pitch, &ix->bytes);
+            return rc;
+        }
+    }
     dev_free(ix->rows, size_t(std::max<uint64_t>(n_old, 1)) * ix->pitch, &ix->bytes);
     ix->rows = nr;
     ix->n = n_new;
@@ -662,9 +724,10 @@ hcg_status hcg_save(const hcg_index* ix, const char* path) {
     fc.f = std::fopen(path, "wb");
     if (!fc.f) return set_error(HCG_EIO, std::string("cannot open ") + path + " for writing");
     FILE* f = fc.f;
-    const uint32_t hdr[6] = {kFormatVersion, ix->d_full, ix->C, ix->m, ix->kind, uint32_t(ix->assign.size())};
+    const uint32_t hdr[7] = {kFormatVersion, ix->d_full, ix->C, ix->m, ix->kind, uint32_t(ix->assign.size()),
+                             ix->dtype};
     const uint64_t ids[3] = {ix->n, ix->id_base, ix->id_stride};
-    bool ok = put(f, kMagic, 8) && put(f, hdr, 6) && put(f, &ix->dist_scale, 1) && put(f, ids, 3) &&
+    bool ok = put(f, kMagic, 8) && put(f, hdr, 7) && put(f, &ix->dist_scale, 1) && put(f, ids, 3) &&
               put(f, ix->lut, 256) && put(f, ix->off.data(), ix->off.size()) &&
               put(f, ix->assign.data(), ix->assign.size());
     // rows, unpadded, in slices
@@ -672,8 +735,8 @@ hcg_status hcg_save(const hcg_index* ix, const char* path) {
     std::vector<uint8_t> buf;
     for (uint64_t r = 0; ok && r < ix->n; r += slice) {
         const uint64_t cnt = std::min(slice, ix->n - r);
-        buf.resize(cnt * ix->d_full);
-        HCG_TRY_CUDA(cudaMemcpy2D(buf.data(), ix->d_full, ix->rows + r * ix->pitch, ix->pitch, ix->d_full, cnt,
+        buf.resize(cnt * ix->row_bytes);
+        HCG_TRY_CUDA(cudaMemcpy2D(buf.data(), ix->row_bytes, ix->rows + r * ix->pitch, ix->pitch, ix->row_bytes, cnt,
                                   cudaMemcpyDeviceToHost));
         ok = put(f, buf.data(), buf.size());
     }
@@ -702,11 +765,11 @@ hcg_status hcg_load(const char* path, int device, void* stream, hcg_index** out)
     if (!fc.f) return set_error(HCG_EIO, std::string("cannot open ") + path);
     FILE* f = fc.f;
     char magic[8];
-    uint32_t hdr[6];
+    uint32_t hdr[7];
     double scale = 0;
     uint64_t ids[3];
     if (!get(f, magic, 8) || std::memcmp(magic, kMagic, 8) != 0) return set_error(HCG_EIO, std::string(path) + ": not an hcg index");
-    if (!get(f, hdr, 6) || hdr[0] != kFormatVersion) return set_error(HCG_EIO, std::string(path) + ": unsupported version");
+    if (!get(f, hdr, 7) || hdr[0] != kFormatVersion) return set_error(HCG_EIO, std::string(path) + ": unsupported version");
     if (!get(f, &scale, 1) || !get(f, ids, 3)) return set_error(HCG_EIO, std::string(path) + ": truncated header");
     hcg_scheme s{};
     s.d_full = hdr[1];
@@ -714,6 +777,7 @@ hcg_status hcg_load(const char* path, int device, void* stream, hcg_index** out)
     s.bits_per_dim = hdr[3];
     s.curve_kind = hdr[4];
     s.dist_scale = scale;
+    s.dtype = hdr[6];
     if (s.curves == 0 || s.curves > 4096 || hdr[5] > 1u << 20) return set_error(HCG_EIO, std::string(path) + ": corrupt header");
     std::vector<uint32_t> off(s.curves + 1), asg(hdr[5]);
     if (!get(f, s.cell_lut, 256) || !get(f, off.data(), off.size()) || !get(f, asg.data(), asg.size()))
@@ -736,9 +800,9 @@ hcg_status hcg_load(const char* path, int device, void* stream, hcg_index** out)
     std::vector<uint8_t> buf;
     for (uint64_t r = 0; r < ix->n; r += slice) {
         const uint64_t cnt = std::min(slice, ix->n - r);
-        buf.resize(cnt * ix->d_full);
+        buf.resize(cnt * ix->row_bytes);
         if (!get(f, buf.data(), buf.size())) return fail(set_error(HCG_EIO, std::string(path) + ": truncated rows"));
-        if (cudaMemcpy2D(ix->rows + r * ix->pitch, ix->pitch, buf.data(), ix->d_full, ix->d_full, cnt,
+        if (cudaMemcpy2D(ix->rows + r * ix->pitch, ix->pitch, buf.data(), ix->row_bytes, ix->row_bytes, cnt,
                          cudaMemcpyHostToDevice) != cudaSuccess)
             return fail(set_error(HCG_ECUDA, "upload rows"));
     }
@@ -780,12 +844,17 @@ hcg_status hcg_load(const char* path, int device, void* stream, hcg_index** out)
 
 static hcg_status search_impl(const hcg_index* ix, const uint8_t* queries, uint32_t nq, uint32_t k, uint32_t depth,
                               uint64_t* out_ids, uint32_t* out_sqdist, uint32_t* out_len, uint64_t* out_packed,
-                              void* stream, float* ms_out = nullptr) {
+                              void* stream, float* ms_out = nullptr, double* out_sq64 = nullptr) {
     HCG_TRY(check_search_args(ix, k, depth));
+    const bool f32 = ix->dtype == HCG_F32;
+    if (f32 != (out_sq64 != nullptr))  // packed / timed searches are u8-only
+        return set_error(HCG_EINVAL, f32 ? "index holds f32 descriptors: use hcg_search_f32"
+                                         : "index holds u8 descriptors: use hcg_search");
     if (nq == 0) return HCG_OK;
     if (!queries) return set_error(HCG_EINVAL, "null queries");
     const bool packed = out_packed != nullptr;
-    if (!packed && (!out_ids || !out_sqdist || !out_len)) return set_error(HCG_EINVAL, "null output");
+    if (!packed && (!out_ids || !(f32 ? static_cast<void*>(out_sq64) : out_sqdist) || !out_len))
+        return set_error(HCG_EINVAL, "null output");
     if (packed && ix->n && ix->id_base + (ix->n - 1) * ix->id_stride >= (1ull << 32))
         return set_error(HCG_ECAPACITY, "packed results need ids < 2^32");
     DeviceGuard g(ix->device);
@@ -793,12 +862,17 @@ static hcg_status search_impl(const hcg_index* ix, const uint8_t* queries, uint3
     Scratch sc(st);
     OutBuf<uint64_t> oi, op;
     OutBuf<uint32_t> os, ol;
+    OutBuf<double> o64;
+    QueryFlag flag;
     const size_t cnt = size_t(nq) * k;
     if (packed) {
         HCG_TRY(stage_out(sc, out_packed, cnt, &op));
     } else {
         HCG_TRY(stage_out(sc, out_ids, cnt, &oi));
-        HCG_TRY(stage_out(sc, out_sqdist, cnt, &os));
+        if (f32)
+            HCG_TRY(stage_out(sc, out_sq64, cnt, &o64));
+        else
+            HCG_TRY(stage_out(sc, out_sqdist, cnt, &os));
         HCG_TRY(stage_out(sc, out_len, nq, &ol));
     }
     if (ix->n == 0) {  // empty index: every list is empty
@@ -806,12 +880,16 @@ static hcg_status search_impl(const hcg_index* ix, const uint8_t* queries, uint3
             HCG_TRY_CUDA(cudaMemsetAsync(op.dev, 0xFF, cnt * 8, st));
         } else {
             HCG_TRY_CUDA(cudaMemsetAsync(oi.dev, 0xFF, cnt * 8, st));
-            HCG_TRY_CUDA(cudaMemsetAsync(os.dev, 0xFF, cnt * 4, st));
+            if (f32)
+                HCG_TRY(fill_inf(o64.dev, cnt, st));
+            else
+                HCG_TRY_CUDA(cudaMemsetAsync(os.dev, 0xFF, cnt * 4, st));
             HCG_TRY_CUDA(cudaMemsetAsync(ol.dev, 0, size_t(nq) * 4, st));
         }
     } else {
         const uint8_t* dq = nullptr;
-        HCG_TRY(stage_rows(sc, queries, nq, ix->d_full, ix->pitch, &dq));
+        HCG_TRY(stage_rows(sc, queries, nq, ix->row_bytes, ix->pitch, &dq));
+        HCG_TRY(make_flag(ix, sc, &flag));
         uint32_t* begins = sc.alloc<uint32_t>(size_t(nq) * ix->C);
         if (!begins) return set_error(HCG_ENOMEM, "window buffer");
         cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -819,7 +897,7 @@ static hcg_status search_impl(const hcg_index* ix, const uint8_t* queries, uint3
             for (auto& e : ev) HCG_TRY_CUDA(cudaEventCreate(&e));
             HCG_TRY_CUDA(cudaEventRecord(ev[0], st));
         }
-        HCG_TRY(locate(ix, sc, dq, nq, depth, begins, nullptr));
+        HCG_TRY(locate(ix, sc, dq, nq, depth, begins, nullptr, flag));
         if (ms_out) HCG_TRY_CUDA(cudaEventRecord(ev[1], st));
         RefineArgs a = refine_args(ix, dq, nq, depth, k, begins);
         if (ms_out) a.ev_mid = ev[2];
@@ -830,6 +908,7 @@ static hcg_status search_impl(const hcg_index* ix, const uint8_t* queries, uint3
             a.mode = kOutIds;
             a.out_ids = oi.dev;
             a.out_sqdist = os.dev;
+            a.out_sqdist_f64 = o64.dev;
             a.out_len = ol.dev;
         }
         HCG_TRY(run_refine(ix, sc, a));
@@ -851,15 +930,24 @@ static hcg_status search_impl(const hcg_index* ix, const uint8_t* queries, uint3
     }
     HCG_TRY(finish_out(sc, oi));
     HCG_TRY(finish_out(sc, os));
+    HCG_TRY(finish_out(sc, o64));
     HCG_TRY(finish_out(sc, ol));
     HCG_TRY(finish_out(sc, op));
-    if (oi.host || os.host || ol.host || op.host) HCG_TRY_CUDA(cudaStreamSynchronize(st));
+    HCG_TRY(check_flag(flag, st));
+    if (oi.host || os.host || o64.host || ol.host || op.host) HCG_TRY_CUDA(cudaStreamSynchronize(st));
     return HCG_OK;
 }
 
 hcg_status hcg_search(const hcg_index* ix, const uint8_t* queries, uint32_t nq, uint32_t k, uint32_t depth,
                       uint64_t* out_ids, uint32_t* out_sqdist, uint32_t* out_len, void* stream) {
     return search_impl(ix, queries, nq, k, depth, out_ids, out_sqdist, out_len, nullptr, stream);
+}
+
+hcg_status hcg_search_f32(const hcg_index* ix, const float* queries, uint32_t nq, uint32_t k, uint32_t depth,
+                          uint64_t* out_ids, double* out_sqdist, uint32_t* out_len, void* stream) {
+    if (!out_sqdist) return set_error(HCG_EINVAL, "null output");
+    return search_impl(ix, reinterpret_cast<const uint8_t*>(queries), nq, k, depth, out_ids, nullptr, out_len,
+                       nullptr, stream, nullptr, out_sqdist);
 }
 
 hcg_status hcg_search_timed(const hcg_index* ix, const uint8_t* queries, uint32_t nq, uint32_t k, uint32_t depth,
@@ -917,17 +1005,22 @@ hcg_status hcg_keys(const hcg_index* ix, const uint8_t* rows, uint64_t n, uint32
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     Scratch sc(st);
     const uint8_t* dr = nullptr;
-    HCG_TRY(stage_rows(sc, rows, n, ix->d_full, ix->pitch, &dr));
+    HCG_TRY(stage_rows(sc, rows, n, ix->row_bytes, ix->pitch, &dr));
     const uint32_t W = ix->curves[curve].w;
     uint64_t* soa = sc.alloc<uint64_t>(size_t(W) * n);
-    unsigned long long* oa = sc.alloc<unsigned long long>(2 * W);
+    unsigned long long* oa = sc.alloc<unsigned long long>(2 * W + 1);
     if (!soa || !oa) return set_error(HCG_ENOMEM, "key buffers");
+    HCG_TRY_CUDA(cudaMemsetAsync(oa + 2 * W, 0, 8, st));
     const uint32_t d = ix->off[curve + 1] - ix->off[curve];
     HCG_TRY(keygen_rows(dr, n, ix->pitch, ix->d_assign + ix->off[curve], int(d), int(ix->m), int(ix->kind),
-                        ix->d_lut, soa, int(W), oa, ix->dmax, st));
+                        ix->d_lut, soa, int(W), oa, ix->dmax, int(ix->dtype), reinterpret_cast<unsigned*>(oa + 2 * W),
+                        st));
     std::vector<uint64_t> h(size_t(W) * n), t(size_t(W) * n);
+    unsigned long long bad = 0;
     HCG_TRY_CUDA(cudaMemcpyAsync(h.data(), soa, h.size() * 8, cudaMemcpyDeviceToHost, st));
+    HCG_TRY_CUDA(cudaMemcpyAsync(&bad, oa + 2 * W, 8, cudaMemcpyDeviceToHost, st));
     HCG_TRY_CUDA(cudaStreamSynchronize(st));
+    if (bad) return set_error(HCG_ENONFINITE, "non-finite component");
     for (uint64_t i = 0; i < n; ++i)
         for (uint32_t w = 0; w < W; ++w) t[i * W + w] = h[uint64_t(w) * n + i];
     return deliver(out_words, t);
@@ -975,11 +1068,14 @@ hcg_status hcg_windows(const hcg_index* ix, const uint8_t* queries, uint32_t nq,
         cudaStream_t st = static_cast<cudaStream_t>(stream);
         Scratch sc(st);
         const uint8_t* dq = nullptr;
-        HCG_TRY(stage_rows(sc, queries, nq, ix->d_full, ix->pitch, &dq));
+        HCG_TRY(stage_rows(sc, queries, nq, ix->row_bytes, ix->pitch, &dq));
         uint32_t* begins = sc.alloc<uint32_t>(cnt);
         uint64_t* ranks = sc.alloc<uint64_t>(cnt);
         if (!begins || !ranks) return set_error(HCG_ENOMEM, "window buffers");
-        HCG_TRY(locate(ix, sc, dq, nq, depth, begins, ranks));
+        QueryFlag flag;
+        HCG_TRY(make_flag(ix, sc, &flag));
+        HCG_TRY(locate(ix, sc, dq, nq, depth, begins, ranks, flag));
+        HCG_TRY(check_flag(flag, st));
         std::vector<uint32_t> hb(cnt);
         HCG_TRY_CUDA(cudaMemcpyAsync(hb.data(), begins, cnt * 4, cudaMemcpyDeviceToHost, st));
         HCG_TRY_CUDA(cudaMemcpyAsync(r.data(), ranks, cnt * 8, cudaMemcpyDeviceToHost, st));
@@ -1011,10 +1107,13 @@ hcg_status hcg_candidates(const hcg_index* ix, const uint8_t* queries, uint32_t 
         HCG_TRY_CUDA(cudaMemsetAsync(oc.dev, 0, size_t(nq) * 4, st));
     } else {
         const uint8_t* dq = nullptr;
-        HCG_TRY(stage_rows(sc, queries, nq, ix->d_full, ix->pitch, &dq));
+        HCG_TRY(stage_rows(sc, queries, nq, ix->row_bytes, ix->pitch, &dq));
         uint32_t* begins = sc.alloc<uint32_t>(size_t(nq) * ix->C);
         if (!begins) return set_error(HCG_ENOMEM, "window buffer");
-        HCG_TRY(locate(ix, sc, dq, nq, depth, begins, nullptr));
+        QueryFlag flag;
+        HCG_TRY(make_flag(ix, sc, &flag));
+        HCG_TRY(locate(ix, sc, dq, nq, depth, begins, nullptr, flag));
+        HCG_TRY(check_flag(flag, st));
         RefineArgs a = refine_args(ix, dq, nq, depth, 1, begins);
         a.mode = kOutCandidates;
         a.out_ids = oi.dev;
@@ -1034,39 +1133,65 @@ hcg_status hcg_candidates(const hcg_index* ix, const uint8_t* queries, uint32_t 
     return HCG_OK;
 }
 
-hcg_status hcg_brute_force(const hcg_index* ix, const uint8_t* queries, uint32_t nq, uint32_t k, uint64_t* out_ids,
-                           uint32_t* out_sqdist, uint32_t* out_len, void* stream) {
+static hcg_status brute_impl(const hcg_index* ix, const uint8_t* queries, uint32_t nq, uint32_t k, uint64_t* out_ids,
+                             uint32_t* out_sqdist, double* out_sq64, uint32_t* out_len, void* stream) {
     HCG_TRY(check_search_args(ix, k, 1));
+    const bool f32 = ix->dtype == HCG_F32;
+    if (f32 != (out_sq64 != nullptr))
+        return set_error(HCG_EINVAL, f32 ? "index holds f32 descriptors: use hcg_brute_force_f32"
+                                         : "index holds u8 descriptors: use hcg_brute_force");
     if (nq == 0) return HCG_OK;
-    if (!queries || !out_ids || !out_sqdist || !out_len) return set_error(HCG_EINVAL, "null buffer");
-    if (ix->n && ix->id_base + (ix->n - 1) * ix->id_stride >= (1ull << 32))
+    if (!queries || !out_ids || !(f32 ? static_cast<void*>(out_sq64) : out_sqdist) || !out_len)
+        return set_error(HCG_EINVAL, "null buffer");
+    if (!f32 && ix->n && ix->id_base + (ix->n - 1) * ix->id_stride >= (1ull << 32))
         return set_error(HCG_ECAPACITY, "brute force needs ids < 2^32");
     DeviceGuard g(ix->device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     Scratch sc(st);
     OutBuf<uint64_t> oi;
     OutBuf<uint32_t> os, ol;
+    OutBuf<double> o64;
     const size_t cnt = size_t(nq) * k;
     HCG_TRY(stage_out(sc, out_ids, cnt, &oi));
-    HCG_TRY(stage_out(sc, out_sqdist, cnt, &os));
+    if (f32)
+        HCG_TRY(stage_out(sc, out_sq64, cnt, &o64));
+    else
+        HCG_TRY(stage_out(sc, out_sqdist, cnt, &os));
     HCG_TRY(stage_out(sc, out_len, nq, &ol));
     if (ix->n == 0) {
         HCG_TRY_CUDA(cudaMemsetAsync(oi.dev, 0xFF, cnt * 8, st));
-        HCG_TRY_CUDA(cudaMemsetAsync(os.dev, 0xFF, cnt * 4, st));
+        if (f32)
+            HCG_TRY(fill_inf(o64.dev, cnt, st));
+        else
+            HCG_TRY_CUDA(cudaMemsetAsync(os.dev, 0xFF, cnt * 4, st));
         HCG_TRY_CUDA(cudaMemsetAsync(ol.dev, 0, size_t(nq) * 4, st));
     } else {
         const uint8_t* dq = nullptr;
-        HCG_TRY(stage_rows(sc, queries, nq, ix->d_full, ix->pitch, &dq));
-        BruteArgs a{ix->rows, ix->n, ix->pitch, dq, nq, k, ix->id_base, ix->id_stride};
-        uint64_t* part = sc.alloc<uint64_t>(brute_scratch_bytes(a) / 8);
+        HCG_TRY(stage_rows(sc, queries, nq, ix->row_bytes, ix->pitch, &dq));
+        BruteArgs a{ix->rows, ix->n, ix->pitch, dq, nq, k, ix->id_base, ix->id_stride, int(ix->dtype)};
+        uint64_t* part = sc.alloc<uint64_t>((brute_scratch_bytes(a) + 7) / 8);
         if (!part) return set_error(HCG_ENOMEM, "brute-force scratch");
-        HCG_TRY(launch_brute(a, part, oi.dev, os.dev, ol.dev, st));
+        HCG_TRY(launch_brute(a, part, oi.dev, os.dev, ol.dev, o64.dev, st));
     }
     HCG_TRY(finish_out(sc, oi));
     HCG_TRY(finish_out(sc, os));
+    HCG_TRY(finish_out(sc, o64));
     HCG_TRY(finish_out(sc, ol));
-    if (oi.host || os.host || ol.host) HCG_TRY_CUDA(cudaStreamSynchronize(st));
+    if (oi.host || os.host || o64.host || ol.host) HCG_TRY_CUDA(cudaStreamSynchronize(st));
     return HCG_OK;
+}
+
+hcg_status hcg_brute_force(const hcg_index* ix, const uint8_t* queries, uint32_t nq, uint32_t k, uint64_t* out_ids,
+                           uint32_t* out_sqdist, uint32_t* out_len, void* stream) {
+    if (!out_sqdist && nq) return set_error(HCG_EINVAL, "null buffer");
+    return brute_impl(ix, queries, nq, k, out_ids, out_sqdist, nullptr, out_len, stream);
+}
+
+hcg_status hcg_brute_force_f32(const hcg_index* ix, const float* queries, uint32_t nq, uint32_t k, uint64_t* out_ids,
+                               double* out_sqdist, uint32_t* out_len, void* stream) {
+    if (!out_sqdist && nq) return set_error(HCG_EINVAL, "null buffer");
+    return brute_impl(ix, reinterpret_cast<const uint8_t*>(queries), nq, k, out_ids, nullptr, out_sqdist, out_len,
+                      stream);
 }
 
 hcg_status hcg_gen_rows(uint64_t first, uint64_t stride, uint64_t count, uint8_t* out_dev, int device, void* stream) {

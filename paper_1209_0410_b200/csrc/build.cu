@@ -26,12 +26,12 @@ struct KeyWords {
 
 // One thread per row: key of curve c (full width, SoA words) plus an OR/AND
 // reduction over all keys that later yields the common prefix.
-template <int DMAX>
+template <int DMAX, class T>
 __global__ void __launch_bounds__(256) k_keygen(const uint8_t* __restrict__ rows, uint64_t n,
                                                 uint32_t pitch, const uint16_t* __restrict__ assign_c,
                                                 int d, int m, int kind, const uint32_t* __restrict__ lut_g,
                                                 uint64_t* __restrict__ keys_soa, int W,
-                                                unsigned long long* __restrict__ or_and) {
+                                                unsigned long long* __restrict__ or_and, unsigned* bad) {
     constexpr int WMAX = KeyWords<DMAX>::value;
     __shared__ uint32_t lut[256];
     __shared__ uint16_t asg[DMAX];
@@ -47,9 +47,9 @@ __global__ void __launch_bounds__(256) k_keygen(const uint8_t* __restrict__ rows
     uint64_t key[WMAX];
     if (valid) {
         uint32_t x[DMAX];
-        const uint8_t* row = rows + i * pitch;
+        const T* row = reinterpret_cast<const T*>(rows + i * pitch);
 #pragma unroll
-        for (int s = 0; s < DMAX; ++s) x[s] = s < d ? lut[__ldg(row + asg[s])] : 0u;
+        for (int s = 0; s < DMAX; ++s) x[s] = s < d ? cell_of(__ldg(row + asg[s]), lut, m, bad) : 0u;
         make_key<DMAX, WMAX>(x, d, m, kind, key);
 #pragma unroll
         for (int w = 0; w < WMAX; ++w)
@@ -247,6 +247,16 @@ __global__ void __launch_bounds__(kSortThreads) k_downsweep(
     }
 }
 
+// Raise *bad if any of the n x d floats (row pitch `pitch` bytes) is NaN / Inf.
+__global__ void k_check_finite(const uint8_t* __restrict__ rows, uint64_t n, uint32_t pitch, uint32_t d,
+                               unsigned* bad) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n * d) return;
+    const uint64_t r = i / d, j = i - r * d;
+    const uint32_t b = reinterpret_cast<const uint32_t*>(rows + r * pitch)[j];
+    if ((b & 0x7F800000u) == 0x7F800000u) *bad = 1u;
+}
+
 __global__ void k_iota(uint32_t* v, uint64_t n, uint32_t base) {
     const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i < n) v[i] = base + uint32_t(i);
@@ -328,22 +338,26 @@ inline unsigned blocks_for(uint64_t n, unsigned t) { return unsigned((n + t - 1)
 template <int DMAX>
 void launch_keygen(const uint8_t* rows, uint64_t n, uint32_t pitch, const uint16_t* assign_c, int d, int m,
                    int kind, const uint32_t* lut, uint64_t* keys_soa, int W, unsigned long long* or_and,
-                   cudaStream_t st) {
-    k_keygen<DMAX><<<blocks_for(n, 256), 256, 0, st>>>(rows, n, pitch, assign_c, d, m, kind, lut, keys_soa, W,
-                                                      or_and);
+                   int dtype, unsigned* bad, cudaStream_t st) {
+    if (dtype == HCG_F32)
+        k_keygen<DMAX, float><<<blocks_for(n, 256), 256, 0, st>>>(rows, n, pitch, assign_c, d, m, kind, lut,
+                                                                  keys_soa, W, or_and, bad);
+    else
+        k_keygen<DMAX, uint8_t><<<blocks_for(n, 256), 256, 0, st>>>(rows, n, pitch, assign_c, d, m, kind, lut,
+                                                                    keys_soa, W, or_and, bad);
 }
 }  // namespace
 
 hcg_status keygen_rows(const uint8_t* rows, uint64_t n, uint32_t pitch, const uint16_t* assign_c, int d, int m,
                        int kind, const uint32_t* lut, uint64_t* keys_soa, int W, unsigned long long* or_and,
-                       int dmax, cudaStream_t st) {
+                       int dmax, int dtype, unsigned* bad, cudaStream_t st) {
     if (n == 0) return HCG_OK;
     switch (dmax) {
-        case 8: launch_keygen<8>(rows, n, pitch, assign_c, d, m, kind, lut, keys_soa, W, or_and, st); break;
-        case 16: launch_keygen<16>(rows, n, pitch, assign_c, d, m, kind, lut, keys_soa, W, or_and, st); break;
-        case 32: launch_keygen<32>(rows, n, pitch, assign_c, d, m, kind, lut, keys_soa, W, or_and, st); break;
-        case 64: launch_keygen<64>(rows, n, pitch, assign_c, d, m, kind, lut, keys_soa, W, or_and, st); break;
-        case 128: launch_keygen<128>(rows, n, pitch, assign_c, d, m, kind, lut, keys_soa, W, or_and, st); break;
+        case 8: launch_keygen<8>(rows, n, pitch, assign_c, d, m, kind, lut, keys_soa, W, or_and, dtype, bad, st); break;
+        case 16: launch_keygen<16>(rows, n, pitch, assign_c, d, m, kind, lut, keys_soa, W, or_and, dtype, bad, st); break;
+        case 32: launch_keygen<32>(rows, n, pitch, assign_c, d, m, kind, lut, keys_soa, W, or_and, dtype, bad, st); break;
+        case 64: launch_keygen<64>(rows, n, pitch, assign_c, d, m, kind, lut, keys_soa, W, or_and, dtype, bad, st); break;
+        case 128: launch_keygen<128>(rows, n, pitch, assign_c, d, m, kind, lut, keys_soa, W, or_and, dtype, bad, st); break;
         default: return set_error(HCG_EINVAL, "unsupported curve dimension bucket");
     }
     return check_launch("k_keygen");
@@ -371,6 +385,11 @@ hcg_status radix_sort_pairs(uint64_t** k, uint32_t** v, uint64_t** k_alt, uint32
 size_t radix_counts_bytes(uint64_t n) {
     const uint64_t tiles = (n + kSortTile - 1) / kSortTile;
     return size_t(tiles) * 256 * 4 + 256 * 4;
+}
+
+void launch_check_finite(const uint8_t* rows, uint64_t n, uint32_t pitch, uint32_t d, unsigned* bad,
+                         cudaStream_t st) {
+    if (n) k_check_finite<<<blocks_for(n * d, 256), 256, 0, st>>>(rows, n, pitch, d, bad);
 }
 
 void launch_iota(uint32_t* v, uint64_t n, uint32_t base, cudaStream_t st) {

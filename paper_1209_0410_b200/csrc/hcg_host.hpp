@@ -18,10 +18,12 @@ hcg_status check_launch(const char* what);
 // build.cu
 hcg_status keygen_rows(const uint8_t* rows, uint64_t n, uint32_t pitch, const uint16_t* assign_c, int d, int m,
                        int kind, const uint32_t* lut, uint64_t* keys_soa, int W, unsigned long long* or_and,
-                       int dmax, cudaStream_t st);
+                       int dmax, int dtype, unsigned* bad, cudaStream_t st);
 hcg_status radix_sort_pairs(uint64_t** k, uint32_t** v, uint64_t** k_alt, uint32_t** v_alt, uint64_t n,
                             uint32_t digit_mask, uint32_t* counts, uint32_t* totals, cudaStream_t st);
 size_t radix_counts_bytes(uint64_t n);
+void launch_check_finite(const uint8_t* rows, uint64_t n, uint32_t pitch, uint32_t d, unsigned* bad,
+                         cudaStream_t st);
 void launch_iota(uint32_t* v, uint64_t n, uint32_t base, cudaStream_t st);
 void launch_offset(const uint32_t* in, uint32_t* out, uint64_t n, uint32_t base, cudaStream_t st);
 void launch_rank_merge(const uint64_t* ak, const uint32_t* as, uint64_t na, const uint64_t* bk, const uint32_t* bs,
@@ -46,6 +48,8 @@ struct LocateArgs {
     uint32_t depth;
     uint32_t* out_begin;  // nq x C
     uint64_t* out_rank;   // nq x C or null
+    int dtype;            // hcg_dtype of the queries
+    unsigned* bad;        // raised when a query component is non-finite (f32)
 };
 hcg_status launch_locate(const LocateArgs& a, int dmax, int wsmax, cudaStream_t st);
 
@@ -71,6 +75,8 @@ struct RefineArgs {
     unsigned long long* prof;  // unused (kept zero)
     cudaEvent_t ev_mid;        // optional: recorded between the union and gather launches
     uint64_t n_rows;           // rows in the index (bounds checks)
+    int dtype;                 // hcg_dtype of rows and queries
+    double* out_sqdist_f64;    // HCG_F32 + kOutIds: nq x k squared distances
 };
 // Scratch bytes the refine launch needs (global hash tables when the table
 // does not fit in shared memory); query with scratch == nullptr first.
@@ -88,10 +94,11 @@ struct BruteArgs {
     uint32_t nq;
     uint32_t k;
     uint64_t id_base, id_stride;
+    int dtype;
 };
 size_t brute_scratch_bytes(const BruteArgs& a);
 hcg_status launch_brute(const BruteArgs& a, uint64_t* scratch, uint64_t* out_ids, uint32_t* out_sqdist,
-                        uint32_t* out_len, cudaStream_t st);
+                        uint32_t* out_len, double* out_sqdist_f64, cudaStream_t st);
 
 // datagen.cu
 hcg_status gen_rows(uint64_t first, uint64_t stride, uint64_t count, uint8_t* out, cudaStream_t st);

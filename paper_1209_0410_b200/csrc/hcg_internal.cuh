@@ -129,6 +129,18 @@ __device__ __forceinline__ void make_key(uint32_t (&x)[DMAX], int d, int m, int 
     }
 }
 
+// Quantized cell of one descriptor component (curve.cpp:166-174):
+//  u8 : the view's 256-entry table (built on the host by the same rule);
+//  f32: float_to_ordinal(x) >> (32 - m) on the device; a NaN / Inf component
+//       raises *bad (the reference throws "non-finite component").
+__device__ __forceinline__ uint32_t cell_of(uint8_t v, const uint32_t* lut, int, unsigned*) { return lut[v]; }
+__device__ __forceinline__ uint32_t cell_of(float v, const uint32_t*, int m, unsigned* bad) {
+    const uint32_t b = __float_as_uint(v);
+    if ((b & 0x7F800000u) == 0x7F800000u) *bad = 1u;
+    const uint32_t ord = (b >> 31) ? ~b : (b | 0x80000000u);
+    return ord >> (32 - m);
+}
+
 // ------------------------------------------------------------ distance ----
 // Squared L2 of 16 bytes, exact in u32: |a-b| per byte then a byte dot product.
 __device__ __forceinline__ uint32_t sad2_16(const uint4& a, const uint4& b, uint32_t acc) {
@@ -137,6 +149,17 @@ __device__ __forceinline__ uint32_t sad2_16(const uint4& a, const uint4& b, uint
     d = __vabsdiffu4(a.y, b.y); acc = __dp4a(d, d, acc);
     d = __vabsdiffu4(a.z, b.z); acc = __dp4a(d, d, acc);
     d = __vabsdiffu4(a.w, b.w); acc = __dp4a(d, d, acc);
+    return acc;
+}
+
+// Squared L2 of 4 floats accumulated in double: the reference's terms
+// (double(a) - double(b))^2 (vecio.cpp:87-95), tree-summed.
+__device__ __forceinline__ double sq4_f64(const uint4& a, const uint4& b, double acc) {
+    double d;
+    d = double(__uint_as_float(a.x)) - double(__uint_as_float(b.x)); acc = fma(d, d, acc);
+    d = double(__uint_as_float(a.y)) - double(__uint_as_float(b.y)); acc = fma(d, d, acc);
+    d = double(__uint_as_float(a.z)) - double(__uint_as_float(b.z)); acc = fma(d, d, acc);
+    d = double(__uint_as_float(a.w)) - double(__uint_as_float(b.w)); acc = fma(d, d, acc);
     return acc;
 }
 
@@ -195,6 +218,74 @@ struct WarpTopK {
             insert(x, lane);
             m &= ~(1u << src);
             m &= __ballot_sync(kFull, cand < thr);
+        }
+    }
+};
+
+// Warp top-k over (u64 key, u32 slot) pairs for f32 indexes: key = the bits of
+// the non-negative double squared distance (order preserving), ties by slot
+// (= id order).  Same blocked layout and insertion as WarpTopK.
+template <int R>
+struct WarpTopK2 {
+    uint64_t a[R];
+    uint32_t b[R];
+    uint64_t ta;
+    uint32_t tb;
+    int thr_lane, thr_reg;
+
+    __device__ static __forceinline__ bool lt(uint64_t xa, uint32_t xb, uint64_t ya, uint32_t yb) {
+        return xa < ya || (xa == ya && xb < yb);
+    }
+
+    __device__ __forceinline__ void init(int k) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            a[r] = kNone;
+            b[r] = 0xFFFFFFFFu;
+        }
+        ta = kNone;
+        tb = 0xFFFFFFFFu;
+        thr_lane = (k - 1) / R;
+        thr_reg = (k - 1) % R;
+    }
+
+    __device__ __forceinline__ void insert(uint64_t xa, uint32_t xb, int lane) {
+        const uint64_t pa = __shfl_up_sync(kFull, a[R - 1], 1);
+        const uint32_t pb = __shfl_up_sync(kFull, b[R - 1], 1);
+        const bool first_lt = lane == 0 || lt(pa, pb, xa, xb);
+#pragma unroll
+        for (int r = R - 1; r >= 0; --r) {
+            const uint64_t qa = r == 0 ? pa : a[r - 1];
+            const uint32_t qb = r == 0 ? pb : b[r - 1];
+            const bool q_lt = r == 0 ? first_lt : lt(a[r - 1], b[r - 1], xa, xb);
+            if (!q_lt) {
+                a[r] = qa;
+                b[r] = qb;
+            } else if (lt(xa, xb, a[r], b[r])) {
+                a[r] = xa;
+                b[r] = xb;
+            }
+        }
+        uint64_t ma = 0;
+        uint32_t mb = 0;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            ma |= a[r] & (0ull - uint64_t(r == thr_reg));
+            mb |= b[r] & (0u - uint32_t(r == thr_reg));
+        }
+        ta = __shfl_sync(kFull, ma, thr_lane);
+        tb = __shfl_sync(kFull, mb, thr_lane);
+    }
+
+    __device__ __forceinline__ void offer(uint64_t ca, uint32_t cb, int lane) {
+        unsigned m = __ballot_sync(kFull, lt(ca, cb, ta, tb));
+        while (m) {
+            const int src = __ffs(m) - 1;
+            const uint64_t xa = __shfl_sync(kFull, ca, src);
+            const uint32_t xb = __shfl_sync(kFull, cb, src);
+            insert(xa, xb, lane);
+            m &= ~(1u << src);
+            m &= __ballot_sync(kFull, lt(ca, cb, ta, tb));
         }
     }
 };

@@ -3,9 +3,10 @@
 // little-endian u32 dimension followed by `dim` payload entries (u8 for
 // bvecs, f32 for fvecs); the dimension is constant across records.
 //
-// Rows are exchanged with the library as bytes.  fvecs components must be
-// byte values of the index view (offset + b * scale), the representation the
-// GPU path stores; bvecs bytes are the reference's widened floats as-is.
+// HCG_BVECS / HCG_FVECS exchange u8 rows: fvecs components must be byte
+// values of the index view (offset + b * scale), bvecs bytes are the
+// reference's widened floats as-is.  HCG_FVECS_F32 exchanges the float
+// components themselves (rows = n x dim floats) for HCG_F32 indexes.
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -36,7 +37,8 @@ hcg_status hcg_read_vectors(const char* path, uint32_t format, float offset, flo
                             uint64_t* n_out, uint32_t* dim_out) {
     using hcg::set_error;
     if (!path || !rows_out || !n_out || !dim_out) return set_error(HCG_EINVAL, "null argument");
-    if (format > HCG_BVECS) return set_error(HCG_EINVAL, "unknown vector format");
+    if (format > HCG_FVECS_F32) return set_error(HCG_EINVAL, "unknown vector format");
+    const size_t esize = format == HCG_FVECS_F32 ? 4 : 1;
     *rows_out = nullptr;
     *n_out = 0;
     *dim_out = 0;
@@ -60,8 +62,17 @@ hcg_status hcg_read_vectors(const char* path, uint32_t format, float offset, flo
                                           " vs " + std::to_string(dim) + ")");
         }
         const size_t at = rows.size();
-        rows.resize(at + dim);
-        if (format == HCG_BVECS) {
+        rows.resize(at + size_t(dim) * esize);
+        if (format == HCG_FVECS_F32) {
+            float* dst = reinterpret_cast<float*>(rows.data() + at);  // vector<uint8_t> storage: memcpy-safe
+            fbuf.resize(dim);
+            if (std::fread(fbuf.data(), 4, dim, fh.f) != dim)
+                return set_error(HCG_EIO, std::string(path) + ": truncated fvecs payload");
+            for (uint32_t j = 0; j < dim; ++j)
+                if (!std::isfinite(fbuf[j]))
+                    return set_error(HCG_EIO, std::string(path) + ": non-finite component in record " + std::to_string(n));
+            std::memcpy(dst, fbuf.data(), size_t(dim) * 4);
+        } else if (format == HCG_BVECS) {
             if (std::fread(rows.data() + at, 1, dim, fh.f) != dim)
                 return set_error(HCG_EIO, std::string(path) + ": truncated bvecs payload");
         } else {
@@ -94,7 +105,7 @@ hcg_status hcg_write_vectors(const char* path, uint32_t format, float offset, fl
                              uint64_t n, uint32_t dim) {
     using hcg::set_error;
     if (!path || (n && !rows)) return set_error(HCG_EINVAL, "null argument");
-    if (format > HCG_BVECS) return set_error(HCG_EINVAL, "unknown vector format");
+    if (format > HCG_FVECS_F32) return set_error(HCG_EINVAL, "unknown vector format");
     if (n && dim == 0) return set_error(HCG_EINVAL, "zero dimension");
     File fh;
     fh.f = std::fopen(path, "wb");
@@ -102,7 +113,9 @@ hcg_status hcg_write_vectors(const char* path, uint32_t format, float offset, fl
     std::vector<float> fbuf(dim);
     for (uint64_t i = 0; i < n; ++i) {
         bool ok = std::fwrite(&dim, 4, 1, fh.f) == 1;
-        if (format == HCG_BVECS) {
+        if (format == HCG_FVECS_F32) {
+            ok = ok && std::fwrite(rows + i * dim * 4, 4, dim, fh.f) == dim;
+        } else if (format == HCG_BVECS) {
             ok = ok && std::fwrite(rows + i * dim, 1, dim, fh.f) == dim;
         } else {
             for (uint32_t j = 0; j < dim; ++j) fbuf[j] = offset + float(rows[i * dim + j]) * scale;

@@ -59,7 +59,7 @@ __device__ __forceinline__ int suffix_cmp(const uint64_t* e, const uint64_t (&qs
 // COOP: one WARP per (query, curve) and a 32-ary lower_bound (each round the
 // lanes probe 32 splitters and a ballot narrows the range 33x: ~5 dependent
 // loads at 10M instead of 24) -- the small-batch latency path.
-template <int DMAX, int WSMAX, bool COOP, int MINB = 1>
+template <int DMAX, int WSMAX, bool COOP, int MINB, class T>
 __global__ void __launch_bounds__(128, MINB) k_locate(LocateArgs a) {
     constexpr int WMAX = DMAX / 2 > kMaxKeyWords ? kMaxKeyWords : (DMAX / 2 < 1 ? 1 : DMAX / 2);
     __shared__ uint32_t lut[256];
@@ -73,10 +73,10 @@ __global__ void __launch_bounds__(128, MINB) k_locate(LocateArgs a) {
     const int d = int(cv.dims);
 
     uint32_t x[DMAX];
-    const uint8_t* row = a.queries + uint64_t(q) * a.pitch;
+    const T* row = reinterpret_cast<const T*>(a.queries + uint64_t(q) * a.pitch);
     const uint16_t* asg = a.assign + cv.off;
 #pragma unroll
-    for (int s = 0; s < DMAX; ++s) x[s] = s < d ? lut[__ldg(row + __ldg(asg + s))] : 0u;
+    for (int s = 0; s < DMAX; ++s) x[s] = s < d ? cell_of(__ldg(row + __ldg(asg + s)), lut, a.m, a.bad) : 0u;
     uint64_t key[WMAX];
     make_key<DMAX, WMAX>(x, d, a.m, a.kind, key);
 
@@ -146,13 +146,21 @@ __global__ void __launch_bounds__(128, MINB) k_locate(LocateArgs a) {
     }
 }
 
-template <int DMAX, int WSMAX>
-static void locate_launch(const LocateArgs& a, cudaStream_t st) {
+template <int DMAX, int WSMAX, class T>
+static void locate_launch_t(const LocateArgs& a, cudaStream_t st) {
     const uint64_t total = uint64_t(a.nq) * a.C;
     if (total <= 1024)  // small batches: a warp per (query, curve), ~5 dependent loads
-        k_locate<DMAX, WSMAX, true><<<unsigned((total * 32 + 127) / 128), 128, 0, st>>>(a);
+        k_locate<DMAX, WSMAX, true, 1, T><<<unsigned((total * 32 + 127) / 128), 128, 0, st>>>(a);
     else  // 8 CTAs/SM: measured 3 % faster than the 88-register default
-        k_locate<DMAX, WSMAX, false, (DMAX <= 16 ? 8 : 1)><<<unsigned((total + 127) / 128), 128, 0, st>>>(a);
+        k_locate<DMAX, WSMAX, false, (DMAX <= 16 ? 8 : 1), T><<<unsigned((total + 127) / 128), 128, 0, st>>>(a);
+}
+
+template <int DMAX, int WSMAX>
+static void locate_launch(const LocateArgs& a, cudaStream_t st) {
+    if (a.dtype == HCG_F32)
+        locate_launch_t<DMAX, WSMAX, float>(a, st);
+    else
+        locate_launch_t<DMAX, WSMAX, uint8_t>(a, st);
 }
 
 template <int DMAX>
@@ -510,6 +518,158 @@ __global__ void __launch_bounds__(NW * 32) k_gather_cta(RefineArgs a, const uint
     }
 }
 
+// ------------------------------------------------------- K3c, f32 rows ----
+// Float descriptors (the reference's native component type): a row is up to
+// 512 B = 32 16-B chunks, so the whole WARP reads one row per load (lane =
+// chunk, 4 full 128-B lines) and keeps 8 rows in flight.  Per-lane partials
+// are double ((double(a) - double(b))^2, vecio.cpp:87-95); a reduce-scatter
+// over lane bits 4,3,2 and an all-reduce over bits 1,0 leave row
+// 4*b4 + 2*b3 + b2 in lane group (lane >> 2), whose lane 0 offers
+// (double bits, slot) to the pair top-k.  The summation is a fixed tree:
+// distances agree with the reference's sequential sum to ~1e-15 relative and
+// identical rows get identical distances.
+template <bool DIRECT>
+__device__ __forceinline__ uint32_t f32_entry(const uint32_t* list, uint32_t e, uint32_t n) {
+    if (DIRECT) return e < n ? e : kEmpty;
+    return e < n ? __ldcg(list + e) : kEmpty;
+}
+
+// Scores entries [start, start + 8), [start + step, ...) of a list (DIRECT:
+// the entries are the row slots themselves, i.e. rows [start, n)).
+template <int R, bool DIRECT>
+__device__ __forceinline__ void gather_list_f32(const uint8_t* rows, uint32_t pitch, const uint32_t* list, uint32_t n,
+                                                uint32_t start, uint32_t step, const uint4& qv, int lane,
+                                                WarpTopK2<R>& tk) {
+    const uint32_t chunks = pitch >> 4;
+    const bool has = uint32_t(lane) < chunks;
+    uint32_t cur = lane < 8 ? f32_entry<DIRECT>(list, start + lane, n) : kEmpty;
+    for (uint32_t base = start; base < n; base += step) {
+        uint32_t nx[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) nx[r] = __shfl_sync(kFull, cur, r);
+        uint4 v[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+            v[r] = (nx[r] != kEmpty && has) ? ldg_stream(rows + uint64_t(nx[r]) * pitch + uint32_t(lane) * 16)
+                                            : make_uint4(0, 0, 0, 0);
+        cur = lane < 8 ? f32_entry<DIRECT>(list, base + step + lane, n) : kEmpty;
+        double acc[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) acc[r] = sq4_f64(v[r], qv, 0.0);
+        const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+        double s4[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const double send = b4 ? acc[i] : acc[i + 4];
+            const double keep = b4 ? acc[i + 4] : acc[i];
+            s4[i] = keep + __shfl_xor_sync(kFull, send, 16);
+        }
+        double s2[2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const double send = b3 ? s4[i] : s4[i + 2];
+            const double keep = b3 ? s4[i + 2] : s4[i];
+            s2[i] = keep + __shfl_xor_sync(kFull, send, 8);
+        }
+        double S = (b2 ? s2[1] : s2[0]) + __shfl_xor_sync(kFull, b2 ? s2[0] : s2[1], 4);
+        S += __shfl_xor_sync(kFull, S, 2);
+        S += __shfl_xor_sync(kFull, S, 1);
+        const int row = (b4 ? 4 : 0) + (b3 ? 2 : 0) + (b2 ? 1 : 0);
+        uint32_t me = nx[0];
+#pragma unroll
+        for (int r = 1; r < 8; ++r)
+            if (r == row) me = nx[r];
+        const bool offer = (lane & 3) == 0 && me != kEmpty;
+        tk.offer(offer ? uint64_t(__double_as_longlong(S)) : kNone, offer ? me : 0xFFFFFFFFu, lane);
+    }
+}
+
+__device__ __forceinline__ uint4 load_query_f32(const uint8_t* queries, uint32_t pitch, uint32_t q, int lane) {
+    return uint32_t(lane) < (pitch >> 4) ? *reinterpret_cast<const uint4*>(queries + uint64_t(q) * pitch + lane * 16)
+                                         : make_uint4(0, 0, 0, 0);
+}
+
+template <int R>
+__device__ __forceinline__ void write_result_f32(const RefineArgs& a, uint32_t q, const WarpTopK2<R>& fin, int lane,
+                                                 uint32_t U) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const uint32_t e = uint32_t(lane) * R + r;
+        if (e < a.k) {
+            const uint64_t o = uint64_t(q) * a.k + e;
+            const bool none = fin.a[r] == kNone;
+            a.out_ids[o] = none ? ~0ull : a.id_base + uint64_t(fin.b[r]) * a.id_stride;
+            a.out_sqdist_f64[o] = none ? __longlong_as_double(0x7FF0000000000000ll) : __longlong_as_double(fin.a[r]);
+        }
+    }
+    if (lane == 0) a.out_len[q] = U < a.k ? U : a.k;
+}
+
+template <int R>
+__global__ void __launch_bounds__(kRefineThreads, 2) k_gather_f32(RefineArgs a, const uint32_t* __restrict__ lists,
+                                                                  const uint32_t* __restrict__ counts,
+                                                                  uint32_t lstride) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t qstep = gridDim.x * (kRefineThreads / 32);
+    for (uint32_t q = (blockIdx.x * kRefineThreads + threadIdx.x) >> 5; q < a.nq; q += qstep) {
+        const uint32_t n = __ldcg(counts + q);
+        const uint4 qv = load_query_f32(a.queries, a.pitch, q, lane);
+        WarpTopK2<R> tk;
+        tk.init(int(a.k));
+        gather_list_f32<R, false>(a.rows, a.pitch, lists + uint64_t(q) * lstride, n, 0, 8, qv, lane, tk);
+        write_result_f32<R>(a, q, tk, lane, n);
+    }
+}
+
+// Merge NW warp-local pair lists (shared memory) into warp 0's top-k.
+template <int R, int NW>
+__device__ __forceinline__ void merge_warps_f32(WarpTopK2<R>& tk, uint64_t* ma, uint32_t* mb, uint32_t k, int lane,
+                                                int warp) {
+    constexpr int KCAP = 32 * R;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        ma[warp * KCAP + lane * R + r] = tk.a[r];
+        mb[warp * KCAP + lane * R + r] = tk.b[r];
+    }
+    __syncthreads();
+    if (warp == 0) {
+        tk.init(int(k));
+        const uint32_t kr = (k + 31) & ~31u;
+        for (int w = 0; w < NW; ++w)
+            for (uint32_t i = 0; i < kr; i += 32) tk.offer(ma[w * KCAP + i + lane], mb[w * KCAP + i + lane], lane);
+    }
+}
+
+template <int R, int NW>
+__global__ void __launch_bounds__(NW * 32) k_gather_cta_f32(RefineArgs a, const uint32_t* __restrict__ lists,
+                                                            const uint32_t* __restrict__ counts, uint32_t lstride) {
+    __shared__ uint64_t ma[NW * 32 * R];
+    __shared__ uint32_t mb[NW * 32 * R];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (uint32_t q = blockIdx.x; q < a.nq; q += gridDim.x) {
+        const uint32_t n = __ldcg(counts + q);
+        const uint4 qv = load_query_f32(a.queries, a.pitch, q, lane);
+        WarpTopK2<R> tk;
+        tk.init(int(a.k));
+        gather_list_f32<R, false>(a.rows, a.pitch, lists + uint64_t(q) * lstride, n, warp * 8, NW * 8, qv, lane, tk);
+        merge_warps_f32<R, NW>(tk, ma, mb, a.k, lane, warp);
+        if (warp == 0) write_result_f32<R>(a, q, tk, lane, n);
+        __syncthreads();
+    }
+}
+
+template <int R>
+hcg_status gather_f32_launch(const RefineArgs& a, const uint32_t* lists, const uint32_t* counts, uint32_t lstride,
+                             int sms, cudaStream_t st) {
+    if (a.nq * 2 < uint32_t(sms) * 16 * 8) {
+        k_gather_cta_f32<R, 8><<<a.nq, 256, 0, st>>>(a, lists, counts, lstride);
+        return check_launch("k_gather_cta_f32");
+    }
+    const uint32_t blocks = std::min<uint32_t>((a.nq + 7) / 8, uint32_t(sms) * 2);
+    k_gather_f32<R><<<blocks, kRefineThreads, 0, st>>>(a, lists, counts, lstride);
+    return check_launch("k_gather_f32");
+}
+
 // K3b (register variant, the default for C x take <= 32 x 256): each thread
 // holds its <= JMAX window ids in registers (coalesced loads, no staging).
 // Round r: every pending id stores (id << 32 | position) into slot h_r(id) of
@@ -821,6 +981,11 @@ hcg_status refine_dispatch(const RefineArgs& a_in, void* scratch, size_t* scratc
             HCG_RET_IF(check_launch("k_lists_to_ids"));
             continue;
         }
+        if (a.dtype == HCG_F32) {
+            if (a.out_sqdist_f64) a.out_sqdist_f64 += uint64_t(q0) * a_in.k;
+            HCG_RET_IF(gather_f32_launch<R>(a, lists, counts, lstride, sms, st));
+            continue;
+        }
         if (a.nq * 2 < uint32_t(sms) * uint32_t(std::max(g_per_sm, 1)) * 8) {
             // fewer queries than half the resident warps: spread each query over a CTA (latency)
             bool wide = false;
@@ -973,7 +1138,7 @@ __global__ void __launch_bounds__(256) k_brute(BruteArgs a, uint64_t* __restrict
 
 size_t brute_scratch_bytes(const BruteArgs& a) {
     const uint64_t chunks = (a.n + kBruteChunk - 1) / kBruteChunk;
-    return size_t(chunks) * a.nq * a.k * 8;
+    return size_t(chunks) * a.nq * a.k * (a.dtype == HCG_F32 ? 12 : 8);
 }
 
 template <int R, int QPW>
@@ -989,10 +1154,89 @@ static hcg_status brute_launch(const BruteArgs& a, uint64_t* scratch, cudaStream
     return check_launch("k_brute");
 }
 
+// f32 rows: warp per (query, chunk of rows) through the gather path, then a
+// pair merge over the chunks.  Scratch: chunks x nq x k (u64 key, u32 slot).
+template <int R>
+__global__ void __launch_bounds__(256) k_brute_f32(BruteArgs a, uint64_t* __restrict__ part_a,
+                                                   uint32_t* __restrict__ part_b) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t chunk = blockIdx.x, q = blockIdx.y * 8 + warp;
+    if (q >= a.nq) return;
+    const uint64_t r0 = uint64_t(chunk) * kBruteChunk;
+    const uint32_t r1 = uint32_t(min(a.n, r0 + kBruteChunk));
+    const uint4 qv = load_query_f32(a.queries, a.pitch, q, lane);
+    WarpTopK2<R> tk;
+    tk.init(int(a.k));
+    gather_list_f32<R, true>(a.rows, a.pitch, nullptr, r1, uint32_t(r0), 8, qv, lane, tk);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const uint32_t e = uint32_t(lane) * R + r;
+        if (e < a.k) {
+            part_a[(uint64_t(chunk) * a.nq + q) * a.k + e] = tk.a[r];
+            part_b[(uint64_t(chunk) * a.nq + q) * a.k + e] = tk.b[r];
+        }
+    }
+}
+
+template <int R>
+__global__ void __launch_bounds__(256) k_merge_f32(const uint64_t* __restrict__ part_a,
+                                                   const uint32_t* __restrict__ part_b, uint32_t parts, BruteArgs a,
+                                                   uint64_t* __restrict__ out_ids, double* __restrict__ out_sq,
+                                                   uint32_t* __restrict__ out_len) {
+    const uint64_t gw = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (gw >= a.nq) return;
+    const uint32_t q = uint32_t(gw), k = a.k;
+    WarpTopK2<R> tk;
+    tk.init(int(k));
+    for (uint32_t p = 0; p < parts; ++p) {
+        const uint64_t off = (uint64_t(p) * a.nq + q) * k;
+        for (uint32_t i = 0; i < k; i += 32) {
+            const bool in = i + lane < k;
+            tk.offer(in ? part_a[off + i + lane] : kNone, in ? part_b[off + i + lane] : 0xFFFFFFFFu, lane);
+        }
+    }
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const uint32_t e = uint32_t(lane) * R + r;
+        if (e < k) {
+            const bool none = tk.a[r] == kNone;
+            out_ids[uint64_t(q) * k + e] = none ? ~0ull : a.id_base + uint64_t(tk.b[r]) * a.id_stride;
+            out_sq[uint64_t(q) * k + e] = none ? __longlong_as_double(0x7FF0000000000000ll) : __longlong_as_double(tk.a[r]);
+            cnt += none ? 0 : 1;
+        }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) cnt += __shfl_xor_sync(kFull, cnt, off);
+    if (lane == 0) out_len[q] = cnt;
+}
+
+template <int R>
+static hcg_status brute_f32_launch(const BruteArgs& a, uint64_t* scratch, uint64_t* out_ids, double* out_sq,
+                                   uint32_t* out_len, cudaStream_t st) {
+    const uint32_t chunks = uint32_t((a.n + kBruteChunk - 1) / kBruteChunk);
+    uint64_t* pa = scratch;
+    uint32_t* pb = reinterpret_cast<uint32_t*>(scratch + uint64_t(chunks) * a.nq * a.k);
+    k_brute_f32<R><<<dim3(chunks, (a.nq + 7) / 8), 256, 0, st>>>(a, pa, pb);
+    HCG_RET_IF(check_launch("k_brute_f32"));
+    k_merge_f32<R><<<unsigned((uint64_t(a.nq) * 32 + 255) / 256), 256, 0, st>>>(pa, pb, chunks, a, out_ids, out_sq,
+                                                                                 out_len);
+    return check_launch("k_merge_f32");
+}
+
 hcg_status launch_brute(const BruteArgs& a, uint64_t* scratch, uint64_t* out_ids, uint32_t* out_sqdist,
-                        uint32_t* out_len, cudaStream_t st) {
+                        uint32_t* out_len, double* out_sqdist_f64, cudaStream_t st) {
     if (a.nq == 0) return HCG_OK;
     const uint32_t chunks = uint32_t((a.n + kBruteChunk - 1) / kBruteChunk);
+    if (a.dtype == HCG_F32) {
+        switch (r_bucket(a.k)) {
+            case 1: return brute_f32_launch<1>(a, scratch, out_ids, out_sqdist_f64, out_len, st);
+            case 2: return brute_f32_launch<2>(a, scratch, out_ids, out_sqdist_f64, out_len, st);
+            case 4: return brute_f32_launch<4>(a, scratch, out_ids, out_sqdist_f64, out_len, st);
+            default: return brute_f32_launch<8>(a, scratch, out_ids, out_sqdist_f64, out_len, st);
+        }
+    }
     hcg_status rc;
     switch (r_bucket(a.k)) {
         case 1: rc = brute_launch<1, 4>(a, scratch, st); break;

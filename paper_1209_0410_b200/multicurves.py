@@ -20,7 +20,7 @@ from typing import NamedTuple
 
 import numpy as np
 
-from ._lib import HCG_HILBERT, HCG_ZORDER, HcgInvalidArgument, HcgScheme, check, lib
+from ._lib import HCG_F32, HCG_HILBERT, HCG_U8, HCG_ZORDER, HcgInvalidArgument, HcgScheme, check, lib
 
 ZORDER, HILBERT = HCG_ZORDER, HCG_HILBERT
 
@@ -124,18 +124,20 @@ def _ptr(x):
     return x.ctypes.data
 
 
-def _u8_2d(x, d_full: int):
+def _u8_2d(x, d_full: int, dtype: str = "u8"):
+    """Validate n x d_full descriptors of the index's element type (u8 / f32)."""
+    np_dt = np.uint8 if dtype == "u8" else np.float32
     if _is_torch(x):
         torch = _torch()
-        if x.dtype != torch.uint8:
-            raise HcgInvalidArgument(-1, "descriptors must be uint8")
+        if x.dtype != (torch.uint8 if dtype == "u8" else torch.float32):
+            raise HcgInvalidArgument(-1, f"descriptors must be {np.dtype(np_dt).name}")
         x = x.contiguous()
         if x.dim() == 1:
             x = x.view(1, -1)
     else:
         x = np.ascontiguousarray(x)
-        if x.dtype != np.uint8:
-            raise HcgInvalidArgument(-1, "descriptors must be uint8")
+        if x.dtype != np_dt:
+            raise HcgInvalidArgument(-1, f"descriptors must be {np.dtype(np_dt).name}")
         if x.ndim == 1:
             x = x.reshape(1, -1)
     if x.shape[1] != d_full:
@@ -146,7 +148,8 @@ def _u8_2d(x, d_full: int):
 def _empty_like_kind(ref, shape, np_dtype):
     if _is_cuda(ref):
         torch = _torch()
-        tdt = {np.uint64: torch.uint64, np.uint32: torch.uint32, np.int64: torch.int64}[np_dtype]
+        tdt = {np.uint64: torch.uint64, np.uint32: torch.uint32, np.int64: torch.int64,
+               np.float64: torch.float64}[np_dtype]
         return torch.empty(shape, dtype=tdt, device=ref.device)
     return np.empty(shape, dtype=np_dtype)
 
@@ -163,12 +166,14 @@ def _stream(stream, ref=None):
 class MulticurvesIndex:
     """hc::MulticurvesIndex (multicurves.hpp:74-107) resident on one B200.
 
-    rows: n x d_full uint8 descriptors (numpy or torch, host or device); the
-    id of row s is id_base + s * id_stride (ids 0..n-1 by default).
+    rows: n x d_full descriptors (numpy or torch, host or device) -- uint8
+    (bvecs, seen through `view`) or float32 (the reference's own component
+    type, fvecs; `view` unused); the id of row s is id_base + s * id_stride
+    (ids 0..n-1 by default).  dtype ("u8" / "f32") defaults to the rows'.
     """
 
     def __init__(self, rows, scheme: ProjectionScheme, view: View = RAW, device: int = 0,
-                 id_base: int = 0, id_stride: int = 1, stream=None, _handle=None):
+                 id_base: int = 0, id_stride: int = 1, stream=None, _handle=None, dtype: str | None = None):
         self.scheme = scheme
         self.view = view
         self.device = device
@@ -177,9 +182,17 @@ class MulticurvesIndex:
         self._h = None
         if _handle is not None:  # MulticurvesIndex.load
             self._h = _handle
+            self.dtype = "f32" if lib().hcg_index_dtype(_handle) == HCG_F32 else "u8"
             return
+        if dtype is None:
+            is_f32 = rows is not None and str(getattr(rows, "dtype", "")).endswith("float32")
+            dtype = "f32" if is_f32 else "u8"
+        if dtype not in ("u8", "f32"):
+            raise HcgInvalidArgument(-1, f"unknown descriptor dtype {dtype!r}")
+        self.dtype = dtype
         d = scheme.d_full
-        rows = _u8_2d(rows, d) if (rows is not None and len(rows)) else np.zeros((0, d), np.uint8)
+        rows = (_u8_2d(rows, d, dtype) if (rows is not None and len(rows))
+                else np.zeros((0, d), np.uint8 if dtype == "u8" else np.float32))
         n = rows.shape[0]
         off = [0]
         flat = []
@@ -198,17 +211,21 @@ class MulticurvesIndex:
         lut = make_lut(view, scheme.bits_per_dim)
         for b in range(256):
             s.cell_lut[b] = int(lut[b])
-        s.dist_scale = float(view.scale)
+        s.dist_scale = float(view.scale) if dtype == "u8" else 1.0
+        s.dtype = HCG_U8 if dtype == "u8" else HCG_F32
         self._scheme_c = s
         h = C.c_void_p()
         check(lib().hcg_build(C.byref(s), _ptr(rows), n, id_base, id_stride, device,
                               _stream(stream, rows), C.byref(h)))
         self._h = h
 
+    def _rows(self, x):
+        return _u8_2d(x, self.scheme.d_full, self.dtype)
+
     # -- growth and persistence
     def insert(self, rows, stream=None) -> None:
         """multicurves.hpp:79, batched: append rows (ids continue id_base + s*id_stride)."""
-        r = _u8_2d(rows, self.scheme.d_full)
+        r = self._rows(rows)
         check(lib().hcg_insert(self._h, _ptr(r), r.shape[0], _stream(stream, r)))
 
     def save(self, path: str) -> None:
@@ -253,28 +270,31 @@ class MulticurvesIndex:
     def rooted(self, sqdist) -> np.ndarray:
         """Reference distance (vecio.cpp:111): sqrt of the exact squared distance."""
         s = np.asarray(sqdist.cpu() if _is_torch(sqdist) else sqdist).astype(np.float64)
-        return np.sqrt(s) * self.view.scale
+        return np.sqrt(s) * (self.view.scale if self.dtype == "u8" else 1.0)
 
     # -- batched search (the hot path)
     def search_batch(self, queries, k: int, probe_depth: int, stream=None, out=None):
-        """Top-k by (distance, id) of every query: (ids u64 [nq,k], sqdist u32
-        [nq,k], len u32 [nq]).  Padding entries are id 2^64-1 / sqdist 2^32-1."""
-        q = _u8_2d(queries, self.scheme.d_full)
+        """Top-k by (distance, id) of every query: (ids u64 [nq,k], sqdist
+        [nq,k], len u32 [nq]).  sqdist is u32 (exact integers) for u8 rows,
+        padded with 2^32-1; f64 for f32 rows, padded with +inf.  Padding ids
+        are 2^64-1."""
+        q = self._rows(queries)
         nq = q.shape[0]
+        f32 = self.dtype == "f32"
         if out is None:
             ids = _empty_like_kind(q, (nq, k), np.uint64)
-            sq = _empty_like_kind(q, (nq, k), np.uint32)
+            sq = _empty_like_kind(q, (nq, k), np.float64 if f32 else np.uint32)
             ln = _empty_like_kind(q, (nq,), np.uint32)
         else:
             ids, sq, ln = out
-        check(lib().hcg_search(self._h, _ptr(q), nq, k, probe_depth, _ptr(ids), _ptr(sq), _ptr(ln),
-                               _stream(stream, q)))
+        fn = lib().hcg_search_f32 if f32 else lib().hcg_search
+        check(fn(self._h, _ptr(q), nq, k, probe_depth, _ptr(ids), _ptr(sq), _ptr(ln), _stream(stream, q)))
         return ids, sq, ln
 
     def search_timed(self, queries, k: int, probe_depth: int, out, stream=None):
         """search_batch into preallocated outputs, returning the device times (ms)
         of (locate, candidate union, gather+score) measured with CUDA events on `stream`."""
-        q = _u8_2d(queries, self.scheme.d_full)
+        q = self._rows(queries)
         ids, sq, ln = out
         ms = (C.c_float * 3)()
         check(lib().hcg_search_timed(self._h, _ptr(q), q.shape[0], k, probe_depth, _ptr(ids), _ptr(sq),
@@ -291,7 +311,7 @@ class MulticurvesIndex:
 
     def search_packed(self, queries, k: int, probe_depth: int, out=None, stream=None):
         """Per-shard packed results (sqdist<<32 | id) for the sharded merge."""
-        q = _u8_2d(queries, self.scheme.d_full)
+        q = self._rows(queries)
         nq = q.shape[0]
         if out is None:
             out = _empty_like_kind(q, (nq, k), np.uint64)
@@ -302,7 +322,7 @@ class MulticurvesIndex:
     # -- parity taps
     def keys(self, rows, c: int) -> np.ndarray:
         """curve_encode(kind, project(v, scheme, c)) of each row: [n, words] u64 (LS word first)."""
-        r = _u8_2d(rows, self.scheme.d_full)
+        r = self._rows(rows)
         out = np.zeros((r.shape[0], self.key_words(c)), np.uint64)
         check(lib().hcg_keys(self._h, _ptr(r), r.shape[0], c, _ptr(out), _stream(None, r)))
         return out
@@ -317,7 +337,7 @@ class MulticurvesIndex:
 
     def windows(self, queries, probe_depth: int):
         """rank_of and window [begin, end) per (query, curve)."""
-        q = _u8_2d(queries, self.scheme.d_full)
+        q = self._rows(queries)
         nq, C_ = q.shape[0], self.curves()
         r = np.zeros((nq, C_), np.uint64)
         b = np.zeros((nq, C_), np.uint64)
@@ -334,7 +354,7 @@ class MulticurvesIndex:
 
     def candidates(self, queries, probe_depth: int):
         """Deduplicated candidate ids per query (list of sorted arrays)."""
-        q = _u8_2d(queries, self.scheme.d_full)
+        q = self._rows(queries)
         nq = q.shape[0]
         cap = self.curves() * min(probe_depth, max(self.size(), 1))
         out = np.zeros((nq, max(cap, 1)), np.uint64)
@@ -345,7 +365,7 @@ class MulticurvesIndex:
 
     def candidate_counts(self, queries, probe_depth: int) -> np.ndarray:
         """|candidate_union| per query (unique candidates U_q)."""
-        q = _u8_2d(queries, self.scheme.d_full)
+        q = self._rows(queries)
         cnt = np.zeros(q.shape[0], np.uint32)
         check(lib().hcg_candidates(self._h, _ptr(q), q.shape[0], probe_depth, None, 0, _ptr(cnt),
                                    _stream(None, q)))
@@ -357,42 +377,52 @@ class MulticurvesIndex:
 
     def brute_force(self, queries, k: int, stream=None):
         """brute_force_knn (vecio.cpp:115-122) over the indexed rows, on the GPU."""
-        q = _u8_2d(queries, self.scheme.d_full)
+        q = self._rows(queries)
         nq = q.shape[0]
+        f32 = self.dtype == "f32"
         ids = _empty_like_kind(q, (nq, k), np.uint64)
-        sq = _empty_like_kind(q, (nq, k), np.uint32)
+        sq = _empty_like_kind(q, (nq, k), np.float64 if f32 else np.uint32)
         ln = _empty_like_kind(q, (nq,), np.uint32)
-        check(lib().hcg_brute_force(self._h, _ptr(q), nq, k, _ptr(ids), _ptr(sq), _ptr(ln),
-                                    _stream(stream, q)))
+        fn = lib().hcg_brute_force_f32 if f32 else lib().hcg_brute_force
+        check(fn(self._h, _ptr(q), nq, k, _ptr(ids), _ptr(sq), _ptr(ln), _stream(stream, q)))
         return ids, sq, ln
 
 
-def read_vectors(path: str, fmt: str = "bvecs", view: View = RAW) -> np.ndarray:
-    """vecio.cpp:18-61: bvecs / fvecs records -> [n, dim] uint8 rows."""
-    from ._lib import HCG_BVECS, HCG_FVECS
+def read_vectors(path: str, fmt: str = "bvecs", view: View = RAW, dtype: str = "u8") -> np.ndarray:
+    """vecio.cpp:18-61: bvecs / fvecs records -> [n, dim] rows: uint8 (the
+    view's bytes), or with fmt="fvecs", dtype="f32" the float32 components
+    as stored (rows of an f32 index)."""
+    from ._lib import HCG_BVECS, HCG_FVECS, HCG_FVECS_F32
+    f32 = dtype == "f32"
+    if f32 and fmt != "fvecs":
+        raise HcgInvalidArgument(-1, "float rows come from fvecs files")
+    code = HCG_FVECS_F32 if f32 else (HCG_BVECS if fmt == "bvecs" else HCG_FVECS)
     buf = C.POINTER(C.c_uint8)()
     n = C.c_uint64()
     dim = C.c_uint32()
-    check(lib().hcg_read_vectors(os.fsencode(path), HCG_BVECS if fmt == "bvecs" else HCG_FVECS,
-                                 C.c_float(view.offset), C.c_float(view.scale), C.byref(buf), C.byref(n),
-                                 C.byref(dim)))
+    check(lib().hcg_read_vectors(os.fsencode(path), code, C.c_float(view.offset), C.c_float(view.scale),
+                                 C.byref(buf), C.byref(n), C.byref(dim)))
     try:
-        total = n.value * dim.value
-        out = np.ctypeslib.as_array(buf, shape=(max(total, 1),))[:total].copy()
+        nbytes = n.value * dim.value * (4 if f32 else 1)
+        out = np.ctypeslib.as_array(buf, shape=(max(nbytes, 1),))[:nbytes].copy()
     finally:
         lib().hcg_free_buffer(buf)
-    return out.reshape(n.value, dim.value) if n.value else np.zeros((0, dim.value), np.uint8)
+    dt = np.float32 if f32 else np.uint8
+    return out.view(dt).reshape(n.value, dim.value) if n.value else np.zeros((0, dim.value), dt)
 
 
 def write_vectors(path: str, rows, fmt: str = "bvecs", view: View = RAW) -> None:
-    """vecio.cpp:63-85."""
-    from ._lib import HCG_BVECS, HCG_FVECS
-    r = np.ascontiguousarray(rows, dtype=np.uint8)
+    """vecio.cpp:63-85.  float32 rows are written to fvecs as-is."""
+    from ._lib import HCG_BVECS, HCG_FVECS, HCG_FVECS_F32
+    f32 = np.asarray(rows).dtype == np.float32
+    if f32 and fmt != "fvecs":
+        raise HcgInvalidArgument(-1, "float rows go to fvecs files")
+    r = np.ascontiguousarray(rows, dtype=np.float32 if f32 else np.uint8)
     if r.ndim == 1:
         r = r.reshape(1, -1)
-    check(lib().hcg_write_vectors(os.fsencode(path), HCG_BVECS if fmt == "bvecs" else HCG_FVECS,
-                                  C.c_float(view.offset), C.c_float(view.scale), _ptr(r), r.shape[0],
-                                  r.shape[1] if r.size else 0))
+    code = HCG_FVECS_F32 if f32 else (HCG_BVECS if fmt == "bvecs" else HCG_FVECS)
+    check(lib().hcg_write_vectors(os.fsencode(path), code, C.c_float(view.offset), C.c_float(view.scale),
+                                  _ptr(r), r.shape[0], r.shape[1] if r.size else 0))
 
 
 def merge_packed(packed, k: int, device: int = 0, stream=None, out=None):

@@ -91,7 +91,7 @@ def _scheme(d_full=128, curves=8, m=8, kind=1, assign=None):
 
 
 def _build_rc(s, n=4):
-    rows = np.zeros((n, s.d_full), np.uint8)
+    rows = np.zeros((n, s.d_full * 4), np.uint8)  # room for f32 rows too
     h = C.c_void_p()
     return H.lib().hcg_build(C.byref(s), rows.ctypes.data, n, 0, 1, 0, None, C.byref(h))
 
@@ -107,6 +107,21 @@ def test_build_validates_before_touching_the_device():
     assert _build_rc(uncovered) == _lib.HCG_EINVAL
     msg = H.lib().hcg_last_error().decode()
     assert "covered" in msg
+
+
+def test_f32_scheme_validation():
+    s = _scheme()
+    s.dtype = 2
+    assert _build_rc(s) == _lib.HCG_EINVAL  # unknown dtype
+    wide = _scheme(d_full=129, curves=3)
+    wide.dtype = _lib.HCG_F32  # 129 floats = 516 bytes > HCG_MAX_ROW_BYTES
+    assert _build_rc(wide) == _lib.HCG_ECAPACITY
+    assert "128" in H.lib().hcg_last_error().decode()
+    m32 = _scheme(curves=8, m=32)
+    m32.dtype = _lib.HCG_F32
+    for b in range(256):
+        m32.cell_lut[b] = 0xFFFFFFFF  # the table is unused for float rows
+    assert _build_rc(m32) in (_lib.HCG_OK, _lib.HCG_ENODEV)
 
 
 def test_no_gpu_is_an_error_not_a_fallback():

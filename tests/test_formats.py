@@ -68,3 +68,24 @@ def test_nonfinite_fvecs_rejected(tmp_path):
 def test_missing_file(tmp_path):
     with pytest.raises(H.HcgIOError, match="cannot open"):
         H.read_vectors(str(tmp_path / "nope.bvecs"))
+
+
+def test_float_fvecs_round_trip_and_reference_reader(tmp_path):
+    """fvecs with arbitrary float components (rows of an HCG_F32 index): the
+    payload is kept bit-for-bit and equals what the reference's reader loads."""
+    rng = np.random.default_rng(2)
+    rows = (rng.standard_normal((257, 96)) * 1e3).astype(np.float32)
+    rows[0, :4] = [0.0, -0.0, 1e-40, -3.4e38]  # zeros, a denormal, a large value
+    path = str(tmp_path / "f.fvecs")
+    H.write_vectors(path, rows, "fvecs")
+    back = H.read_vectors(path, "fvecs", dtype="f32")
+    assert back.dtype == np.float32 and back.tobytes() == rows.tobytes()
+    if P.ref_available():
+        rc, f = ref_read(path, False)
+        assert rc == 0 and f.tobytes() == rows.tobytes()
+    p = tmp_path / "nan.fvecs"
+    p.write_bytes(struct.pack("<I", 2) + struct.pack("<2f", 1.0, float("inf")))
+    with pytest.raises(H.HcgIOError, match="non-finite"):
+        H.read_vectors(str(p), "fvecs", dtype="f32")
+    with pytest.raises(H.HcgInvalidArgument):
+        H.read_vectors(path, "bvecs", dtype="f32")
