@@ -5,12 +5,15 @@
 //     hc::MulticurvesIndex idx(ds, hc::default_scheme(128, 8, 16, hc::CurveKind::Hilbert, 0));
 //     hc::NeighborList nl = idx.search(q, {10, 350});
 // for
-//     hcb::MulticurvesIndex idx(ds, hcb::default_scheme(128, 8, 16, hcb::CurveKind::Hilbert, 0),
-//                               hcb::View::lifted());
+//     hcb::MulticurvesIndex idx(ds, hcb::default_scheme(128, 8, 16, hcb::CurveKind::Hilbert, 0));
 //     hcb::NeighborList nl = idx.search(q, {10, 350});
 //
-// and gets bit-identical NeighborLists (same ids, same rooted double
-// distances, same (distance, id) tie order) from the B200.  The dataset and
+// and gets the same NeighborLists from the B200.  The default view keeps the
+// float components as they are (HCG_F32: same ids and tie order, distances
+// within 1e-12 relative -- the double terms are summed in a tree instead of
+// sequentially).  Byte-valued data can instead be stored as one byte per
+// component through View::raw() (bvecs) or View::lifted() (1 + b/256): a 4x
+// smaller row, exact integer distances, bit-identical NeighborLists.  The dataset and
 // query types are templates: anything with hc::Dataset / hc::FeatureVector's
 // shape (`.vectors[i].id`, `.vectors[i].components`, `.dims`) works, the
 // reference's own types included.  Errors map back to the reference's
@@ -18,9 +21,8 @@
 // non-finite violations (curve.cpp:35-59,167; vecio.cpp:88,116),
 // std::runtime_error for device failures.
 //
-// Descriptors must be byte-valued in the chosen view (component == offset +
-// b * scale for an integral b in [0, 255]): raw bvecs (View::raw) or the
-// lifted view 1 + b/256 (View::lifted).
+// With a byte view, descriptors must be byte-valued in it (component ==
+// offset + b * scale for an integral b in [0, 255]).
 #pragma once
 
 #include <algorithm>
@@ -59,12 +61,16 @@ struct ProjectionScheme {  // multicurves.hpp:18-32
     std::uint32_t dims_of(std::uint32_t c) const { return static_cast<std::uint32_t>(assignment[c].size()); }
 };
 
-// How the reference sees a stored byte b: offset + b * scale (f32).
+// How descriptors are stored: float components as-is (floats(), the
+// reference's own representation), or one byte b per component that the
+// reference sees as offset + b * scale.
 struct View {
     float offset = 0.0f;
     float scale = 1.0f;
-    static View raw() { return {0.0f, 1.0f}; }             // bvecs widening, vecio.cpp:50-51
-    static View lifted() { return {1.0f, 1.0f / 256.0f}; }  // 1 + b/256
+    bool f32 = false;
+    static View floats() { return {0.0f, 1.0f, true}; }           // HCG_F32
+    static View raw() { return {0.0f, 1.0f, false}; }             // bvecs widening, vecio.cpp:50-51
+    static View lifted() { return {1.0f, 1.0f / 256.0f, false}; }  // 1 + b/256
 };
 
 namespace detail {
@@ -88,6 +94,17 @@ template <class Vec>
 void append_bytes(const Vec& v, std::uint32_t dims, const View& view, std::vector<std::uint8_t>& out) {
     if (v.components.size() != dims) throw std::invalid_argument("dimension mismatch");
     for (float x : v.components) out.push_back(to_byte(x, view));
+}
+
+template <class Vec>
+void append_floats(const Vec& v, std::uint32_t dims, std::vector<float>& out) {
+    if (v.components.size() != dims) throw std::invalid_argument("dimension mismatch");
+    out.insert(out.end(), v.components.begin(), v.components.end());
+}
+
+inline void check_params(const SearchParams& p) {
+    if (p.k < 1 || p.probe_depth < 1) throw std::invalid_argument("invalid search params");
+    if (p.k > HCG_MAX_K || p.probe_depth > 0xFFFFFFFFu) throw std::invalid_argument("k / probe_depth beyond capacity");
 }
 }  // namespace detail
 
@@ -114,21 +131,34 @@ class MulticurvesIndex {
     MulticurvesIndex() = default;
 
     template <class Dataset>
-    MulticurvesIndex(const Dataset& ds, ProjectionScheme scheme, View view = View::raw(), int device = 0)
+    MulticurvesIndex(const Dataset& ds, ProjectionScheme scheme, View view = View::floats(), int device = 0)
         : scheme_(std::move(scheme)), view_(view) {
         std::vector<std::uint8_t> rows;
-        rows.reserve(ds.vectors.size() * scheme_.d_full);
+        std::vector<float> frows;
+        (view_.f32 ? frows.reserve(ds.vectors.size() * scheme_.d_full)
+                   : rows.reserve(ds.vectors.size() * scheme_.d_full));
         for (std::size_t i = 0; i < ds.vectors.size(); ++i) {
             if (ds.vectors[i].id != i) throw std::invalid_argument("dataset ids must be 0..n-1 in order (vecio.hpp:22)");
-            detail::append_bytes(ds.vectors[i], scheme_.d_full, view_, rows);
+            if (view_.f32)
+                detail::append_floats(ds.vectors[i], scheme_.d_full, frows);
+            else
+                detail::append_bytes(ds.vectors[i], scheme_.d_full, view_, rows);
         }
-        build(rows.data(), ds.vectors.size(), device);
+        build(view_.f32 ? static_cast<const void*>(frows.data()) : rows.data(), ds.vectors.size(), device);
+    }
+
+    // Float rows (n x d_full, e.g. fvecs payloads), ids id_base + s * id_stride.
+    MulticurvesIndex(const float* rows, std::uint64_t n, ProjectionScheme scheme, int device = 0,
+                     std::uint64_t id_base = 0, std::uint64_t id_stride = 1)
+        : scheme_(std::move(scheme)), view_(View::floats()) {
+        build(rows, n, device, id_base, id_stride);
     }
 
     // Raw byte rows (bvecs payloads), ids id_base + s * id_stride.
     MulticurvesIndex(const std::uint8_t* rows, std::uint64_t n, ProjectionScheme scheme, View view, int device = 0,
                      std::uint64_t id_base = 0, std::uint64_t id_stride = 1)
         : scheme_(std::move(scheme)), view_(view) {
+        if (view_.f32) throw std::invalid_argument("byte rows need a byte view");
         build(rows, n, device, id_base, id_stride);
     }
 
@@ -152,16 +182,39 @@ class MulticurvesIndex {
     // multicurves.hpp:81 for one query.
     template <class FeatureVector>
     NeighborList search(const FeatureVector& q, const SearchParams& p) const {
+        if (view_.f32) {
+            std::vector<float> qf;
+            detail::append_floats(q, scheme_.d_full, qf);
+            return search_floats(qf.data(), 1, p).front();
+        }
         std::vector<std::uint8_t> qb;
         detail::append_bytes(q, scheme_.d_full, view_, qb);
         return search_bytes(qb.data(), 1, p).front();
     }
 
+    // Batched search over float queries (nq x d_full) of a floats() index.
+    std::vector<NeighborList> search_floats(const float* queries, std::uint32_t nq, const SearchParams& p,
+                                            void* stream = nullptr) const {
+        detail::check_params(p);
+        const std::uint32_t k = static_cast<std::uint32_t>(p.k);
+        std::vector<std::uint64_t> ids(std::size_t(nq) * k);
+        std::vector<double> sq(std::size_t(nq) * k);
+        std::vector<std::uint32_t> len(nq);
+        detail::check(hcg_search_f32(ix_, queries, nq, k, static_cast<std::uint32_t>(p.probe_depth), ids.data(),
+                                     sq.data(), len.data(), stream));
+        std::vector<NeighborList> out(nq);
+        for (std::uint32_t q = 0; q < nq; ++q) {
+            out[q].resize(len[q]);
+            for (std::uint32_t i = 0; i < len[q]; ++i)
+                out[q][i] = {ids[std::size_t(q) * k + i], std::sqrt(sq[std::size_t(q) * k + i])};
+        }
+        return out;
+    }
+
     // Batched search over byte queries (nq x d_full); one NeighborList each.
     std::vector<NeighborList> search_bytes(const std::uint8_t* queries, std::uint32_t nq, const SearchParams& p,
                                            void* stream = nullptr) const {
-        if (p.k < 1 || p.probe_depth < 1) throw std::invalid_argument("invalid search params");
-        if (p.k > HCG_MAX_K || p.probe_depth > 0xFFFFFFFFu) throw std::invalid_argument("k / probe_depth beyond capacity");
+        detail::check_params(p);
         const std::uint32_t k = static_cast<std::uint32_t>(p.k);
         std::vector<std::uint64_t> ids(std::size_t(nq) * k);
         std::vector<std::uint32_t> sq(std::size_t(nq) * k), len(nq);
@@ -181,19 +234,24 @@ class MulticurvesIndex {
     template <class FeatureVector>
     std::vector<std::uint64_t> candidate_union(const FeatureVector& q, std::size_t depth) const {
         std::vector<std::uint8_t> qb;
-        detail::append_bytes(q, scheme_.d_full, view_, qb);
+        std::vector<float> qf;
+        if (view_.f32)
+            detail::append_floats(q, scheme_.d_full, qf);
+        else
+            detail::append_bytes(q, scheme_.d_full, view_, qb);
+        const void* qp = view_.f32 ? static_cast<const void*>(qf.data()) : qb.data();
         const std::uint32_t cap = static_cast<std::uint32_t>(scheme_.curves() * std::min<std::size_t>(depth, size()));
         std::vector<std::uint64_t> ids(cap ? cap : 1);
         std::uint32_t cnt = 0;
-        detail::check(hcg_candidates(ix_, qb.data(), 1, static_cast<std::uint32_t>(depth), ids.data(), cap ? cap : 1,
-                                     &cnt, nullptr));
+        detail::check(hcg_candidates(ix_, static_cast<const std::uint8_t*>(qp), 1, static_cast<std::uint32_t>(depth),
+                                     ids.data(), cap ? cap : 1, &cnt, nullptr));
         ids.resize(cnt);
         std::sort(ids.begin(), ids.end());
         return ids;
     }
 
   private:
-    void build(const std::uint8_t* rows, std::uint64_t n, int device, std::uint64_t id_base = 0,
+    void build(const void* rows, std::uint64_t n, int device, std::uint64_t id_base = 0,
                std::uint64_t id_stride = 1) {
         std::vector<std::uint32_t> off{0}, asg;
         for (const auto& slots : scheme_.assignment) {
@@ -207,9 +265,11 @@ class MulticurvesIndex {
         s.curve_kind = static_cast<std::uint32_t>(scheme_.curve_kind);
         s.assign_off = off.data();
         s.assign = asg.data();
-        s.dist_scale = view_.scale;
-        detail::check(hcg_make_lut(view_.offset, view_.scale, scheme_.bits_per_dim, s.cell_lut));
-        detail::check(hcg_build(&s, rows, n, id_base, id_stride, device, nullptr, &ix_));
+        s.dist_scale = view_.f32 ? 1.0 : view_.scale;
+        s.dtype = view_.f32 ? HCG_F32 : HCG_U8;
+        if (!view_.f32) detail::check(hcg_make_lut(view_.offset, view_.scale, scheme_.bits_per_dim, s.cell_lut));
+        detail::check(hcg_build(&s, static_cast<const std::uint8_t*>(rows), n, id_base, id_stride, device, nullptr,
+                                &ix_));
     }
 
     hcg_index* ix_ = nullptr;

@@ -2,7 +2,9 @@
 // libhcg.so against the CPU oracle (oracle/liboracle.so, test infrastructure).
 // Prints "wrapper ok" and exits 0 on bit-identical NeighborLists.
 #include <cstdio>
+#include <cmath>
 #include <cstdlib>
+#include <limits>
 #include <vector>
 
 #include "hypercurves_b200.hpp"
@@ -77,6 +79,41 @@ int main() {
     } catch (const std::invalid_argument&) {
     }
     orc_free(oi);
+
+    // Float descriptors through the default view (HCG_F32): arbitrary signed
+    // floats, ids exact, distances within 1e-12 relative of the oracle.
+    {
+        std::srand(7);
+        auto rnd = [] { return (float(std::rand()) / float(RAND_MAX) - 0.5f) * 200.0f; };
+        Data fd{d, {}};
+        std::vector<float> ff(size_t(n) * d), fq(size_t(nq) * d);
+        for (uint32_t i = 0; i < n; ++i) {
+            Vec v{i, std::vector<float>(d)};
+            for (uint32_t j = 0; j < d; ++j) v.components[j] = ff[size_t(i) * d + j] = rnd();
+            fd.vectors.push_back(std::move(v));
+        }
+        for (auto& x : fq) x = rnd();
+        hcb::MulticurvesIndex fidx(fd, hcb::default_scheme(d, C, m, hcb::CurveKind::Hilbert, 0));
+        void* fo = orc_build(d, C, m, 1, off.data(), asg.data(), ff.data(), n, nullptr, 4, &err);
+        orc_search(fo, fq.data(), nq, k, depth, oids.data(), od.data(), ol.data(), 4);
+        for (uint32_t q = 0; q < nq; ++q) {
+            Vec qv{q, std::vector<float>(fq.begin() + size_t(q) * d, fq.begin() + size_t(q + 1) * d)};
+            const hcb::NeighborList nl = fidx.search(qv, {k, depth});
+            if (nl.size() != ol[q]) ++bad;
+            for (size_t i = 0; i < nl.size() && i < ol[q]; ++i)
+                if (nl[i].id != oids[q * k + i] ||
+                    std::abs(nl[i].distance - od[q * k + i]) > 1e-12 * od[q * k + i])
+                    ++bad;
+        }
+        try {  // non-finite query component: invalid_argument (curve.cpp:167)
+            Vec qv{0, std::vector<float>(d, 1.0f)};
+            qv.components[3] = std::numeric_limits<float>::quiet_NaN();
+            fidx.search(qv, {k, depth});
+            ++bad;
+        } catch (const std::invalid_argument&) {
+        }
+        orc_free(fo);
+    }
     if (bad) {
         std::printf("wrapper FAILED: %d mismatches\n", bad);
         return 1;
