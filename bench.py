@@ -61,7 +61,10 @@ def parse():
     p.add_argument("--shard-depth", default="planned",
                    help="N>1 per-shard depth: planned | full | optimist | <int>")
     p.add_argument("--recall-sample", type=int, default=1000)
-    p.add_argument("--cpu-sample", type=int, default=4000, help="queries in the CPU baseline sample")
+    p.add_argument("--cpu-sample", type=int, default=100_000,
+                   help="queries of step 0 in our arm's CPU baseline + parity sample (~10 s on 16 cores)")
+    p.add_argument("--ref-sample", type=int, default=20_000,
+                   help="queries per step timed by the reference arm (--impl reference)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--latency-batches", default="1,16,256,4096,65536")
     p.add_argument("--latency-reps", type=int, default=20)
@@ -436,7 +439,7 @@ def run_reference(a):
     t0 = time.perf_counter()
     ri = P.RefIndex(rows, C, m, kind, view)
     build_s = time.perf_counter() - t0
-    S = min(a.cpu_sample, a.queries)
+    S = min(a.ref_sample, a.queries)
     steps_q = [P.gen_queries(b * a.queries, S, n_total, threads) for b in range(a.warmup + a.steps)]
     for b in range(a.warmup):
         ri.search(steps_q[b], k, depth, threads)

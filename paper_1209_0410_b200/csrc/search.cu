@@ -688,23 +688,37 @@ __global__ void __launch_bounds__(NT, MINB) k_union_reg(RefineArgs a, uint32_t* 
     extern __shared__ __align__(16) unsigned char smem[];
     unsigned long long* tab = reinterpret_cast<unsigned long long*>(smem);  // [1 << tb]
     const uint32_t** sptr = reinterpret_cast<const uint32_t**>(tab + (size_t(1) << tb));
-    uint32_t* sbeg = reinterpret_cast<uint32_t*>(sptr + a.C);
-    uint32_t* wsum = sbeg + a.C;  // [NT/32] scan scratch
+    uint32_t* wsum = reinterpret_cast<uint32_t*>(sptr + a.C);  // [NT/32] scan scratch
     const uint32_t T = a.C * a.take;
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t take = a.take, shift = 32 - tb, tmask = (1u << tb) - 1;
     for (uint32_t c = tid; c < a.C; c += NT) sptr[c] = a.slots[c];
+    __syncthreads();
+    constexpr uint32_t kWarps = NT / 32;
+    // Layouts: a warp per curve (coalesced 128-B window reads) when the warps
+    // divide evenly over the curves; else a fixed curve per thread; else a walk.
+    const int layout = kWarps % a.C == 0 ? 0 : (NT % a.C == 0 ? 1 : 2);
 
     for (uint32_t q = blockIdx.x; q < a.nq; q += gridDim.x) {
-        __syncthreads();  // previous query done with tab / sbeg
-        for (uint32_t c = tid; c < a.C; c += NT) sbeg[c] = a.begins[uint64_t(q) * a.C + c];
-        __syncthreads();
+        // (the previous query's scan barriers ordered every read of tab / wsum)
         uint32_t id[JMAX];
         uint32_t pending = 0;
-        if (NT % a.C == 0) {
-            // fixed curve per thread: position (c, p0 + j * step), no walking
+        if (layout == 0) {
+            const uint32_t c = warp % a.C, step = 32 * (kWarps / a.C);
+            const uint32_t* src = sptr[c] + __ldg(a.begins + uint64_t(q) * a.C + c);
+            uint32_t p = lane + 32 * (warp / a.C);
+#pragma unroll
+            for (int j = 0; j < JMAX; ++j) {
+                id[j] = 0;
+                if (p < take) {
+                    id[j] = __ldg(src + p);
+                    pending |= 1u << j;
+                }
+                p += step;
+            }
+        } else if (layout == 1) {
             const uint32_t c = tid % a.C, step = NT / a.C;
-            const uint32_t* src = sptr[c] + sbeg[c];
+            const uint32_t* src = sptr[c] + __ldg(a.begins + uint64_t(q) * a.C + c);
             uint32_t p = tid / a.C;
 #pragma unroll
             for (int j = 0; j < JMAX; ++j) {
@@ -716,6 +730,7 @@ __global__ void __launch_bounds__(NT, MINB) k_union_reg(RefineArgs a, uint32_t* 
                 p += step;
             }
         } else {
+            const uint32_t* bq = a.begins + uint64_t(q) * a.C;
             uint32_t c = 0, p = tid;
             while (p >= take && c + 1 < a.C) {
                 p -= take;
@@ -726,7 +741,7 @@ __global__ void __launch_bounds__(NT, MINB) k_union_reg(RefineArgs a, uint32_t* 
                 const uint32_t i = tid + j * NT;
                 id[j] = 0;
                 if (i < T) {
-                    id[j] = __ldg(sptr[c] + sbeg[c] + p);
+                    id[j] = __ldg(sptr[c] + __ldg(bq + c) + p);
                     pending |= 1u << j;
                 }
                 p += NT;
@@ -737,8 +752,9 @@ __global__ void __launch_bounds__(NT, MINB) k_union_reg(RefineArgs a, uint32_t* 
             }
         }
         uint32_t keep = 0;
+        bool left = true;
 #pragma unroll 1
-        for (int r = 0; r < kRegRounds; ++r) {
+        for (int r = 0; r < kRegRounds && left; ++r) {
             const uint32_t mul = 0x9E3779B1u + 0x7F4A7C16u * uint32_t(r) * 2u;  // odd
 #pragma unroll
             for (int j = 0; j < JMAX; ++j)
@@ -755,9 +771,9 @@ __global__ void __launch_bounds__(NT, MINB) k_union_reg(RefineArgs a, uint32_t* 
                     }
                 }
             }
-            if (!__syncthreads_or(pending != 0)) break;
+            left = __syncthreads_or(pending != 0);  // also orders this round's reads before the next stores
         }
-        if (__syncthreads_or(pending != 0)) {  // rare: CAS set over the cleared table
+        if (left) {  // rare: CAS set over the cleared table
             for (uint32_t i = tid; i <= tmask; i += NT) tab[i] = ~0ull;
             __syncthreads();
 #pragma unroll
@@ -905,7 +921,10 @@ hcg_status union_reg_launch(const RefineArgs& a, uint32_t* lists, uint32_t* coun
 template <int NT>
 hcg_status union_reg_dispatch(const RefineArgs& a, uint32_t* lists, uint32_t* counts, uint32_t lstride, uint32_t tb,
                               int device, cudaStream_t st) {
-    const uint32_t jn = NT % a.C == 0 ? (a.take + NT / a.C - 1) / (NT / a.C) : (a.C * a.take + NT - 1) / NT;
+    constexpr uint32_t kWarps = NT / 32;
+    const uint32_t jn = kWarps % a.C == 0 ? (a.take + 32 * (kWarps / a.C) - 1) / (32 * (kWarps / a.C))
+                        : NT % a.C == 0   ? (a.take + NT / a.C - 1) / (NT / a.C)
+                                          : (a.C * a.take + NT - 1) / NT;
     if (jn > 32) return set_error(HCG_ECAPACITY, "union: more than 32 ids per thread");
     if (jn <= 4) return union_reg_launch<4, NT>(a, lists, counts, lstride, tb, device, st);
     if (jn <= 8) return union_reg_launch<8, NT>(a, lists, counts, lstride, tb, device, st);
@@ -967,7 +986,8 @@ hcg_status refine_dispatch(const RefineArgs& a_in, void* scratch, size_t* scratc
         if (a.out_len) a.out_len += q0;
         if (a.out_packed) a.out_packed += uint64_t(q0) * a_in.k;
         if (reg_union) {
-            HCG_RET_IF(launch_union_reg(a, lists, counts, lstride, tb, device, st));
+            static const int tb_extra = getenv("HCG_UNION_TB_EXTRA") ? atoi(getenv("HCG_UNION_TB_EXTRA")) : 0;
+            HCG_RET_IF(launch_union_reg(a, lists, counts, lstride, tb + uint32_t(tb_extra), device, st));
         } else if (smem_union) {
             const uint32_t ugrid = persistent_grid(reinterpret_cast<const void*>(k_union), usmem, device, a.nq);
             k_union<<<ugrid, kRefineThreads, usmem, st>>>(a, lists, counts, lstride, utb);
