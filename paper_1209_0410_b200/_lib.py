@@ -8,7 +8,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libhcg.so")
+# HCG_LIB_OVERRIDE: load a differently-compiled libhcg.so (tuning experiments).
+LIB_PATH = os.environ.get("HCG_LIB_OVERRIDE") or os.path.join(HERE, "libhcg.so")
 
 HCG_OK = 0
 HCG_EINVAL = -1

@@ -172,6 +172,62 @@ __device__ __forceinline__ uint4 ldg_stream(const void* p) {
 }
 
 // ------------------------------------------------------------ warp top-k ----
+// Bitonic sort of one u64 per lane, ascending over the warp (15 exchanges).
+__device__ __forceinline__ uint64_t warp_sort_asc(uint64_t c, int lane) {
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            const uint64_t y = __shfl_xor_sync(kFull, c, j);
+            const bool keep_min = ((lane & j) == 0) == ((lane & k) == 0);
+            c = keep_min ? (c < y ? c : y) : (c < y ? y : c);
+        }
+    }
+    return c;
+}
+
+// Keep the N = 32*R smallest of a sorted blocked list a (element e in lane
+// e / R, register e % R) and a warp-sorted b (one per lane): c_i = min(a_i,
+// b_{N-1-i}) is bitonic and holds exactly those N, a bitonic merge sorts it.
+template <int R>
+__device__ __forceinline__ void merge_sorted32(uint64_t (&a)[R], uint64_t b, int lane) {
+    constexpr int N = 32 * R;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int t = lane * R + r - (N - 32);
+        const uint64_t y = __shfl_sync(kFull, b, (31 - t) & 31);
+        if (t >= 0 && y < a[r]) a[r] = y;
+    }
+#pragma unroll
+    for (int j = N / 2; j >= 1; j >>= 1) {
+        if (j >= R) {
+            const int lj = j / R;
+            const bool lower = (lane & lj) == 0;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const uint64_t y = __shfl_xor_sync(kFull, a[r], lj);
+                a[r] = lower ? (a[r] < y ? a[r] : y) : (a[r] < y ? y : a[r]);
+            }
+        } else {
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                if ((r & j) == 0) {
+                    const uint64_t x = a[r], y = a[r | j];
+                    a[r] = x < y ? x : y;
+                    a[r | j] = x < y ? y : x;
+                }
+            }
+        }
+    }
+}
+
+// Offers passing the threshold in one call at or above which WarpTopK sorts
+// them and merges the whole batch instead of inserting them one by one.
+#ifndef HCG_TOPK_BATCH_MIN
+#define HCG_TOPK_BATCH_MIN 6
+#endif
+constexpr int kTopkBatchMin = HCG_TOPK_BATCH_MIN;
+
 // A warp holds a sorted (ascending) list of KCAP = 32*R packed (sqdist<<32 |
 // slot) values in registers, blocked layout: element e lives in lane e / R,
 // register e % R.  Packing makes the reference's (distance, id) order
@@ -190,6 +246,15 @@ struct WarpTopK {
         thr_reg = (k - 1) % R;
     }
 
+    __device__ __forceinline__ void update_thr() {
+        // arithmetic select: a runtime-indexed a[thr_reg] would spill the
+        // list to local memory
+        uint64_t mine = 0;
+#pragma unroll
+        for (int r = 0; r < R; ++r) mine |= a[r] & (0ull - uint64_t(r == thr_reg));
+        thr = __shfl_sync(kFull, mine, thr_lane);
+    }
+
     // Insert a warp-uniform value x (must be distinct from every held value).
     __device__ __forceinline__ void insert(uint64_t x, int lane) {
         const uint64_t prev_last = __shfl_up_sync(kFull, a[R - 1], 1);
@@ -201,17 +266,18 @@ struct WarpTopK {
             if (!p_lt) a[r] = p;
             else if (a[r] > x) a[r] = x;
         }
-        // arithmetic select: a runtime-indexed a[thr_reg] would spill the
-        // list to local memory
-        uint64_t mine = 0;
-#pragma unroll
-        for (int r = 0; r < R; ++r) mine |= a[r] & (0ull - uint64_t(r == thr_reg));
-        thr = __shfl_sync(kFull, mine, thr_lane);
+        update_thr();
     }
 
-    // Offer one candidate per lane (kNone = no candidate).
+    // Offer one candidate per lane (kNone = no candidate).  Many passing
+    // offers (the fill phase of a large k) are sorted and merged in one go.
     __device__ __forceinline__ void offer(uint64_t cand, int lane) {
         unsigned m = __ballot_sync(kFull, cand < thr);
+        if (R >= 2 && __popc(m) >= kTopkBatchMin) {
+            merge_sorted32<R>(a, warp_sort_asc(cand < thr ? cand : kNone, lane), lane);
+            update_thr();
+            return;
+        }
         while (m) {
             const int src = __ffs(m) - 1;
             const uint64_t x = __shfl_sync(kFull, cand, src);
