@@ -25,6 +25,7 @@ CUDA events, two streams) and the CPU tests (a simulated device).
 """
 from __future__ import annotations
 
+import gc
 import time
 from collections import deque
 from dataclasses import dataclass, field
@@ -73,6 +74,15 @@ class BatchController:
         backend.poll(token) -> completion time or None
         clock() -> now; idle(next_event_time) -> None (sleep/spin or advance a
         virtual clock)."""
+        gc_on = gc.isenabled()
+        gc.disable()  # a full collection mid-run stalls dispatch for milliseconds
+        try:
+            return self._run(arrivals, backend, clock, idle)
+        finally:
+            if gc_on:
+                gc.enable()
+
+    def _run(self, arrivals, backend, clock, idle) -> RunResult:
         p = self.policy
         arrivals = np.asarray(arrivals, dtype=np.float64)
         n = len(arrivals)
@@ -192,28 +202,33 @@ def spin_idle(clock):
 
 class ShardedBackend:
     """Multi-GPU serving (configs[4]): rank 0 runs the controller; every
-    dispatch broadcasts (first, count) to the other ranks, all ranks run the
-    sharded search of that batch (whose NCCL all-gather keeps them in
-    lockstep), and rank 0 observes completion.  One batch in flight across the
-    group (slots=1): the collectives of consecutive batches stay ordered."""
+    dispatch sends (first, count) to the other ranks over a host-side (gloo)
+    group, and all ranks enqueue the sharded search of that batch, whose NCCL
+    all-gather keeps the GPUs in lockstep; rank 0 observes completion.  The
+    command channel never waits on a GPU, so with `slots` = 2 every rank
+    enqueues batch b+1 while batch b runs (double buffering, SPEC.md:436);
+    consecutive batches' collectives are issued in the same order on every
+    rank, which keeps them matched."""
 
     STOP = -1
 
-    def __init__(self, search_fn, queries, k: int, max_batch: int = 8192):
+    def __init__(self, search_fn, queries, k: int, max_batch: int = 8192, slots: int = 2, cmd_group=None):
         import torch
+        import torch.distributed as dist
         self.torch = torch
         self.search_fn = search_fn  # search_fn(queries_slice, out)
         self.queries = queries
         dev = queries.device
-        self.cmd = torch.zeros(2, dtype=torch.int64, device=dev)
-        self.out = (torch.empty((max_batch, k), dtype=torch.uint64, device=dev),
-                    torch.empty((max_batch, k), dtype=torch.uint32, device=dev),
-                    torch.empty((max_batch,), dtype=torch.uint32, device=dev))
+        self.group = cmd_group if cmd_group is not None else dist.new_group(backend="gloo")
+        self.cmd = torch.zeros(2, dtype=torch.int64)  # host tensor: gloo
+        self.outs = [(torch.empty((max_batch, k), dtype=torch.uint64, device=dev),
+                      torch.empty((max_batch, k), dtype=torch.uint32, device=dev),
+                      torch.empty((max_batch,), dtype=torch.uint32, device=dev)) for _ in range(slots)]
         self.start = None
         self.clock = None
 
-    def _run_batch(self, first: int, count: int):
-        out = tuple(o[:count] for o in self.out)
+    def _run_batch(self, first: int, count: int, slot: int):
+        out = tuple(o[:count] for o in self.outs[slot])
         self.search_fn(self.queries[first:first + count], out)
 
     def begin(self):
@@ -225,11 +240,14 @@ class ShardedBackend:
         self.clock = _WallClock()
         return self.clock
 
-    def launch(self, first: int, count: int, slot: int):
+    def _send(self, first: int, count: int, slot: int):
         import torch.distributed as dist
-        self.cmd[0], self.cmd[1] = first, count
-        dist.broadcast(self.cmd, 0)
-        self._run_batch(first, count)
+        self.cmd[0], self.cmd[1] = first, (count << 8) | slot
+        dist.broadcast(self.cmd, 0, group=self.group)
+
+    def launch(self, first: int, count: int, slot: int):
+        self._send(first, count, slot)
+        self._run_batch(first, count, slot)
         ev = self.torch.cuda.Event(enable_timing=True)
         ev.record()
         return ev
@@ -240,16 +258,23 @@ class ShardedBackend:
         return self.start.elapsed_time(ev) * 1e-3
 
     def stop(self):
-        import torch.distributed as dist
-        self.cmd[0], self.cmd[1] = self.STOP, 0
-        dist.broadcast(self.cmd, 0)
+        self._send(self.STOP, 0, 0)
 
     def follow(self):
         """Non-zero ranks: run every broadcast batch until the stop command."""
         import torch.distributed as dist
+        gc_on = gc.isenabled()
+        gc.disable()
+        try:
+            self._follow(dist)
+        finally:
+            if gc_on:
+                gc.enable()
+
+    def _follow(self, dist):
         while True:
-            dist.broadcast(self.cmd, 0)
-            first, count = (int(x) for x in self.cmd.tolist())
+            dist.broadcast(self.cmd, 0, group=self.group)
+            first, word = int(self.cmd[0]), int(self.cmd[1])
             if first == self.STOP:
                 break
-            self._run_batch(first, count)
+            self._run_batch(first, word >> 8, word & 0xFF)

@@ -72,12 +72,17 @@ class ShardedIndex:
         return cls(local, rank, world, group)
 
     def _buf(self, key, shape, dtype, device):
+        """A view of a grow-only scratch buffer: batches of varying size (the
+        online controller) reuse one allocation instead of the allocator."""
         import torch
+        numel = 1
+        for x in shape:
+            numel *= int(x)
         b = self._bufs.get(key)
-        if b is None or tuple(b.shape) != tuple(shape):
-            b = torch.empty(shape, dtype=dtype, device=device)
+        if b is None or b.numel() < numel:
+            b = torch.empty(max(numel, 1), dtype=dtype, device=device)
             self._bufs[key] = b
-        return b
+        return b[:numel].view(shape)
 
     def search(self, queries, k: int, shard_depth: int, out=None):
         """Global top-k of a query batch (device tensors in and out).

@@ -29,6 +29,7 @@ ap.add_argument("--k", type=int, default=10)
 ap.add_argument("--depth", type=int, default=350)
 ap.add_argument("--max-batch", type=int, default=8192)
 ap.add_argument("--loads", default="0.05,0.2,0.4,0.6,0.8,1.0")
+ap.add_argument("--slots", type=int, default=2, help="batches in flight (2 = double buffer)")
 a = ap.parse_args()
 
 world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -51,10 +52,14 @@ def search(q, out, stream=None):
         sidx.search(q, a.k, depth, out=out)
 
 
+cmd_group = dist.new_group(backend="gloo") if world > 1 else None
+
+
 def make_backend(pol):
     if world == 1:
         return CudaBackend(search, queries, a.k, slots=pol.slots, max_batch=pol.max_batch)
-    return ShardedBackend(lambda q, out: search(q, out), queries, a.k, max_batch=pol.max_batch)
+    return ShardedBackend(lambda q, out: search(q, out), queries, a.k, max_batch=pol.max_batch, slots=pol.slots,
+                          cmd_group=cmd_group)
 
 
 def serve(arrivals, pol):
@@ -69,7 +74,7 @@ def serve(arrivals, pol):
     return res.summary()
 
 
-pol = Policy(max_batch=a.max_batch, slots=2 if world == 1 else 1)
+pol = Policy(max_batch=a.max_batch, slots=a.slots)
 serve(np.zeros(min(a.queries, 50000)), pol)  # warm-up
 sat = serve(np.zeros(a.queries), pol)  # calibrate_max_throughput
 qmax = torch.tensor([sat["throughput_qps"] if rank == 0 else 0.0], device=f"cuda:{local}")
