@@ -18,7 +18,7 @@ ROOT = os.path.dirname(HERE)
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
                      "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]
-CU = ["build.cu", "search.cu", "datagen.cu", "api.cu"]
+CU = ["build.cu", "search.cu", "brute_tc.cu", "datagen.cu", "api.cu"]
 CPP = ["planner.cpp", "io.cpp"]
 HEADERS = ["hcg_internal.cuh", "hcg_host.hpp"]
 

@@ -8,6 +8,12 @@
 
 #include "../../include/hcg.h"
 
+#define HCG_RET_IF(x)                   \
+    do {                                \
+        const hcg_status r_ = (x);      \
+        if (r_ != HCG_OK) return r_;    \
+    } while (0)
+
 namespace hcg {
 
 struct CurveDev;
@@ -97,6 +103,11 @@ struct BruteArgs {
     int dtype;
 };
 size_t brute_scratch_bytes(const BruteArgs& a);
+// brute_tc.cu: the same on the tensor cores (u8 rows of 128 B, k <= 32)
+bool brute_tc_eligible(const BruteArgs& a);
+size_t brute_tc_scratch_bytes(const BruteArgs& a);
+hcg_status launch_brute_tc(const BruteArgs& a, void* scratch, uint64_t* out_ids, uint32_t* out_sqdist,
+                           uint32_t* out_len, cudaStream_t st);
 hcg_status launch_brute(const BruteArgs& a, uint64_t* scratch, uint64_t* out_ids, uint32_t* out_sqdist,
                         uint32_t* out_len, double* out_sqdist_f64, cudaStream_t st);
 

@@ -28,12 +28,6 @@
 
 namespace hcg {
 
-#define HCG_RET_IF(x)                   \
-    do {                                \
-        const hcg_status r_ = (x);      \
-        if (r_ != HCG_OK) return r_;    \
-    } while (0)
-
 __device__ __forceinline__ unsigned lanemask_lt_s() {
     unsigned m;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
@@ -1158,7 +1152,8 @@ __global__ void __launch_bounds__(256) k_brute(BruteArgs a, uint64_t* __restrict
 
 size_t brute_scratch_bytes(const BruteArgs& a) {
     const uint64_t chunks = (a.n + kBruteChunk - 1) / kBruteChunk;
-    return size_t(chunks) * a.nq * a.k * (a.dtype == HCG_F32 ? 12 : 8);
+    const size_t cc = size_t(chunks) * a.nq * a.k * (a.dtype == HCG_F32 ? 12 : 8);
+    return brute_tc_eligible(a) ? std::max(cc, brute_tc_scratch_bytes(a)) : cc;
 }
 
 template <int R, int QPW>
@@ -1257,6 +1252,7 @@ hcg_status launch_brute(const BruteArgs& a, uint64_t* scratch, uint64_t* out_ids
             default: return brute_f32_launch<8>(a, scratch, out_ids, out_sqdist_f64, out_len, st);
         }
     }
+    if (brute_tc_eligible(a)) return launch_brute_tc(a, scratch, out_ids, out_sqdist, out_len, st);
     hcg_status rc;
     switch (r_bucket(a.k)) {
         case 1: rc = brute_launch<1, 4>(a, scratch, st); break;
