@@ -39,7 +39,11 @@ constexpr int kThreads = 384;     // 12 warps
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kATileBytes = kBM * kRowBytes;  // 16 KB
 constexpr uint32_t kBTileBytes = kBN * kRowBytes;  // 32 KB
-constexpr size_t kSmemBytes = 1024 + kATileBytes + size_t(kStages) * kBTileBytes + 256;
+constexpr int kEpiThreads = 256;  // warps 4-11
+// + per-epilogue-thread spill of 32 distances for the rare insertion path
+// + the distance spill + a double buffer of row norms (one tile each)
+constexpr size_t kSmemBytes = 1024 + kATileBytes + size_t(kStages) * kBTileBytes + 256 + 32 * kEpiThreads * 4 +
+                              2 * kBN * 4;
 
 // ---- PTX helpers (tcgen05 / TMA / mbarrier) ----
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -118,6 +122,10 @@ constexpr uint32_t idesc_u8(int M, int N) {
            | (uint32_t(N >> 3) << 17) | (uint32_t(M >> 4) << 24);
 }
 
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+
 template <int KT>
 __device__ __forceinline__ void topk_insert(uint64_t (&a)[KT], uint64_t v) {
 #pragma unroll
@@ -161,6 +169,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* acc_full = a_full + 1;        // [2]
     uint64_t* acc_empty = acc_full + 2;     // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+    uint32_t* spill = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(bars) + 256);  // [32][kEpiThreads]
+    uint32_t* nbuf = spill + 32 * kEpiThreads;                                                      // [2][kBN]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t qt = blockIdx.x / chunks, chunk = blockIdx.x % chunks;
@@ -241,35 +251,62 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint64_t top[KT];
 #pragma unroll
         for (int i = 0; i < KT; ++i) top[i] = kNone;
+        // Row norms: the epilogue prefetches tile t+1's 256 norms (cp.async,
+        // 64 x 16 B) into a shared double buffer while it scores tile t.
+        const int et = threadIdx.x - 128;
+        auto fetch_norms = [&](int t) {
+            if (et < kBN / 4) cp_async16(nbuf + (t & 1) * kBN + et * 4, xnorm + (t_begin + t) * kBN + et * 4);
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        };
+        if (n_local > 0) fetch_norms(0);
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        asm volatile("bar.sync 1, 256;" ::: "memory");
         for (int t = 0; t < n_local; ++t) {
             const int b = t & 1;
+            if (t + 1 < n_local) fetch_norms(t + 1);
             mbar_wait(&acc_full[b], (t >> 1) & 1);
             tc_fence_after();
+            const uint32_t* tn = nbuf + (t & 1) * kBN + half * 128;
             const uint64_t row0 = (t_begin + t) * kBN + uint64_t(half) * 128;
 #pragma unroll 1
             for (int c0 = 0; c0 < 128; c0 += 32) {
                 uint32_t dot[32];
                 tmem_ld32(tmem + (uint32_t(g * 32) << 16) + uint32_t(b) * kBN + uint32_t(half) * 128 + c0, dot);
-                const uint4* xn4 = reinterpret_cast<const uint4*>(xnorm + row0 + c0);
+                // Fast path (almost every column): S and one compare against
+                // the current k-th distance, no branches in the unrolled body.
+                const uint4* xn4 = reinterpret_cast<const uint4*>(tn + c0);
+                const uint32_t thr = uint32_t(top[KT - 1] >> 32);
+                uint32_t pass = 0;
 #pragma unroll
                 for (int j4 = 0; j4 < 8; ++j4) {
-                    const uint4 xv = __ldg(xn4 + j4);
+                    const uint4 xv = xn4[j4];
                     const uint32_t xs[4] = {xv.x, xv.y, xv.z, xv.w};
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
                         const int j = j4 * 4 + u;
-                        const uint64_t slot = row0 + c0 + j;
-                        const uint32_t S = qn + xs[u] - 2u * dot[j];
-                        if (S <= uint32_t(top[KT - 1] >> 32) && slot < n) {
-                            const uint64_t v = (uint64_t(S) << 32) | slot;
-                            if (v < top[KT - 1]) topk_insert<KT>(top, v);
-                        }
+                        dot[j] = qn + xs[u] - 2u * dot[j];
+                        pass |= uint32_t(dot[j] <= thr) << j;
+                    }
+                }
+                const uint64_t base = row0 + c0;  // columns past n are TMA zero fill
+                if (base >= n) pass = 0;
+                else if (n - base < 32) pass &= (1u << (n - base)) - 1u;
+                if (pass) {  // slow path: spill the distances, insert the passing ones
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) spill[j * kEpiThreads + et] = dot[j];
+#pragma unroll 1
+                    for (; pass; pass &= pass - 1) {
+                        const int j = __ffs(pass) - 1;
+                        const uint64_t v = (uint64_t(spill[j * kEpiThreads + et]) << 32) | (row0 + c0 + j);
+                        if (v < top[KT - 1]) topk_insert<KT>(top, v);
                     }
                 }
             }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&acc_empty[b]);
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+            asm volatile("bar.sync 1, 256;" ::: "memory");  // norms of t+1 visible; buffer t reusable
         }
         if (q_ok) {
             const uint64_t p = uint64_t(chunk) * 2 + uint64_t(half);
@@ -368,7 +405,7 @@ bool brute_tc_eligible(const BruteArgs& a) {
 
 size_t brute_tc_scratch_bytes(const BruteArgs& a) {
     const TcPlan p = plan(a, device_sms());
-    return size_t(p.chunks) * 2 * a.nq * a.k * 8 + size_t(p.n_pad) * 4 + 256;
+    return (((size_t(p.chunks) * 2 * a.nq * a.k) + 31) & ~size_t(31)) * 8 + size_t(p.n_pad) * 4 + 256;
 }
 
 hcg_status launch_brute_tc(const BruteArgs& a, void* scratch, uint64_t* out_ids, uint32_t* out_sqdist,
@@ -376,7 +413,7 @@ hcg_status launch_brute_tc(const BruteArgs& a, void* scratch, uint64_t* out_ids,
     const TcPlan p = plan(a, device_sms());
     uint64_t* part = static_cast<uint64_t*>(scratch);
     const size_t part_n = size_t(p.chunks) * 2 * a.nq * a.k;
-    uint32_t* xn = reinterpret_cast<uint32_t*>(part + part_n);
+    uint32_t* xn = reinterpret_cast<uint32_t*>(part + ((part_n + 31) & ~size_t(31)));  // 256-B aligned
     CUtensorMap mq, mx;
     if (!make_map(&mq, a.queries, a.nq, kBM) || !make_map(&mx, a.rows, a.n, kBN))
         return set_error(HCG_ECUDA, "brute_tc: tensor map encoding failed");
