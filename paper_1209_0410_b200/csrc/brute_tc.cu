@@ -42,8 +42,10 @@ constexpr uint32_t kBTileBytes = kBN * kRowBytes;  // 32 KB
 constexpr int kEpiThreads = 256;  // warps 4-11
 // + per-epilogue-thread spill of 32 distances for the rare insertion path
 // + the distance spill + a double buffer of row norms (one tile each)
+constexpr int kNormRing = 8;      // row-norm tiles in flight (prefetched kNormAhead tiles ahead)
+constexpr int kNormAhead = 6;
 constexpr size_t kSmemBytes = 1024 + kATileBytes + size_t(kStages) * kBTileBytes + 256 + 32 * kEpiThreads * 4 +
-                              2 * kBN * 4;
+                              size_t(kNormRing) * kBN * 4;
 
 // ---- PTX helpers (tcgen05 / TMA / mbarrier) ----
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -158,8 +160,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                const uint8_t* __restrict__ queries, const uint32_t* __restrict__ xnorm, uint32_t nq, uint64_t n,
                uint32_t k, uint32_t chunks, uint32_t tiles_per_chunk, uint64_t* __restrict__ part) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    // 1024-B alignment for SWIZZLE_128B tiles
-    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1024-B alignment for SWIZZLE_128B tiles (pointer arithmetic on the shared
+    // array keeps the address space visible to the compiler: LDS, not LD)
+    unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     unsigned char* sa = smem;
     unsigned char* sb = smem + kATileBytes;
     uint64_t* bars = reinterpret_cast<uint64_t*>(sb + size_t(kStages) * kBTileBytes);
@@ -170,7 +173,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* acc_empty = acc_full + 2;     // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
     uint32_t* spill = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(bars) + 256);  // [32][kEpiThreads]
-    uint32_t* nbuf = spill + 32 * kEpiThreads;                                                      // [2][kBN]
+    uint32_t* nbuf = spill + 32 * kEpiThreads;                                                      // [kNormRing][kBN]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t qt = blockIdx.x / chunks, chunk = blockIdx.x % chunks;
@@ -251,22 +254,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint64_t top[KT];
 #pragma unroll
         for (int i = 0; i < KT; ++i) top[i] = kNone;
-        // Row norms: the epilogue prefetches tile t+1's 256 norms (cp.async,
-        // 64 x 16 B) into a shared double buffer while it scores tile t.
+        // Row norms: the epilogue streams each tile's 256 norms (cp.async,
+        // 64 x 16 B) into a shared ring kNormAhead tiles ahead of scoring;
+        // one commit group per tile (empty past the end) keeps the counts
+        // uniform for cp.async.wait_group.
         const int et = threadIdx.x - 128;
         auto fetch_norms = [&](int t) {
-            if (et < kBN / 4) cp_async16(nbuf + (t & 1) * kBN + et * 4, xnorm + (t_begin + t) * kBN + et * 4);
+            if (t < n_local && et < kBN / 4)
+                cp_async16(nbuf + (t % kNormRing) * kBN + et * 4, xnorm + (t_begin + t) * kBN + et * 4);
             asm volatile("cp.async.commit_group;" ::: "memory");
         };
-        if (n_local > 0) fetch_norms(0);
-        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        for (int i = 0; i < kNormAhead; ++i) fetch_norms(i);
+        asm volatile("cp.async.wait_group %0;" ::"n"(kNormAhead - 1) : "memory");
         asm volatile("bar.sync 1, 256;" ::: "memory");
         for (int t = 0; t < n_local; ++t) {
             const int b = t & 1;
-            if (t + 1 < n_local) fetch_norms(t + 1);
+            fetch_norms(t + kNormAhead);  // its buffer last served tile t + kNormAhead - kNormRing < t
             mbar_wait(&acc_full[b], (t >> 1) & 1);
             tc_fence_after();
-            const uint32_t* tn = nbuf + (t & 1) * kBN + half * 128;
+            const uint32_t* tn = nbuf + (t % kNormRing) * kBN + half * 128;
             const uint64_t row0 = (t_begin + t) * kBN + uint64_t(half) * 128;
 #pragma unroll 1
             for (int c0 = 0; c0 < 128; c0 += 32) {
@@ -275,29 +281,42 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // Fast path (almost every column): S and one compare against
                 // the current k-th distance, no branches in the unrolled body.
                 const uint4* xn4 = reinterpret_cast<const uint4*>(tn + c0);
+                // t = |x|^2 - 2 q.x (S = |q|^2 + t, all < 2^31): one IMAD and
+                // one IMNMX per column; the minimum decides the slow path.
                 const uint32_t thr = uint32_t(top[KT - 1] >> 32);
-                uint32_t pass = 0;
+                const int32_t thr_t = thr == 0xFFFFFFFFu ? INT32_MAX : int32_t(thr) - int32_t(qn);
+                int32_t m8[8];  // independent partial minima: no 32-long dependency chain
 #pragma unroll
                 for (int j4 = 0; j4 < 8; ++j4) {
                     const uint4 xv = xn4[j4];
-                    const uint32_t xs[4] = {xv.x, xv.y, xv.z, xv.w};
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const int j = j4 * 4 + u;
-                        dot[j] = qn + xs[u] - 2u * dot[j];
-                        pass |= uint32_t(dot[j] <= thr) << j;
-                    }
+                    const int32_t t0 = int32_t(xv.x) - 2 * int32_t(dot[j4 * 4 + 0]);
+                    const int32_t t1 = int32_t(xv.y) - 2 * int32_t(dot[j4 * 4 + 1]);
+                    const int32_t t2 = int32_t(xv.z) - 2 * int32_t(dot[j4 * 4 + 2]);
+                    const int32_t t3 = int32_t(xv.w) - 2 * int32_t(dot[j4 * 4 + 3]);
+                    dot[j4 * 4 + 0] = uint32_t(t0);
+                    dot[j4 * 4 + 1] = uint32_t(t1);
+                    dot[j4 * 4 + 2] = uint32_t(t2);
+                    dot[j4 * 4 + 3] = uint32_t(t3);
+                    m8[j4] = min(min(t0, t1), min(t2, t3));
                 }
+                const int32_t tmin = min(min(min(m8[0], m8[1]), min(m8[2], m8[3])),
+                                         min(min(m8[4], m8[5]), min(m8[6], m8[7])));
                 const uint64_t base = row0 + c0;  // columns past n are TMA zero fill
-                if (base >= n) pass = 0;
-                else if (n - base < 32) pass &= (1u << (n - base)) - 1u;
-                if (pass) {  // slow path: spill the distances, insert the passing ones
+                if (tmin <= thr_t && base < n) {
+                    // slow path (a lane's chunk holds a new top-KT candidate; the
+                    // warp runs it when any lane does, ~40 % of chunks at k=10):
+                    // spill, then visit only the passing columns
+                    uint32_t pass = 0;
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) spill[j * kEpiThreads + et] = dot[j];
+                    for (int j = 0; j < 32; ++j) {
+                        spill[j * kEpiThreads + et] = dot[j];
+                        pass |= uint32_t(int32_t(dot[j]) <= thr_t) << j;
+                    }
+                    if (n - base < 32) pass &= (1u << (n - base)) - 1u;
 #pragma unroll 1
                     for (; pass; pass &= pass - 1) {
                         const int j = __ffs(pass) - 1;
-                        const uint64_t v = (uint64_t(spill[j * kEpiThreads + et]) << 32) | (row0 + c0 + j);
+                        const uint64_t v = (uint64_t(qn + spill[j * kEpiThreads + et]) << 32) | (base + j);
                         if (v < top[KT - 1]) topk_insert<KT>(top, v);
                     }
                 }
@@ -305,8 +324,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&acc_empty[b]);
-            asm volatile("cp.async.wait_group 0;" ::: "memory");
-            asm volatile("bar.sync 1, 256;" ::: "memory");  // norms of t+1 visible; buffer t reusable
+            asm volatile("cp.async.wait_group %0;" ::"n"(kNormAhead - 1) : "memory");
+            asm volatile("bar.sync 1, 256;" ::: "memory");  // norms of t+1 visible to all epilogue threads
         }
         if (q_ok) {
             const uint64_t p = uint64_t(chunk) * 2 + uint64_t(half);
