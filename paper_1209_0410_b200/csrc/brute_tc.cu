@@ -15,9 +15,10 @@
 //   warps 4-11 epilogue: tcgen05.ld of the accumulator (lane = query,
 //              column = row), S = |q|^2 + |x|^2 - 2 q.x, a per-thread sorted
 //              top-KT of packed (S << 32 | slot) -- the reference's (distance,
-//              id) order; warps 4-7 take columns 0-127, warps 8-11 128-255
+//              id) order; warp quad e (warps 4+4e .. 7+4e) takes columns
+//              [128e, 128e + 128) of every tile
 // Two accumulators let the epilogue of tile t overlap the MMAs of tile t+1.
-// Per-(query, chunk, column half) lists go through K4 (k_merge), as for the
+// Per-(query, chunk, column group) lists go through K4 (k_merge), as for the
 // CUDA-core K5.
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -35,11 +36,13 @@ constexpr int kBM = 128;          // queries per tile (UMMA M)
 constexpr int kBN = 256;          // rows per tile (UMMA N)
 constexpr int kRowBytes = 128;    // K: one SWIZZLE_128B atom per row
 constexpr int kStages = 4;
-constexpr int kThreads = 384;     // 12 warps
+constexpr int kEpiGroups = 2;     // epilogue warp quads; quad e scores columns [e*128, e*128+128) of a tile (4 quads: 1.2x slower)
+constexpr int kEpiCols = kBN / kEpiGroups;
+constexpr int kThreads = 128 + 128 * kEpiGroups;
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kATileBytes = kBM * kRowBytes;  // 16 KB
 constexpr uint32_t kBTileBytes = kBN * kRowBytes;  // 32 KB
-constexpr int kEpiThreads = 256;  // warps 4-11
+constexpr int kEpiThreads = 128 * kEpiGroups;  // warps 4 ..
 // + per-epilogue-thread spill of 32 distances for the rare insertion path
 // + the distance spill + a double buffer of row norms (one tile each)
 constexpr int kNormRing = 8;      // row-norm tiles in flight (prefetched kNormAhead tiles ahead)
@@ -190,7 +193,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_init(a_full, 1);
         for (int b = 0; b < 2; ++b) {
             mbar_init(&acc_full[b], 1);
-            mbar_init(&acc_empty[b], 8);  // one arrive per epilogue warp
+            mbar_init(&acc_empty[b], 4 * kEpiGroups);  // one arrive per epilogue warp
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -236,7 +239,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp >= 4) {  // ---- epilogue
-        const int ew = warp - 4, g = warp & 3, half = ew >> 2;
+        const int ew = warp - 4, g = warp & 3, half = ew >> 2;  // half: the column group
         const uint32_t q = qt * kBM + uint32_t(g * 32 + lane);
         const bool q_ok = q < nq;
         uint32_t qn = 0;
@@ -266,18 +269,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         };
         for (int i = 0; i < kNormAhead; ++i) fetch_norms(i);
         asm volatile("cp.async.wait_group %0;" ::"n"(kNormAhead - 1) : "memory");
-        asm volatile("bar.sync 1, 256;" ::: "memory");
+        asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
         for (int t = 0; t < n_local; ++t) {
             const int b = t & 1;
             fetch_norms(t + kNormAhead);  // its buffer last served tile t + kNormAhead - kNormRing < t
             mbar_wait(&acc_full[b], (t >> 1) & 1);
             tc_fence_after();
-            const uint32_t* tn = nbuf + (t % kNormRing) * kBN + half * 128;
-            const uint64_t row0 = (t_begin + t) * kBN + uint64_t(half) * 128;
+            const uint32_t* tn = nbuf + (t % kNormRing) * kBN + half * kEpiCols;
+            const uint64_t row0 = (t_begin + t) * kBN + uint64_t(half) * kEpiCols;
 #pragma unroll 1
-            for (int c0 = 0; c0 < 128; c0 += 32) {
+            for (int c0 = 0; c0 < kEpiCols; c0 += 32) {
                 uint32_t dot[32];
-                tmem_ld32(tmem + (uint32_t(g * 32) << 16) + uint32_t(b) * kBN + uint32_t(half) * 128 + c0, dot);
+                tmem_ld32(tmem + (uint32_t(g * 32) << 16) + uint32_t(b) * kBN + uint32_t(half) * kEpiCols + c0, dot);
                 // Fast path (almost every column): S and one compare against
                 // the current k-th distance, no branches in the unrolled body.
                 const uint4* xn4 = reinterpret_cast<const uint4*>(tn + c0);
@@ -325,10 +328,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&acc_empty[b]);
             asm volatile("cp.async.wait_group %0;" ::"n"(kNormAhead - 1) : "memory");
-            asm volatile("bar.sync 1, 256;" ::: "memory");  // norms of t+1 visible to all epilogue threads
+            asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");  // norms of t+1 visible to all epilogue threads
         }
         if (q_ok) {
-            const uint64_t p = uint64_t(chunk) * 2 + uint64_t(half);
+            const uint64_t p = uint64_t(chunk) * kEpiGroups + uint64_t(half);
             uint64_t* dst = part + (p * nq + q) * k;
 #pragma unroll
             for (int i = 0; i < KT; ++i)
@@ -424,14 +427,14 @@ bool brute_tc_eligible(const BruteArgs& a) {
 
 size_t brute_tc_scratch_bytes(const BruteArgs& a) {
     const TcPlan p = plan(a, device_sms());
-    return (((size_t(p.chunks) * 2 * a.nq * a.k) + 31) & ~size_t(31)) * 8 + size_t(p.n_pad) * 4 + 256;
+    return (((size_t(p.chunks) * kEpiGroups * a.nq * a.k) + 31) & ~size_t(31)) * 8 + size_t(p.n_pad) * 4 + 256;
 }
 
 hcg_status launch_brute_tc(const BruteArgs& a, void* scratch, uint64_t* out_ids, uint32_t* out_sqdist,
                            uint32_t* out_len, cudaStream_t st) {
     const TcPlan p = plan(a, device_sms());
     uint64_t* part = static_cast<uint64_t*>(scratch);
-    const size_t part_n = size_t(p.chunks) * 2 * a.nq * a.k;
+    const size_t part_n = size_t(p.chunks) * kEpiGroups * a.nq * a.k;
     uint32_t* xn = reinterpret_cast<uint32_t*>(part + ((part_n + 31) & ~size_t(31)));  // 256-B aligned
     CUtensorMap mq, mx;
     if (!make_map(&mq, a.queries, a.nq, kBM) || !make_map(&mx, a.rows, a.n, kBN))
@@ -448,7 +451,7 @@ hcg_status launch_brute_tc(const BruteArgs& a, void* scratch, uint64_t* out_ids,
     if (rc != HCG_OK) return rc;
     k_slots_to_ids<<<unsigned((part_n + 255) / 256), 256, 0, st>>>(part, part_n, a.id_base, a.id_stride);
     HCG_RET_IF(check_launch("k_slots_to_ids"));
-    return launch_merge(part, p.chunks * 2, a.nq, a.k, out_ids, out_sqdist, out_len, st);
+    return launch_merge(part, p.chunks * kEpiGroups, a.nq, a.k, out_ids, out_sqdist, out_len, st);
 }
 
 }  // namespace hcg
