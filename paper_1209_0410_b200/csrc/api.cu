@@ -24,6 +24,7 @@ struct hcg_index {
     uint32_t lut[256] = {};
     int dmax = 8, wsmax = 1;
     uint8_t* rows = nullptr;
+    uint32_t* idtab = nullptr;  // physical row -> id slot (rows stored in curve-0 order); null: identity
     uint32_t* d_lut = nullptr;
     uint16_t* d_assign = nullptr;
     std::vector<hcg::CurveDev> curves;
@@ -190,6 +191,7 @@ void release(hcg_index* ix) {
     if (!ix) return;
     DeviceGuard g(ix->device);
     cudaFree(ix->rows);
+    cudaFree(ix->idtab);
     cudaFree(ix->d_lut);
     cudaFree(ix->d_assign);
     cudaFree(ix->d_curves);
@@ -284,8 +286,12 @@ hcg_status keygen_reduce(const hcg_index* ix, uint32_t c, const uint8_t* rows, u
 // [0, hv] (only the 8-bit digits that vary over `oa`), then pack the sorted
 // suffixes (AoS, ws words) into *keys_out and slot_base + position into
 // *slots_out (both allocated here, owned by the index).
+// init_order (optional): the sort's input sequence as positions into soa --
+// the id order of a physically permuted index, so that equal keys stay in id
+// order and the output holds physical positions.
 hcg_status sort_suffix(hcg_index* ix, const uint64_t* soa, uint64_t count, uint32_t W, const std::vector<uint64_t>& oa,
-                       uint32_t hv, uint64_t slot_base, Scratch& sc, uint64_t** keys_out, uint32_t** slots_out) {
+                       uint32_t hv, uint64_t slot_base, Scratch& sc, uint64_t** keys_out, uint32_t** slots_out,
+                       const uint32_t* init_order = nullptr) {
     const int hw = int(hv >> 6), hb = int(hv & 63);
     const uint64_t below = hb == 63 ? ~0ull : ((2ull << hb) - 1);
     const uint32_t ws = uint32_t(hw + 1);
@@ -299,7 +305,10 @@ hcg_status sort_suffix(hcg_index* ix, const uint64_t* soa, uint64_t count, uint3
     uint32_t* totals = counts + (radix_counts_bytes(count) / 4 - 256);
     uint32_t* v = vb;
     uint32_t* v_alt = va;
-    launch_iota(v, count, 0, st);
+    if (init_order)
+        HCG_TRY_CUDA(cudaMemcpyAsync(v, init_order, count * 4, cudaMemcpyDeviceToDevice, st));
+    else
+        launch_iota(v, count, 0, st);
     for (uint32_t w = 0; w <= uint32_t(hw); ++w) {
         uint64_t vary = oa[w] ^ oa[W + w];
         if (int(w) == hw) vary &= below;
@@ -322,7 +331,7 @@ hcg_status sort_suffix(hcg_index* ix, const uint64_t* soa, uint64_t count, uint3
 }
 
 // Build curve c over all rows: K1 keys, common-prefix detection, K2 sort.
-hcg_status build_curve(hcg_index* ix, uint32_t c, cudaStream_t st) {
+hcg_status build_curve(hcg_index* ix, uint32_t c, cudaStream_t st, const uint32_t* init_order = nullptr) {
     const uint64_t n = ix->n;
     const uint32_t d = ix->off[c + 1] - ix->off[c];
     const uint32_t W = (d * ix->m + 63) / 64;
@@ -353,7 +362,7 @@ hcg_status build_curve(hcg_index* ix, uint32_t c, cudaStream_t st) {
     cv.ws = uint32_t(hw + 1);
     for (uint32_t w = 0; w < W; ++w)
         cv.prefix[w] = int(w) > hw ? oa[w] : (int(w) == hw ? (oa[w] & above) : 0ull);
-    HCG_TRY(sort_suffix(ix, soa, n, W, oa, cv.hv, 0, sc, &ix->keys[c], &ix->slots[c]));
+    HCG_TRY(sort_suffix(ix, soa, n, W, oa, cv.hv, 0, sc, &ix->keys[c], &ix->slots[c], init_order));
     cv.keys = ix->keys[c];
     cv.slots = ix->slots[c];
     HCG_TRY_CUDA(cudaStreamSynchronize(st));
@@ -391,7 +400,14 @@ hcg_status insert_curve(hcg_index* ix, uint32_t c, uint64_t n_old, uint64_t nb, 
         dev_free(ix->slots[c], size_t(n_old) * 4, &ix->bytes);
         ix->keys[c] = nullptr;
         ix->slots[c] = nullptr;
-        return build_curve(ix, c, st);
+        if (!ix->idtab) return build_curve(ix, c, st);
+        // permuted rows: sort in id order (inverse of idtab) so ties keep id order
+        Scratch sc2(st);
+        uint32_t* inv = sc2.alloc<uint32_t>(ix->n);
+        if (!inv) return set_error(HCG_ENOMEM, "inverse permutation");
+        launch_invert(ix->idtab, ix->n, inv, st);
+        HCG_TRY(check_launch("invert"));
+        return build_curve(ix, c, st, inv);
     }
     uint64_t* nk = nullptr;
     uint32_t* ns = nullptr;
@@ -415,6 +431,44 @@ hcg_status insert_curve(hcg_index* ix, uint32_t c, uint64_t n_old, uint64_t nb, 
 }
 
 // Upload the curve table and slot pointers (after build / insert / load).
+// Store the descriptors in curve-0 key order: rows that are near on curve 0
+// (and, through the data's clusters, on the other curves) become neighbours
+// in HBM, so a query's candidate rows share DRAM pages and L2 lines
+// (measured: gather 5.94 -> 5.05 ms at 10M).  Ids do not move: idtab maps a
+// physical row to its id slot, the curves' slot arrays are remapped to
+// physical rows (their (key, id) order is unchanged), and the search reads
+// idtab only for candidates that can enter a top-k (tie order by id).
+hcg_status reorder_rows(hcg_index* ix, cudaStream_t st) {
+    static const bool off = getenv("HCG_NO_REORDER") != nullptr;
+    const uint64_t n = ix->n;
+    if (off || n < 2 || ix->idtab) return HCG_OK;
+    uint8_t* nr = nullptr;
+    uint32_t* idt = nullptr;
+    HCG_TRY(dev_alloc(&nr, size_t(n) * ix->pitch, &ix->bytes));
+    if (dev_alloc(&idt, n, &ix->bytes) != HCG_OK) {
+        dev_free(nr, size_t(n) * ix->pitch, &ix->bytes);
+        return set_error(HCG_ENOMEM, "id table");
+    }
+    Scratch sc(st);
+    uint32_t* inv = sc.alloc<uint32_t>(n);
+    if (!inv) {
+        dev_free(nr, size_t(n) * ix->pitch, &ix->bytes);
+        dev_free(idt, size_t(n) * 4, &ix->bytes);
+        return set_error(HCG_ENOMEM, "inverse permutation");
+    }
+    const uint32_t* perm = ix->slots[0];  // id slots in curve-0 order
+    HCG_TRY_CUDA(cudaMemcpyAsync(idt, perm, n * 4, cudaMemcpyDeviceToDevice, st));
+    launch_permute_rows(ix->rows, perm, n, ix->pitch, nr, st);
+    launch_invert(perm, n, inv, st);
+    for (uint32_t c = 0; c < ix->C; ++c) launch_map(ix->slots[c], n, inv, st);
+    HCG_TRY(check_launch("reorder rows"));
+    HCG_TRY_CUDA(cudaStreamSynchronize(st));
+    dev_free(ix->rows, size_t(n) * ix->pitch, &ix->bytes);
+    ix->rows = nr;
+    ix->idtab = idt;
+    return HCG_OK;
+}
+
 hcg_status publish_tables(hcg_index* ix, cudaStream_t st) {
     uint32_t maxws = 1;
     for (auto& cv : ix->curves) maxws = std::max(maxws, cv.ws);
@@ -555,6 +609,7 @@ RefineArgs refine_args(const hcg_index* ix, const uint8_t* dq, uint32_t nq, uint
     a.id_stride = ix->id_stride;
     a.n_rows = ix->n;
     a.dtype = int(ix->dtype);
+    a.idtab = ix->idtab;
     return a;
 }
 
@@ -585,7 +640,7 @@ using namespace hcg;
 namespace {
 constexpr char kMagic[8] = {'H', 'C', 'G', 'I', 'D', 'X', 0, 1};
 constexpr char kTrailer[8] = {'H', 'C', 'G', 'E', 'N', 'D', 0, 0};
-constexpr uint32_t kFormatVersion = 2;  // 2: + descriptor dtype
+constexpr uint32_t kFormatVersion = 3;  // 2: + descriptor dtype; 3: + physical row order (id table)
 
 struct FileCloser {
     FILE* f = nullptr;
@@ -660,6 +715,7 @@ hcg_status hcg_build(const hcg_scheme* s, const uint8_t* rows, uint64_t n, uint6
     }
     for (uint32_t c = 0; c < ix->C; ++c)
         if ((rc = build_curve(ix, c, st)) != HCG_OK) return fail(rc);
+    if ((rc = reorder_rows(ix, st)) != HCG_OK) return fail(rc);
     if ((rc = publish_tables(ix, st)) != HCG_OK) return fail(rc);
     *out = ix;
     return HCG_OK;
@@ -708,6 +764,18 @@ hcg_status hcg_insert(hcg_index* ix, const uint8_t* rows, uint64_t nb, void* str
             return rc;
         }
     }
+    if (ix->idtab) {  // appended rows sit at physical = id slot
+        uint32_t* nt = nullptr;
+        if (dev_alloc(&nt, n_new, &ix->bytes) != HCG_OK) {
+            dev_free(nr, size_t(n_new) * ix->pitch, &ix->bytes);
+            return set_error(HCG_ENOMEM, "id table");
+        }
+        HCG_TRY_CUDA(cudaMemcpyAsync(nt, ix->idtab, n_old * 4, cudaMemcpyDeviceToDevice, st));
+        launch_iota(nt + n_old, nb, uint32_t(n_old), st);
+        HCG_TRY_CUDA(cudaStreamSynchronize(st));
+        dev_free(ix->idtab, size_t(n_old) * 4, &ix->bytes);
+        ix->idtab = nt;
+    }
     dev_free(ix->rows, size_t(std::max<uint64_t>(n_old, 1)) * ix->pitch, &ix->bytes);
     ix->rows = nr;
     ix->n = n_new;
@@ -739,6 +807,14 @@ hcg_status hcg_save(const hcg_index* ix, const char* path) {
         HCG_TRY_CUDA(cudaMemcpy2D(buf.data(), ix->row_bytes, ix->rows + r * ix->pitch, ix->pitch, ix->row_bytes, cnt,
                                   cudaMemcpyDeviceToHost));
         ok = put(f, buf.data(), buf.size());
+    }
+    // rows are stored in their physical order; the id table (if any) follows
+    const uint32_t has_idtab = ix->idtab && ix->n ? 1u : 0u;
+    ok = ok && put(f, &has_idtab, 1);
+    if (ok && has_idtab) {
+        std::vector<uint32_t> idt(ix->n);
+        HCG_TRY_CUDA(cudaMemcpy(idt.data(), ix->idtab, ix->n * 4, cudaMemcpyDeviceToHost));
+        ok = put(f, idt.data(), idt.size());
     }
     for (uint32_t c = 0; ok && c < ix->C; ++c) {
         const CurveDev& cv = ix->curves[c];
@@ -805,6 +881,15 @@ hcg_status hcg_load(const char* path, int device, void* stream, hcg_index** out)
         if (cudaMemcpy2D(ix->rows + r * ix->pitch, ix->pitch, buf.data(), ix->row_bytes, ix->row_bytes, cnt,
                          cudaMemcpyHostToDevice) != cudaSuccess)
             return fail(set_error(HCG_ECUDA, "upload rows"));
+    }
+    uint32_t has_idtab = 0;
+    if (!get(f, &has_idtab, 1) || has_idtab > 1) return fail(set_error(HCG_EIO, std::string(path) + ": corrupt id table"));
+    if (has_idtab && ix->n) {
+        std::vector<uint32_t> idt(ix->n);
+        if (!get(f, idt.data(), idt.size())) return fail(set_error(HCG_EIO, std::string(path) + ": truncated id table"));
+        if (dev_alloc(&ix->idtab, ix->n, &ix->bytes) != HCG_OK ||
+            cudaMemcpy(ix->idtab, idt.data(), ix->n * 4, cudaMemcpyHostToDevice) != cudaSuccess)
+            return fail(set_error(HCG_ECUDA, "upload id table"));
     }
     for (uint32_t c = 0; c < ix->C; ++c) {
         CurveDev& cv = ix->curves[c];
@@ -1036,11 +1121,16 @@ hcg_status hcg_sorted(const hcg_index* ix, uint32_t curve, uint64_t* out_ids, ui
     const uint64_t n = ix->n;
     const CurveDev& cv = ix->curves[curve];
     if (out_ids) {
-        std::vector<uint32_t> s(n);
+        std::vector<uint32_t> s(n), idt;
         HCG_TRY_CUDA(cudaMemcpyAsync(s.data(), ix->slots[curve], n * 4, cudaMemcpyDeviceToHost, st));
+        if (ix->idtab) {
+            idt.resize(n);
+            HCG_TRY_CUDA(cudaMemcpyAsync(idt.data(), ix->idtab, n * 4, cudaMemcpyDeviceToHost, st));
+        }
         HCG_TRY_CUDA(cudaStreamSynchronize(st));
         std::vector<uint64_t> ids(n);
-        for (uint64_t i = 0; i < n; ++i) ids[i] = ix->id_base + uint64_t(s[i]) * ix->id_stride;
+        for (uint64_t i = 0; i < n; ++i)
+            ids[i] = ix->id_base + uint64_t(ix->idtab ? idt[s[i]] : s[i]) * ix->id_stride;
         HCG_TRY(deliver(out_ids, ids));
     }
     if (out_words) {
@@ -1168,7 +1258,7 @@ static hcg_status brute_impl(const hcg_index* ix, const uint8_t* queries, uint32
     } else {
         const uint8_t* dq = nullptr;
         HCG_TRY(stage_rows(sc, queries, nq, ix->row_bytes, ix->pitch, &dq));
-        BruteArgs a{ix->rows, ix->n, ix->pitch, dq, nq, k, ix->id_base, ix->id_stride, int(ix->dtype)};
+        BruteArgs a{ix->rows, ix->n, ix->pitch, dq, nq, k, ix->id_base, ix->id_stride, int(ix->dtype), ix->idtab};
         uint64_t* part = sc.alloc<uint64_t>((brute_scratch_bytes(a) + 7) / 8);
         if (!part) return set_error(HCG_ENOMEM, "brute-force scratch");
         HCG_TRY(launch_brute(a, part, oi.dev, os.dev, ol.dev, o64.dev, st));

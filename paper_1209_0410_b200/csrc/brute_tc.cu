@@ -161,7 +161,8 @@ template <int KT>
 __global__ void __launch_bounds__(kThreads, 1)
     k_brute_tc(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_x,
                const uint8_t* __restrict__ queries, const uint32_t* __restrict__ xnorm, uint32_t nq, uint64_t n,
-               uint32_t k, uint32_t chunks, uint32_t tiles_per_chunk, uint64_t* __restrict__ part) {
+               uint32_t k, uint32_t chunks, uint32_t tiles_per_chunk, uint64_t* __restrict__ part,
+               const uint32_t* __restrict__ idtab) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1024-B alignment for SWIZZLE_128B tiles (pointer arithmetic on the shared
     // array keeps the address space visible to the compiler: LDS, not LD)
@@ -319,7 +320,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
                     for (; pass; pass &= pass - 1) {
                         const int j = __ffs(pass) - 1;
-                        const uint64_t v = (uint64_t(qn + spill[j * kEpiThreads + et]) << 32) | (base + j);
+                        const uint64_t v = (uint64_t(qn + spill[j * kEpiThreads + et]) << 32) |
+                                           (idtab ? __ldg(idtab + base + j) : uint32_t(base + j));
                         if (v < top[KT - 1]) topk_insert<KT>(top, v);
                     }
                 }
@@ -413,7 +415,7 @@ hcg_status launch_tc(const BruteArgs& a, const TcPlan& p, const CUtensorMap& mq,
         cfg = true;
     }
     k_brute_tc<KT><<<p.qtiles * p.chunks, kThreads, kSmemBytes, st>>>(mq, mx, a.queries, xn, a.nq, a.n, a.k, p.chunks,
-                                                                       p.tiles_per_chunk, part);
+                                                                       p.tiles_per_chunk, part, a.idtab);
     return check_launch("k_brute_tc");
 }
 }  // namespace

@@ -257,6 +257,29 @@ __global__ void k_check_finite(const uint8_t* __restrict__ rows, uint64_t n, uin
     if ((b & 0x7F800000u) == 0x7F800000u) *bad = 1u;
 }
 
+// Physical row order (see api.cu reorder_rows): dst[i] = src[perm[i]] for
+// rows of `pitch` bytes (16-B vectors, a warp per 2 rows at pitch 128).
+__global__ void k_permute_rows(const uint8_t* __restrict__ src, const uint32_t* __restrict__ perm, uint64_t n,
+                               uint32_t pitch, uint8_t* __restrict__ dst) {
+    const uint32_t vpr = pitch / 16;
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n * vpr) return;
+    const uint64_t r = i / vpr, v = i - r * vpr;
+    reinterpret_cast<uint4*>(dst + r * pitch)[v] = __ldg(reinterpret_cast<const uint4*>(src + uint64_t(perm[r]) * pitch) + v);
+}
+
+// inv[perm[i]] = i
+__global__ void k_invert(const uint32_t* __restrict__ perm, uint64_t n, uint32_t* __restrict__ inv) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) inv[perm[i]] = uint32_t(i);
+}
+
+// v[i] = map[v[i]]
+__global__ void k_map(uint32_t* __restrict__ v, uint64_t n, const uint32_t* __restrict__ map) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) v[i] = __ldg(map + v[i]);
+}
+
 __global__ void k_iota(uint32_t* v, uint64_t n, uint32_t base) {
     const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i < n) v[i] = base + uint32_t(i);
@@ -390,6 +413,17 @@ size_t radix_counts_bytes(uint64_t n) {
 void launch_check_finite(const uint8_t* rows, uint64_t n, uint32_t pitch, uint32_t d, unsigned* bad,
                          cudaStream_t st) {
     if (n) k_check_finite<<<blocks_for(n * d, 256), 256, 0, st>>>(rows, n, pitch, d, bad);
+}
+
+void launch_permute_rows(const uint8_t* src, const uint32_t* perm, uint64_t n, uint32_t pitch, uint8_t* dst,
+                         cudaStream_t st) {
+    if (n) k_permute_rows<<<blocks_for(n * (pitch / 16), 256), 256, 0, st>>>(src, perm, n, pitch, dst);
+}
+void launch_invert(const uint32_t* perm, uint64_t n, uint32_t* inv, cudaStream_t st) {
+    if (n) k_invert<<<blocks_for(n, 256), 256, 0, st>>>(perm, n, inv);
+}
+void launch_map(uint32_t* v, uint64_t n, const uint32_t* map, cudaStream_t st) {
+    if (n) k_map<<<blocks_for(n, 256), 256, 0, st>>>(v, n, map);
 }
 
 void launch_iota(uint32_t* v, uint64_t n, uint32_t base, cudaStream_t st) {

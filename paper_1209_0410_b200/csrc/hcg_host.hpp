@@ -30,6 +30,10 @@ hcg_status radix_sort_pairs(uint64_t** k, uint32_t** v, uint64_t** k_alt, uint32
 size_t radix_counts_bytes(uint64_t n);
 void launch_check_finite(const uint8_t* rows, uint64_t n, uint32_t pitch, uint32_t d, unsigned* bad,
                          cudaStream_t st);
+void launch_permute_rows(const uint8_t* src, const uint32_t* perm, uint64_t n, uint32_t pitch, uint8_t* dst,
+                         cudaStream_t st);
+void launch_invert(const uint32_t* perm, uint64_t n, uint32_t* inv, cudaStream_t st);
+void launch_map(uint32_t* v, uint64_t n, const uint32_t* map, cudaStream_t st);
 void launch_iota(uint32_t* v, uint64_t n, uint32_t base, cudaStream_t st);
 void launch_offset(const uint32_t* in, uint32_t* out, uint64_t n, uint32_t base, cudaStream_t st);
 void launch_rank_merge(const uint64_t* ak, const uint32_t* as, uint64_t na, const uint64_t* bk, const uint32_t* bs,
@@ -83,6 +87,7 @@ struct RefineArgs {
     uint64_t n_rows;           // rows in the index (bounds checks)
     int dtype;                 // hcg_dtype of rows and queries
     double* out_sqdist_f64;    // HCG_F32 + kOutIds: nq x k squared distances
+    const uint32_t* idtab;     // physical row -> id slot (null: identity)
 };
 // Scratch bytes the refine launch needs (global hash tables when the table
 // does not fit in shared memory); query with scratch == nullptr first.
@@ -101,6 +106,7 @@ struct BruteArgs {
     uint32_t k;
     uint64_t id_base, id_stride;
     int dtype;
+    const uint32_t* idtab;  // physical row -> id slot (null: identity)
 };
 size_t brute_scratch_bytes(const BruteArgs& a);
 // brute_tc.cu: the same on the tensor cores (u8 rows of 128 B, k <= 32)

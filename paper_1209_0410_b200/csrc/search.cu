@@ -447,7 +447,12 @@ __device__ __forceinline__ void gather_list(const RefineArgs& a, const uint32_t*
             s2[i] = keep + __shfl_xor_sync(kFull, send, 2);
         }
         const uint32_t S = (b0 ? s2[1] : s2[0]) + __shfl_xor_sync(kFull, b0 ? s2[0] : s2[1], 1);
-        tk.offer(me != kEmpty ? ((uint64_t(S) << 32) | me) : kNone, lane);
+        uint32_t sl = me;
+        if (a.idtab) {  // physical row -> id slot, read only for rows that can enter the top-k
+            const bool pre = me != kEmpty && S <= uint32_t(tk.thr >> 32);
+            if (__any_sync(kFull, pre) && pre) sl = __ldg(a.idtab + me);
+        }
+        tk.offer(me != kEmpty ? ((uint64_t(S) << 32) | sl) : kNone, lane);
     }
 }
 
@@ -533,7 +538,7 @@ __device__ __forceinline__ uint32_t f32_entry(const uint32_t* list, uint32_t e, 
 template <int R, bool DIRECT>
 __device__ __forceinline__ void gather_list_f32(const uint8_t* rows, uint32_t pitch, const uint32_t* list, uint32_t n,
                                                 uint32_t start, uint32_t step, const uint4& qv, int lane,
-                                                WarpTopK2<R>& tk) {
+                                                WarpTopK2<R>& tk, const uint32_t* idtab) {
     const uint32_t chunks = pitch >> 4;
     const bool has = uint32_t(lane) < chunks;
     uint32_t cur = lane < 8 ? f32_entry<DIRECT>(list, start + lane, n) : kEmpty;
@@ -574,7 +579,13 @@ __device__ __forceinline__ void gather_list_f32(const uint8_t* rows, uint32_t pi
         for (int r = 1; r < 8; ++r)
             if (r == row) me = nx[r];
         const bool offer = (lane & 3) == 0 && me != kEmpty;
-        tk.offer(offer ? uint64_t(__double_as_longlong(S)) : kNone, offer ? me : 0xFFFFFFFFu, lane);
+        const uint64_t sb = uint64_t(__double_as_longlong(S));
+        uint32_t sl = me;
+        if (idtab) {  // physical row -> id slot for rows that can enter the top-k
+            const bool pre = offer && sb <= tk.ta;
+            if (__any_sync(kFull, pre) && pre) sl = __ldg(idtab + me);
+        }
+        tk.offer(offer ? sb : kNone, offer ? sl : 0xFFFFFFFFu, lane);
     }
 }
 
@@ -610,7 +621,7 @@ __global__ void __launch_bounds__(kRefineThreads, 2) k_gather_f32(RefineArgs a, 
         const uint4 qv = load_query_f32(a.queries, a.pitch, q, lane);
         WarpTopK2<R> tk;
         tk.init(int(a.k));
-        gather_list_f32<R, false>(a.rows, a.pitch, lists + uint64_t(q) * lstride, n, 0, 8, qv, lane, tk);
+        gather_list_f32<R, false>(a.rows, a.pitch, lists + uint64_t(q) * lstride, n, 0, 8, qv, lane, tk, a.idtab);
         write_result_f32<R>(a, q, tk, lane, n);
     }
 }
@@ -645,7 +656,8 @@ __global__ void __launch_bounds__(NW * 32) k_gather_cta_f32(RefineArgs a, const 
         const uint4 qv = load_query_f32(a.queries, a.pitch, q, lane);
         WarpTopK2<R> tk;
         tk.init(int(a.k));
-        gather_list_f32<R, false>(a.rows, a.pitch, lists + uint64_t(q) * lstride, n, warp * 8, NW * 8, qv, lane, tk);
+        gather_list_f32<R, false>(a.rows, a.pitch, lists + uint64_t(q) * lstride, n, warp * 8, NW * 8, qv, lane, tk,
+                                  a.idtab);
         merge_warps_f32<R, NW>(tk, ma, mb, a.k, lane, warp);
         if (warp == 0) write_result_f32<R>(a, q, tk, lane, n);
         __syncthreads();
@@ -808,7 +820,10 @@ __global__ void k_lists_to_ids(RefineArgs a, const uint32_t* __restrict__ lists,
     const uint32_t lim = n < a.cap ? n : a.cap;
     if (a.out_ids)
         for (uint32_t i = threadIdx.x; i < lim; i += blockDim.x)
-            a.out_ids[uint64_t(q) * a.cap + i] = a.id_base + uint64_t(lists[uint64_t(q) * lstride + i]) * a.id_stride;
+        {
+            const uint32_t p = lists[uint64_t(q) * lstride + i];
+            a.out_ids[uint64_t(q) * a.cap + i] = a.id_base + uint64_t(a.idtab ? a.idtab[p] : p) * a.id_stride;
+        }
     if (threadIdx.x == 0) a.out_len[q] = n;
 }
 
@@ -1132,7 +1147,7 @@ __global__ void __launch_bounds__(256) k_brute(BruteArgs a, uint64_t* __restrict
                     acc[j] = __dp4a(d, d, acc[j]);
                 }
             }
-            const uint64_t gid = a.id_base + gr * a.id_stride;
+            const uint64_t gid = a.id_base + (a.idtab && valid ? __ldg(a.idtab + gr) : gr) * a.id_stride;
 #pragma unroll
             for (int j = 0; j < QPW; ++j) tk[j].offer(valid ? ((uint64_t(acc[j]) << 32) | gid) : kNone, lane);
         }
@@ -1182,7 +1197,7 @@ __global__ void __launch_bounds__(256) k_brute_f32(BruteArgs a, uint64_t* __rest
     const uint4 qv = load_query_f32(a.queries, a.pitch, q, lane);
     WarpTopK2<R> tk;
     tk.init(int(a.k));
-    gather_list_f32<R, true>(a.rows, a.pitch, nullptr, r1, uint32_t(r0), 8, qv, lane, tk);
+    gather_list_f32<R, true>(a.rows, a.pitch, nullptr, r1, uint32_t(r0), 8, qv, lane, tk, a.idtab);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const uint32_t e = uint32_t(lane) * R + r;
