@@ -25,7 +25,6 @@ struct hcg_index {
     int dmax = 8, wsmax = 1;
     uint8_t* rows = nullptr;
     uint32_t* idtab = nullptr;  // physical row -> id slot (rows stored in curve-0 order); null: identity
-    bool c0_iota = false;       // curve 0's slots are 0..n-1 (true from the reorder until an insert)
     uint32_t* d_lut = nullptr;
     uint16_t* d_assign = nullptr;
     std::vector<hcg::CurveDev> curves;
@@ -467,7 +466,6 @@ hcg_status reorder_rows(hcg_index* ix, cudaStream_t st) {
     dev_free(ix->rows, size_t(n) * ix->pitch, &ix->bytes);
     ix->rows = nr;
     ix->idtab = idt;
-    ix->c0_iota = true;
     return HCG_OK;
 }
 
@@ -612,8 +610,6 @@ RefineArgs refine_args(const hcg_index* ix, const uint8_t* dq, uint32_t nq, uint
     a.n_rows = ix->n;
     a.dtype = int(ix->dtype);
     a.idtab = ix->idtab;
-    static const bool no_c0 = getenv("HCG_NO_C0") != nullptr;
-    a.c0_iota = ix->c0_iota && !no_c0;
     return a;
 }
 
@@ -743,7 +739,6 @@ hcg_status hcg_insert(hcg_index* ix, const uint8_t* rows, uint64_t nb, void* str
     const uint64_t n_old = ix->n, n_new = n_old + nb;
     if (n_new >= (1ull << 32)) return set_error(HCG_ECAPACITY, "more than 2^32-1 rows in one index");
     DeviceGuard g(ix->device);
-    ix->c0_iota = false;  // appended rows break curve 0's identity order
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     uint8_t* nr = nullptr;
     HCG_TRY(dev_alloc(&nr, size_t(n_new) * ix->pitch, &ix->bytes));
@@ -815,8 +810,7 @@ hcg_status hcg_save(const hcg_index* ix, const char* path) {
     }
     // rows are stored in their physical order; the id table (if any) follows
     const uint32_t has_idtab = ix->idtab && ix->n ? 1u : 0u;
-    const uint32_t order_flags = has_idtab | (has_idtab && ix->c0_iota ? 2u : 0u);
-    ok = ok && put(f, &order_flags, 1);
+    ok = ok && put(f, &has_idtab, 1);
     if (ok && has_idtab) {
         std::vector<uint32_t> idt(ix->n);
         HCG_TRY_CUDA(cudaMemcpy(idt.data(), ix->idtab, ix->n * 4, cudaMemcpyDeviceToHost));
@@ -888,10 +882,8 @@ hcg_status hcg_load(const char* path, int device, void* stream, hcg_index** out)
                          cudaMemcpyHostToDevice) != cudaSuccess)
             return fail(set_error(HCG_ECUDA, "upload rows"));
     }
-    uint32_t order_flags = 0;
-    if (!get(f, &order_flags, 1) || order_flags > 3) return fail(set_error(HCG_EIO, std::string(path) + ": corrupt id table"));
-    const uint32_t has_idtab = order_flags & 1u;
-    ix->c0_iota = has_idtab && (order_flags & 2u);
+    uint32_t has_idtab = 0;
+    if (!get(f, &has_idtab, 1) || has_idtab > 1) return fail(set_error(HCG_EIO, std::string(path) + ": corrupt id table"));
     if (has_idtab && ix->n) {
         std::vector<uint32_t> idt(ix->n);
         if (!get(f, idt.data(), idt.size())) return fail(set_error(HCG_EIO, std::string(path) + ": truncated id table"));

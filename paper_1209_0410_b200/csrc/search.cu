@@ -710,30 +710,8 @@ __global__ void __launch_bounds__(NT, MINB) k_union_reg(RefineArgs a, uint32_t* 
         // (the previous query's scan barriers ordered every read of tab / wsum)
         const uint32_t qq = a.qorder ? __ldg(a.qorder + q) : q;  // list q holds query qq
         uint32_t id[JMAX];
-        uint32_t pending = 0, keep = 0;
-        if (layout == 0 && a.c0_iota) {
-            // Rows stored in curve-0 order: curve 0's window is the physical
-            // range [b0, b0 + take) -- kept without hashing -- and any other
-            // curve's id inside it is a duplicate, dropped without hashing.
-            const uint32_t c = warp % a.C, step = 32 * (kWarps / a.C);
-            const uint32_t b0 = __ldg(a.begins + uint64_t(qq) * a.C);
-            const uint32_t* src = sptr[c] + __ldg(a.begins + uint64_t(qq) * a.C + c);
-            uint32_t p = lane + 32 * (warp / a.C);
-#pragma unroll
-            for (int j = 0; j < JMAX; ++j) {
-                id[j] = 0;
-                if (p < take) {
-                    if (c == 0) {
-                        id[j] = b0 + p;
-                        keep |= 1u << j;
-                    } else {
-                        id[j] = __ldg(src + p);
-                        if (id[j] - b0 >= take) pending |= 1u << j;
-                    }
-                }
-                p += step;
-            }
-        } else if (layout == 0) {
+        uint32_t pending = 0;
+        if (layout == 0) {
             const uint32_t c = warp % a.C, step = 32 * (kWarps / a.C);
             const uint32_t* src = sptr[c] + __ldg(a.begins + uint64_t(qq) * a.C + c);
             uint32_t p = lane + 32 * (warp / a.C);
@@ -781,6 +759,7 @@ __global__ void __launch_bounds__(NT, MINB) k_union_reg(RefineArgs a, uint32_t* 
                 }
             }
         }
+        uint32_t keep = 0;
         bool left = true;
 #pragma unroll 1
         for (int r = 0; r < kRegRounds && left; ++r) {
