@@ -253,3 +253,19 @@ def test_host_pipeline_matches_direct_search():
         np.testing.assert_array_equal(ids.numpy(), wi)
         np.testing.assert_array_equal(sq.numpy(), ws)
         np.testing.assert_array_equal(ln.numpy(), wl)
+
+
+@pytest.mark.parametrize("view,m", VIEWS, ids=["raw", "lifted"])
+@pytest.mark.parametrize("k", [1, 10, 32])
+def test_large_batch_paths(view, m, k):
+    """Batches large enough for the warp-per-query gather, the curve-0 batch
+    order and (k <= 32, 128-B rows) the row-sketch filter: bit-exact vs the
+    oracle, ties included (duplicated rows)."""
+    n, nq = 30_000, 20_000
+    rows = P.gen_rows(0, n)
+    rows[1000:1100] = rows[5]  # exact ties
+    qs = P.gen_queries(0, nq, n)
+    qs[:50] = rows[5]
+    gi = H.MulticurvesIndex(rows, H.default_scheme(128, 8, m), view)
+    oi = _oracle(rows, view, 8, m, H.HILBERT)
+    _check_search(gi, oi, view, qs, k, 350)
