@@ -269,3 +269,38 @@ def test_large_batch_paths(view, m, k):
     gi = H.MulticurvesIndex(rows, H.default_scheme(128, 8, m), view)
     oi = _oracle(rows, view, 8, m, H.HILBERT)
     _check_search(gi, oi, view, qs, k, 350)
+
+
+def test_concurrent_searches_from_threads():
+    """search is const and may run concurrently -- four host
+    threads, each on its own CUDA stream, get the single-threaded results."""
+    import threading
+    import torch
+    rows = P.gen_rows(0, 20_000)
+    qs = P.gen_queries(0, 80_000, 20_000)  # 20K per thread: warp-per-query gather + batch order
+    gi = H.MulticurvesIndex(rows, H.default_scheme(128, 8, 16), H.LIFTED)
+    want = [gi.search_batch(qs[i::4], 10, 200) for i in range(4)]
+    got = [None] * 4
+    errors = []
+
+    def work(i):
+        try:
+            st = torch.cuda.Stream()
+            q = torch.from_numpy(np.ascontiguousarray(qs[i::4])).cuda()
+            for _ in range(3):
+                with torch.cuda.stream(st):
+                    out = gi.search_batch(q, 10, 200, stream=st)
+            st.synchronize()
+            got[i] = tuple(t.cpu().numpy() for t in out)
+        except Exception as e:  # surfaced below
+            errors.append(e)
+
+    threads = [threading.Thread(target=work, args=(i,)) for i in range(4)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    for i in range(4):
+        for a, b in zip(got[i], want[i]):
+            np.testing.assert_array_equal(a, b)
