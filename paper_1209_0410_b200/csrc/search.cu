@@ -974,7 +974,8 @@ hcg_status refine_dispatch(const RefineArgs& a_in, void* scratch, size_t* scratc
     const uint32_t utb = std::min<uint32_t>(tb + 1, 16);
     const size_t usmem = union_smem_bytes(a_in.C, T, utb);
     const bool smem_union = T <= kUnionMaxT && usmem <= 160 * 1024;
-    const bool reg_union = T <= 32u * 256 && (size_t(8) << tb) <= 128 * 1024 && !getenv("HCG_UNION_SMEM");
+    static const bool force_smem_union = getenv("HCG_UNION_SMEM") != nullptr;
+    const bool reg_union = T <= 32u * 256 && (size_t(8) << tb) <= 128 * 1024 && !force_smem_union;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     const uint32_t chunk = uint32_t(std::max<size_t>(1, std::min<size_t>(a_in.nq, kListBudget / (size_t(lstride) * 4))));
@@ -1030,8 +1031,7 @@ hcg_status refine_dispatch(const RefineArgs& a_in, void* scratch, size_t* scratc
         if (a.out_len) a.out_len += q0;
         if (a.out_packed) a.out_packed += uint64_t(q0) * a_in.k;
         if (reg_union) {
-            static const int tb_extra = getenv("HCG_UNION_TB_EXTRA") ? atoi(getenv("HCG_UNION_TB_EXTRA")) : 0;
-            HCG_RET_IF(launch_union_reg(a, lists, counts, lstride, tb + uint32_t(tb_extra), device, st));
+            HCG_RET_IF(launch_union_reg(a, lists, counts, lstride, tb, device, st));
         } else if (smem_union) {
             const uint32_t ugrid = persistent_grid(reinterpret_cast<const void*>(k_union), usmem, device, a.nq);
             k_union<<<ugrid, kRefineThreads, usmem, st>>>(a, lists, counts, lstride, utb);
