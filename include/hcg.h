@@ -134,6 +134,8 @@ uint32_t hcg_key_words(const hcg_index* index, uint32_t curve);
 /* Device bytes owned by the index. */
 uint64_t hcg_device_bytes(const hcg_index* index);
 uint32_t hcg_index_dtype(const hcg_index* index); /* hcg_dtype of the rows */
+/* Kernels this library has launched (searches, merges, sorts), for launch accounting. */
+uint64_t hcg_launch_count(void);
 
 /* Batched search: for each of nq queries (nq x d_full bytes) the top-k of the
  * deduplicated union of every curve's probe-depth window, ordered by

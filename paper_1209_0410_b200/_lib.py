@@ -36,7 +36,7 @@ EXPORTS = [
     "hcg_free", "hcg_size", "hcg_curves", "hcg_key_words", "hcg_device_bytes", "hcg_search",
     "hcg_search_timed", "hcg_search_packed", "hcg_merge_packed", "hcg_keys", "hcg_sorted", "hcg_windows",
     "hcg_candidates", "hcg_brute_force", "hcg_binomial_tail", "hcg_miss_bound",
-    "hcg_search_f32", "hcg_brute_force_f32", "hcg_index_dtype", "hcg_plan_depth", "hcg_gen_rows", "hcg_gen_queries", "hcg_insert", "hcg_save", "hcg_load",
+    "hcg_search_f32", "hcg_brute_force_f32", "hcg_index_dtype", "hcg_launch_count", "hcg_plan_depth", "hcg_gen_rows", "hcg_gen_queries", "hcg_insert", "hcg_save", "hcg_load",
     "hcg_read_vectors", "hcg_write_vectors", "hcg_free_buffer",
 ]
 
@@ -97,6 +97,8 @@ def lib() -> C.CDLL:
     L.hcg_key_words.argtypes = [vp, u32]
     L.hcg_device_bytes.restype = u64
     L.hcg_device_bytes.argtypes = [vp]
+    L.hcg_launch_count.restype = u64
+    L.hcg_launch_count.argtypes = []
     L.hcg_index_dtype.restype = u32
     L.hcg_index_dtype.argtypes = [vp]
     L.hcg_search.argtypes = [vp, vp, u32, u32, u32, vp, vp, vp, vp]

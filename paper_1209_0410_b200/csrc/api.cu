@@ -4,6 +4,7 @@
 // reference's preconditions and turns them into status codes (the C++ wrapper
 // turns the codes back into the reference's exceptions).
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -45,6 +46,11 @@ hcg_status set_error(hcg_status code, const std::string& msg) {
     g_err = msg;
     return code;
 }
+
+namespace {
+std::atomic<unsigned long long> g_launches{0};
+}
+void count_launches(unsigned n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 hcg_status check_launch(const char* what) {
     const cudaError_t e = cudaGetLastError();
@@ -730,6 +736,7 @@ uint64_t hcg_size(const hcg_index* ix) { return ix ? ix->n : 0; }
 uint32_t hcg_curves(const hcg_index* ix) { return ix ? ix->C : 0; }
 uint32_t hcg_key_words(const hcg_index* ix, uint32_t c) { return ix && c < ix->C ? ix->curves[c].w : 0; }
 uint64_t hcg_device_bytes(const hcg_index* ix) { return ix ? ix->bytes : 0; }
+uint64_t hcg_launch_count(void) { return hcg::g_launches.load(); }
 uint32_t hcg_index_dtype(const hcg_index* ix) { return ix ? ix->dtype : 0; }
 
 hcg_status hcg_insert(hcg_index* ix, const uint8_t* rows, uint64_t nb, void* stream) {

@@ -396,6 +396,7 @@ hcg_status radix_sort_pairs(uint64_t** k, uint32_t** v, uint64_t** k_alt, uint32
     for (int s = 0; s < 8; ++s) {
         if (!((digit_mask >> s) & 1)) continue;
         const int shift = 8 * s;
+        count_launches(3);
         k_upsweep<<<tiles, kSortThreads, 0, st>>>(*k, n, shift, counts, tiles);
         k_scan_rows<<<256, 1024, 0, st>>>(counts, tiles, totals);
         k_downsweep<<<tiles, kSortThreads, 0, st>>>(*k, *v, *k_alt, *v_alt, n, shift, counts, totals, tiles);

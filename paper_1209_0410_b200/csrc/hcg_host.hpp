@@ -25,6 +25,8 @@ hcg_status check_launch(const char* what);
 hcg_status keygen_rows(const uint8_t* rows, uint64_t n, uint32_t pitch, const uint16_t* assign_c, int d, int m,
                        int kind, const uint32_t* lut, uint64_t* keys_soa, int W, unsigned long long* or_and,
                        int dmax, int dtype, unsigned* bad, cudaStream_t st);
+// Kernel-launch counter behind hcg_launch_count (search-path launchers and the radix sort add to it).
+void count_launches(unsigned n);
 hcg_status radix_sort_pairs(uint64_t** k, uint32_t** v, uint64_t** k_alt, uint32_t** v_alt, uint64_t n,
                             uint32_t digit_mask, uint32_t* counts, uint32_t* totals, cudaStream_t st);
 size_t radix_counts_bytes(uint64_t n);

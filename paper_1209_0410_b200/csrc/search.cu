@@ -177,6 +177,7 @@ static hcg_status locate_ws(const LocateArgs& a, int wsmax, cudaStream_t st) {
 
 hcg_status launch_locate(const LocateArgs& a, int dmax, int wsmax, cudaStream_t st) {
     if (uint64_t(a.nq) * a.C == 0) return HCG_OK;
+    count_launches(1);
     switch (dmax) {
         case 8: return locate_ws<8>(a, wsmax, st);
         case 16: return locate_ws<16>(a, wsmax, st);
@@ -1007,6 +1008,7 @@ hcg_status refine_dispatch(const RefineArgs& a_in, void* scratch, size_t* scratc
         uint32_t* v1 = v0 + a_in.nq;
         uint32_t* cnt = reinterpret_cast<uint32_t*>((reinterpret_cast<uintptr_t>(v1 + a_in.nq) + 255) & ~uintptr_t(255));
         uint32_t* totals = cnt + (radix_counts_bytes(a_in.nq) / 4 - 256);
+        count_launches(1);
         k_qkeys<<<unsigned((a_in.nq + 255) / 256), 256, 0, st>>>(a_in.begins, a_in.C, a_in.nq, k0, v0);
         HCG_RET_IF(check_launch("k_qkeys"));
         uint32_t dmask = 0;  // digits of the largest window start (< 2^32)
@@ -1039,6 +1041,7 @@ hcg_status refine_dispatch(const RefineArgs& a_in, void* scratch, size_t* scratc
             k_union_cas<<<std::min(a.nq, cas_ctas), kRefineThreads, 0, st>>>(a, lists, counts, lstride, tb, gtab);
         }
         HCG_RET_IF(check_launch("candidate union"));
+        count_launches(2);  // the union and its consumer (gather or the lists -> ids tap)
         if (a.ev_mid && q0 + chunk >= a_in.nq) cudaEventRecord(a.ev_mid, st);
         if (a.mode == kOutCandidates) {
             k_lists_to_ids<<<a.nq, 128, 0, st>>>(a, lists, counts, lstride);
@@ -1128,6 +1131,7 @@ __global__ void __launch_bounds__(256) k_merge(const uint64_t* __restrict__ pack
 hcg_status launch_merge(const uint64_t* packed, uint32_t parts, uint32_t nq, uint32_t k, uint64_t* out_ids,
                         uint32_t* out_sqdist, uint32_t* out_len, cudaStream_t st) {
     if (nq == 0) return HCG_OK;
+    count_launches(1);
     const unsigned blocks = unsigned((uint64_t(nq) * 32 + 255) / 256);
     switch (r_bucket(k)) {
         case 1: k_merge<1><<<blocks, 256, 0, st>>>(packed, parts, nq, k, out_ids, out_sqdist, out_len); break;
