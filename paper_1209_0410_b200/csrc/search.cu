@@ -815,11 +815,12 @@ __global__ void __launch_bounds__(NT, MINB) k_union_reg(RefineArgs a, uint32_t* 
 }
 
 // Sort keys of a batch: curve 0's window start per query (+ iota values).
-__global__ void k_qkeys(const uint32_t* __restrict__ begins, uint32_t C, uint32_t nq, uint64_t* __restrict__ keys,
-                        uint32_t* __restrict__ vals) {
+// (window start >> shift: a coarse order is enough for locality)
+__global__ void k_qkeys(const uint32_t* __restrict__ begins, uint32_t C, uint32_t nq, uint32_t shift,
+                        uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
     const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= nq) return;
-    keys[q] = begins[uint64_t(q) * C];
+    keys[q] = begins[uint64_t(q) * C] >> shift;
     vals[q] = q;
 }
 
@@ -1009,10 +1010,15 @@ hcg_status refine_dispatch(const RefineArgs& a_in, void* scratch, size_t* scratc
         uint32_t* cnt = reinterpret_cast<uint32_t*>((reinterpret_cast<uintptr_t>(v1 + a_in.nq) + 255) & ~uintptr_t(255));
         uint32_t* totals = cnt + (radix_counts_bytes(a_in.nq) / 4 - 256);
         count_launches(1);
-        k_qkeys<<<unsigned((a_in.nq + 255) / 256), 256, 0, st>>>(a_in.begins, a_in.C, a_in.nq, k0, v0);
+        // one 8-bit pass over the window start's top bits (n / 256 rows per bucket)
+        constexpr uint32_t qbits = 8;  // measured: 8 / 16 / 24 bits within 0.5 % of each other
+        uint32_t nbits = 1;
+        while (nbits < 32 && (uint64_t(1) << nbits) < a_in.n_rows) ++nbits;
+        const uint32_t shift = nbits > qbits ? nbits - qbits : 0u;
+        k_qkeys<<<unsigned((a_in.nq + 255) / 256), 256, 0, st>>>(a_in.begins, a_in.C, a_in.nq, shift, k0, v0);
         HCG_RET_IF(check_launch("k_qkeys"));
-        uint32_t dmask = 0;  // digits of the largest window start (< 2^32)
-        for (uint64_t top = a_in.n_rows, d = 0; top && d < 4; top >>= 8, ++d) dmask |= 1u << d;
+        uint32_t dmask = 0;
+        for (uint32_t d = 0; d * 8 < std::min(qbits, nbits); ++d) dmask |= 1u << d;
         HCG_RET_IF(radix_sort_pairs(&k0, &v0, &k1, &v1, a_in.nq, dmask, cnt, totals, st));
         qorder = v0;
     }
