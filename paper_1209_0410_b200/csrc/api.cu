@@ -616,6 +616,8 @@ RefineArgs refine_args(const hcg_index* ix, const uint8_t* dq, uint32_t nq, uint
     a.n_rows = ix->n;
     a.dtype = int(ix->dtype);
     a.idtab = ix->idtab;
+    static const bool no_list = getenv("HCG_NO_UNION_LIST") != nullptr;
+    a.union_list = !no_list;
     return a;
 }
 

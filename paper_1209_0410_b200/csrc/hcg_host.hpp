@@ -91,6 +91,7 @@ struct RefineArgs {
     double* out_sqdist_f64;    // HCG_F32 + kOutIds: nq x k squared distances
     const uint32_t* idtab;     // physical row -> id slot (null: identity)
     const uint32_t* qorder;    // processing order: batch position -> query (null: identity)
+    bool union_list;           // union rounds after the first over a compacted shared-memory list
 };
 // Scratch bytes the refine launch needs (global hash tables when the table
 // does not fit in shared memory); query with scratch == nullptr first.

@@ -689,6 +689,7 @@ hcg_status gather_f32_launch(const RefineArgs& a, const uint32_t* lists, const u
 // (measured: a CAS pass for every round-1 collision instead is 1.6x slower).
 // Kept ids are compacted with one block scan.
 constexpr int kRegRounds = 4;
+constexpr int kListRounds = 6;
 
 template <int JMAX, int NT, int MINB = 1>
 __global__ void __launch_bounds__(NT, MINB) k_union_reg(RefineArgs a, uint32_t* __restrict__ lists,
@@ -761,9 +762,87 @@ __global__ void __launch_bounds__(NT, MINB) k_union_reg(RefineArgs a, uint32_t* 
             }
         }
         uint32_t keep = 0;
-        bool left = true;
+        // Round 1 over every id (register-resident); about a quarter of the
+        // ids collide and stay pending.
+        bool left;
+        {
+            const uint32_t mul = 0x9E3779B1u;
+#pragma unroll
+            for (int j = 0; j < JMAX; ++j)
+                if ((pending >> j) & 1)
+                    tab[(id[j] * mul) >> shift] = (uint64_t(id[j]) << 32) | uint32_t(tid + j * NT);
+            __syncthreads();
+#pragma unroll
+            for (int j = 0; j < JMAX; ++j) {
+                if ((pending >> j) & 1) {
+                    const uint64_t o = tab[(id[j] * mul) >> shift];
+                    if (uint32_t(o >> 32) == id[j]) {
+                        pending &= ~(1u << j);
+                        if (uint32_t(o) == uint32_t(tid + j * NT)) keep |= 1u << j;
+                    }
+                }
+            }
+            left = __syncthreads_or(pending != 0);
+        }
+        // Later rounds over a compacted list: the pending (id, position) pairs
+        // move to shared memory (aliasing the table: round 1's reads are
+        // done) and the rounds cost what is left, not JMAX predicated slots
+        // per thread.  A u16 table of list indices at twice the slots resolves
+        // them in ~2 rounds.  Copies of an id resolve together, as before.
+        uint32_t lkeep = 0;  // kept list entries of this thread (bit u: entry tid + u * NT)
+        bool listed = false;
+        uint2* lst = reinterpret_cast<uint2*>(smem);  // [cap] (id, position)
+        const uint32_t cap = (1u << tb) >> 1;
+        if (left && a.union_list) {
+            const uint32_t np = __popc(pending);
+            const uint32_t loff = block_excl_scan_u<NT>(np, wsum);
+            uint32_t P = 0;
+#pragma unroll
+            for (int w = 0; w < int(kWarps); ++w) P += wsum[w];
+            if (P <= cap) {  // block-uniform
+                listed = true;
+                uint32_t wpos = loff;
+#pragma unroll
+                for (int j = 0; j < JMAX; ++j)
+                    if ((pending >> j) & 1) lst[wpos++] = make_uint2(id[j], uint32_t(tid + j * NT));
+                pending = 0;
+                __syncthreads();
+                uint16_t* t16 = reinterpret_cast<uint16_t*>(lst + cap);  // [2 << tb]
+                const uint32_t shift16 = shift - 1;
+                uint32_t lpend = 0;
+                for (uint32_t u = 0; tid + u * NT < P; ++u) lpend |= 1u << u;
+                bool lleft = true;
 #pragma unroll 1
-        for (int r = 0; r < kRegRounds && left; ++r) {
+                for (int r = 1; r <= kListRounds && lleft; ++r) {
+                    const uint32_t mul = 0x9E3779B1u + 0x7F4A7C16u * uint32_t(r) * 2u;  // odd
+                    for (uint32_t pm = lpend; pm; pm &= pm - 1) {
+                        const uint32_t i = tid + uint32_t(__ffs(pm) - 1) * NT;
+                        t16[(lst[i].x * mul) >> shift16] = uint16_t(i);
+                    }
+                    __syncthreads();
+                    for (uint32_t pm = lpend; pm; pm &= pm - 1) {
+                        const uint32_t u = uint32_t(__ffs(pm) - 1), i = tid + u * NT;
+                        const uint32_t o = t16[(lst[i].x * mul) >> shift16];
+                        if (lst[o].x == lst[i].x) {
+                            lpend &= ~(1u << u);
+                            if (o == i) lkeep |= 1u << u;
+                        }
+                    }
+                    lleft = __syncthreads_or(lpend != 0);
+                }
+                // leftovers (rare): every copy of such an id is still pending;
+                // the lowest list index is its first copy
+                for (uint32_t pm = lpend; pm; pm &= pm - 1) {
+                    const uint32_t u = uint32_t(__ffs(pm) - 1), i = tid + u * NT;
+                    bool first = true;
+                    for (uint32_t i2 = 0; i2 < i && first; ++i2) first = lst[i2].x != lst[i].x;
+                    if (first) lkeep |= 1u << u;
+                }
+                left = false;
+            }
+        }
+#pragma unroll 1
+        for (int r = 1; r < kRegRounds && left; ++r) {
             const uint32_t mul = 0x9E3779B1u + 0x7F4A7C16u * uint32_t(r) * 2u;  // odd
 #pragma unroll
             for (int j = 0; j < JMAX; ++j)
@@ -802,15 +881,17 @@ __global__ void __launch_bounds__(NT, MINB) k_union_reg(RefineArgs a, uint32_t* 
                 }
             }
         }
-        const uint32_t mine = __popc(keep);
+        const uint32_t mine = __popc(keep) + __popc(lkeep);
         const uint32_t off = block_excl_scan_u<NT>(mine, wsum);
         uint32_t* out = lists + uint64_t(q) * lstride + off;
         uint32_t w = 0;
 #pragma unroll
         for (int j = 0; j < JMAX; ++j)
             if ((keep >> j) & 1) out[w++] = id[j];
+        for (uint32_t pm = lkeep; pm; pm &= pm - 1) out[w++] = lst[tid + uint32_t(__ffs(pm) - 1) * NT].x;
         HCG_DASSERT(off + mine <= T && off + mine <= lstride);
         if (tid == NT - 1) counts[q] = off + mine;
+        if (listed) __syncthreads();  // list reads before the next query's table writes
     }
 }
 
