@@ -500,7 +500,7 @@ __global__ void __launch_bounds__(NW * 32) k_gather_cta(RefineArgs a, const uint
     for (uint32_t q = blockIdx.x; q < a.nq; q += gridDim.x) {
         const uint32_t n = __ldcg(counts + q);
         uint4 qv[CR];
-        load_query<CR>(a, q, lane, qv);
+        load_query<CR>(a, a.qorder ? __ldg(a.qorder + q) : q, lane, qv);
         WarpTopK<R> tk;
         tk.init(int(a.k));
         gather_list<R, CR>(a, lists + uint64_t(q) * lstride, n, warp * 32, NW * 32, qv, lane, tk);
@@ -513,7 +513,7 @@ __global__ void __launch_bounds__(NW * 32) k_gather_cta(RefineArgs a, const uint
             const uint32_t kr = (a.k + 31) & ~31u;
             for (int w = 0; w < kWarps; ++w)
                 for (uint32_t i = 0; i < kr; i += 32) fin.offer(mbuf[w * KCAP + i + lane], lane);
-            write_result<R>(a, q, fin, lane, n);
+            write_result<R>(a, a.qorder ? __ldg(a.qorder + q) : q, fin, lane, n);
         }
         __syncthreads();
     }
@@ -620,11 +620,12 @@ __global__ void __launch_bounds__(kRefineThreads, 2) k_gather_f32(RefineArgs a, 
     const uint32_t qstep = gridDim.x * (kRefineThreads / 32);
     for (uint32_t q = (blockIdx.x * kRefineThreads + threadIdx.x) >> 5; q < a.nq; q += qstep) {
         const uint32_t n = __ldcg(counts + q);
-        const uint4 qv = load_query_f32(a.queries, a.pitch, q, lane);
+        const uint32_t qq = a.qorder ? __ldg(a.qorder + q) : q;  // list q holds query qq
+        const uint4 qv = load_query_f32(a.queries, a.pitch, qq, lane);
         WarpTopK2<R> tk;
         tk.init(int(a.k));
         gather_list_f32<R, false>(a.rows, a.pitch, lists + uint64_t(q) * lstride, n, 0, 8, qv, lane, tk, a.idtab);
-        write_result_f32<R>(a, q, tk, lane, n);
+        write_result_f32<R>(a, qq, tk, lane, n);
     }
 }
 
@@ -655,13 +656,13 @@ __global__ void __launch_bounds__(NW * 32) k_gather_cta_f32(RefineArgs a, const 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (uint32_t q = blockIdx.x; q < a.nq; q += gridDim.x) {
         const uint32_t n = __ldcg(counts + q);
-        const uint4 qv = load_query_f32(a.queries, a.pitch, q, lane);
+        const uint4 qv = load_query_f32(a.queries, a.pitch, a.qorder ? __ldg(a.qorder + q) : q, lane);
         WarpTopK2<R> tk;
         tk.init(int(a.k));
         gather_list_f32<R, false>(a.rows, a.pitch, lists + uint64_t(q) * lstride, n, warp * 8, NW * 8, qv, lane, tk,
                                   a.idtab);
         merge_warps_f32<R, NW>(tk, ma, mb, a.k, lane, warp);
-        if (warp == 0) write_result_f32<R>(a, q, tk, lane, n);
+        if (warp == 0) write_result_f32<R>(a, a.qorder ? __ldg(a.qorder + q) : q, tk, lane, n);
         __syncthreads();
     }
 }
@@ -1070,8 +1071,8 @@ hcg_status refine_dispatch(const RefineArgs& a_in, void* scratch, size_t* scratc
     // same time share candidate rows (rows are stored in curve-0 order), so
     // part of the gather hits L2 (measured 5.15 -> 4.75 ms at 100K queries).
     static const bool no_qsort = getenv("HCG_NO_QSORT") != nullptr;
-    const bool qsort = !no_qsort && reg_union && a_in.dtype == HCG_U8 && a_in.mode != kOutCandidates &&
-                       a_in.nq >= 16384 && chunk >= a_in.nq && a_in.idtab != nullptr;
+    const bool qsort = !no_qsort && reg_union && a_in.mode != kOutCandidates && a_in.nq >= 16384 &&
+                       chunk >= a_in.nq && a_in.idtab != nullptr;  // both gathers map list q -> qorder[q]
     const size_t qsort_bytes = qsort ? size_t(a_in.nq) * 24 + radix_counts_bytes(a_in.nq) + 256 : 0;
     if (!scratch) {
         *scratch_bytes = lists_bytes + counts_bytes + table_bytes + qsort_bytes;

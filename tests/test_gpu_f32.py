@@ -226,3 +226,12 @@ def test_f32_errors():
     # 129 float components exceed the 512-byte row
     with pytest.raises(HcgError):
         H.MulticurvesIndex(float_rows(10, 129, 0), H.default_scheme(129, 3, 8))
+
+
+def test_f32_large_batch():
+    """Warp-per-query f32 gather with the curve-0 batch order (>= 16K queries)."""
+    rows = float_rows(20_000, 128, 21)
+    qs = float_rows(17_000, 128, 22)
+    gi = H.MulticurvesIndex(rows, H.default_scheme(128, 8, 16))
+    oi = _oracle(rows, 8, 16, H.HILBERT)
+    _check_search(gi, oi, qs, 10, 300)
