@@ -100,6 +100,8 @@ typedef struct hcg_scheme {
     uint32_t cell_lut[256];     /* HCG_U8: quantized cell of each byte value        */
     double dist_scale;          /* HCG_U8 view scale: distance = sqrt(sqdist)*scale */
     uint32_t dtype;             /* an hcg_dtype; 0 = HCG_U8                        */
+    float view_offset;          /* HCG_U8: byte b is the float view_offset + b *   */
+                                /* dist_scale (kept with the index for wrappers)   */
 } hcg_scheme;
 
 typedef struct hcg_index hcg_index;
@@ -207,6 +209,16 @@ hcg_status hcg_keys(const hcg_index* index, const uint8_t* rows, uint64_t n, uin
 /* Sorted subindex c: ids (n) and, when out_words != NULL, full keys (n x words). */
 hcg_status hcg_sorted(const hcg_index* index, uint32_t curve, uint64_t* out_ids,
                       uint64_t* out_words, void* stream);
+/* Ids of positions [begin, begin + count) of sorted subindex c
+ * (SubIndex::entries() slice; retrieve_candidates = hcg_windows + this). */
+hcg_status hcg_sorted_range(const hcg_index* index, uint32_t curve, uint64_t begin, uint64_t count,
+                            uint64_t* out_ids, void* stream);
+/* The scheme an index was built with (hcg_load callers recover it here).
+ * *assign_len receives the assignment length; with assign_off / assign NULL
+ * only the sizes are reported, else out->assign_off / out->assign point at
+ * the caller's arrays (curves + 1 and *assign_len entries). */
+hcg_status hcg_describe(const hcg_index* index, hcg_scheme* out, uint32_t* assign_off, uint32_t* assign,
+                        uint32_t* assign_len);
 /* rank_of and window [begin, end) of every (query, curve), nq x curves each. */
 hcg_status hcg_windows(const hcg_index* index, const uint8_t* queries, uint32_t nq, uint32_t depth,
                        uint64_t* out_rank, uint64_t* out_begin, uint64_t* out_end, void* stream);

@@ -28,6 +28,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstring>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -176,6 +177,54 @@ class MulticurvesIndex {
     }
 
     std::size_t size() const { return ix_ ? hcg_size(ix_) : 0; }
+
+    // multicurves.hpp:79.  Ids are dense here: v.id must be size() (the next id).
+    template <class FeatureVector>
+    void insert(const FeatureVector& v) {
+        if (v.id != size()) throw std::invalid_argument("insert: ids must continue 0..n-1 in order");
+        if (view_.f32) {
+            std::vector<float> r;
+            detail::append_floats(v, scheme_.d_full, r);
+            detail::check(hcg_insert(ix_, reinterpret_cast<const std::uint8_t*>(r.data()), 1, nullptr));
+        } else {
+            std::vector<std::uint8_t> r;
+            detail::append_bytes(v, scheme_.d_full, view_, r);
+            detail::check(hcg_insert(ix_, r.data(), 1, nullptr));
+        }
+    }
+
+    // multicurves.hpp:84: ids of the window of `depth` entries on curve c, in key order.
+    template <class FeatureVector>
+    std::vector<std::uint64_t> retrieve_candidates(const FeatureVector& q, std::uint32_t c, std::size_t depth) const {
+        if (c >= scheme_.curves()) throw std::invalid_argument("curve out of range");
+        const std::vector<std::uint8_t> qb = query_bytes(q);
+        std::vector<std::uint64_t> rank(scheme_.curves()), begin(scheme_.curves()), end(scheme_.curves());
+        detail::check(hcg_windows(ix_, qb.data(), 1, static_cast<std::uint32_t>(depth), rank.data(), begin.data(),
+                                  end.data(), nullptr));
+        std::vector<std::uint64_t> ids(end[c] - begin[c]);
+        detail::check(hcg_sorted_range(ix_, c, begin[c], ids.size(), ids.data(), nullptr));
+        return ids;
+    }
+
+    // multicurves.hpp:96-98: little-endian binary persistence, bit-exact round trip.
+    void save(const std::string& path) const { detail::check(hcg_save(ix_, path.c_str())); }
+    static MulticurvesIndex load(const std::string& path, int device = 0) {
+        MulticurvesIndex idx;
+        detail::check(hcg_load(path.c_str(), device, nullptr, &idx.ix_));
+        hcg_scheme s{};
+        std::uint32_t n_asg = 0;
+        detail::check(hcg_describe(idx.ix_, &s, nullptr, nullptr, &n_asg));
+        std::vector<std::uint32_t> off(s.curves + 1), asg(n_asg);
+        detail::check(hcg_describe(idx.ix_, &s, off.data(), asg.data(), &n_asg));
+        idx.scheme_.d_full = s.d_full;
+        idx.scheme_.bits_per_dim = s.bits_per_dim;
+        idx.scheme_.curve_kind = static_cast<CurveKind>(s.curve_kind);
+        for (std::uint32_t c = 0; c < s.curves; ++c)
+            idx.scheme_.assignment.emplace_back(asg.begin() + off[c], asg.begin() + off[c + 1]);
+        idx.view_ = s.dtype == HCG_F32 ? View::floats()
+                                        : View{s.view_offset, static_cast<float>(s.dist_scale), false};
+        return idx;
+    }
     const ProjectionScheme& scheme() const { return scheme_; }
     hcg_index* handle() const { return ix_; }
 
@@ -251,6 +300,21 @@ class MulticurvesIndex {
     }
 
   private:
+    // One query as the index stores it (floats or view bytes), as raw bytes.
+    template <class FeatureVector>
+    std::vector<std::uint8_t> query_bytes(const FeatureVector& q) const {
+        std::vector<std::uint8_t> out;
+        if (view_.f32) {
+            std::vector<float> f;
+            detail::append_floats(q, scheme_.d_full, f);
+            out.resize(f.size() * sizeof(float));
+            std::memcpy(out.data(), f.data(), out.size());
+        } else {
+            detail::append_bytes(q, scheme_.d_full, view_, out);
+        }
+        return out;
+    }
+
     void build(const void* rows, std::uint64_t n, int device, std::uint64_t id_base = 0,
                std::uint64_t id_stride = 1) {
         std::vector<std::uint32_t> off{0}, asg;
@@ -267,6 +331,7 @@ class MulticurvesIndex {
         s.assign = asg.data();
         s.dist_scale = view_.f32 ? 1.0 : view_.scale;
         s.dtype = view_.f32 ? HCG_F32 : HCG_U8;
+        s.view_offset = view_.f32 ? 0.0f : view_.offset;
         if (!view_.f32) detail::check(hcg_make_lut(view_.offset, view_.scale, scheme_.bits_per_dim, s.cell_lut));
         detail::check(hcg_build(&s, static_cast<const std::uint8_t*>(rows), n, id_base, id_stride, device, nullptr,
                                 &ix_));

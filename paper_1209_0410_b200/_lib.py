@@ -36,7 +36,7 @@ EXPORTS = [
     "hcg_free", "hcg_size", "hcg_curves", "hcg_key_words", "hcg_device_bytes", "hcg_search",
     "hcg_search_timed", "hcg_search_packed", "hcg_merge_packed", "hcg_keys", "hcg_sorted", "hcg_windows",
     "hcg_candidates", "hcg_brute_force", "hcg_binomial_tail", "hcg_miss_bound",
-    "hcg_search_f32", "hcg_brute_force_f32", "hcg_index_dtype", "hcg_launch_count", "hcg_plan_depth", "hcg_gen_rows", "hcg_gen_queries", "hcg_insert", "hcg_save", "hcg_load",
+    "hcg_search_f32", "hcg_brute_force_f32", "hcg_index_dtype", "hcg_launch_count", "hcg_sorted_range", "hcg_describe", "hcg_plan_depth", "hcg_gen_rows", "hcg_gen_queries", "hcg_insert", "hcg_save", "hcg_load",
     "hcg_read_vectors", "hcg_write_vectors", "hcg_free_buffer",
 ]
 
@@ -52,6 +52,7 @@ class HcgScheme(C.Structure):
         ("cell_lut", C.c_uint32 * 256),
         ("dist_scale", C.c_double),
         ("dtype", C.c_uint32),
+        ("view_offset", C.c_float),
     ]
 
 
@@ -107,6 +108,8 @@ def lib() -> C.CDLL:
     L.hcg_merge_packed.argtypes = [vp, u32, u32, u32, vp, vp, vp, C.c_int, vp]
     L.hcg_keys.argtypes = [vp, vp, u64, u32, vp, vp]
     L.hcg_sorted.argtypes = [vp, u32, vp, vp, vp]
+    L.hcg_sorted_range.argtypes = [vp, u32, u64, u64, vp, vp]
+    L.hcg_describe.argtypes = [vp, P(HcgScheme), vp, vp, P(u32)]
     L.hcg_windows.argtypes = [vp, vp, u32, u32, vp, vp, vp, vp]
     L.hcg_candidates.argtypes = [vp, vp, u32, u32, vp, u32, vp, vp]
     L.hcg_brute_force.argtypes = [vp, vp, u32, u32, vp, vp, vp, vp]
@@ -129,7 +132,8 @@ def lib() -> C.CDLL:
     L.hcg_free_buffer.restype = None
     for name in ("hcg_make_lut", "hcg_default_assignment", "hcg_build", "hcg_free", "hcg_search",
                  "hcg_search_timed", "hcg_search_packed", "hcg_merge_packed", "hcg_keys", "hcg_sorted", "hcg_windows",
-                 "hcg_candidates", "hcg_brute_force", "hcg_search_f32", "hcg_brute_force_f32", "hcg_gen_rows", "hcg_gen_queries", "hcg_insert",
+                 "hcg_candidates", "hcg_brute_force", "hcg_search_f32", "hcg_brute_force_f32", "hcg_sorted_range",
+                 "hcg_describe", "hcg_gen_rows", "hcg_gen_queries", "hcg_insert",
                  "hcg_save", "hcg_load", "hcg_read_vectors", "hcg_write_vectors"):
         getattr(L, name).restype = C.c_int
     del u8

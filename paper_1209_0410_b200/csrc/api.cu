@@ -20,6 +20,7 @@ struct hcg_index {
     uint32_t d_full = 0, pitch = 0, C = 0, m = 0, kind = 0;
     uint32_t dtype = HCG_U8, row_bytes = 0;  // row_bytes = d_full * element size
     double dist_scale = 1.0;
+    float view_offset = 0.0f;
     uint64_t n = 0, id_base = 0, id_stride = 1;
     std::vector<uint32_t> off, assign;
     uint32_t lut[256] = {};
@@ -502,6 +503,7 @@ hcg_status new_index(const hcg_scheme* s, uint64_t n, uint64_t id_base, uint64_t
     ix->m = s->bits_per_dim;
     ix->kind = s->curve_kind;
     ix->dist_scale = s->dist_scale;
+    ix->view_offset = std::isfinite(s->view_offset) ? s->view_offset : 0.0f;
     ix->n = n;
     ix->id_base = id_base;
     ix->id_stride = id_stride;
@@ -648,7 +650,7 @@ using namespace hcg;
 namespace {
 constexpr char kMagic[8] = {'H', 'C', 'G', 'I', 'D', 'X', 0, 1};
 constexpr char kTrailer[8] = {'H', 'C', 'G', 'E', 'N', 'D', 0, 0};
-constexpr uint32_t kFormatVersion = 3;  // 2: + descriptor dtype; 3: + physical row order (id table)
+constexpr uint32_t kFormatVersion = 4;  // 2: + dtype; 3: + physical row order (id table); 4: + view offset
 
 struct FileCloser {
     FILE* f = nullptr;
@@ -804,7 +806,8 @@ hcg_status hcg_save(const hcg_index* ix, const char* path) {
     const uint32_t hdr[7] = {kFormatVersion, ix->d_full, ix->C, ix->m, ix->kind, uint32_t(ix->assign.size()),
                              ix->dtype};
     const uint64_t ids[3] = {ix->n, ix->id_base, ix->id_stride};
-    bool ok = put(f, kMagic, 8) && put(f, hdr, 7) && put(f, &ix->dist_scale, 1) && put(f, ids, 3) &&
+    bool ok = put(f, kMagic, 8) && put(f, hdr, 7) && put(f, &ix->dist_scale, 1) && put(f, &ix->view_offset, 1) &&
+              put(f, ids, 3) &&
               put(f, ix->lut, 256) && put(f, ix->off.data(), ix->off.size()) &&
               put(f, ix->assign.data(), ix->assign.size());
     // rows, unpadded, in slices
@@ -855,13 +858,16 @@ hcg_status hcg_load(const char* path, int device, void* stream, hcg_index** out)
     uint64_t ids[3];
     if (!get(f, magic, 8) || std::memcmp(magic, kMagic, 8) != 0) return set_error(HCG_EIO, std::string(path) + ": not an hcg index");
     if (!get(f, hdr, 7) || hdr[0] != kFormatVersion) return set_error(HCG_EIO, std::string(path) + ": unsupported version");
-    if (!get(f, &scale, 1) || !get(f, ids, 3)) return set_error(HCG_EIO, std::string(path) + ": truncated header");
+    float voff = 0.0f;
+    if (!get(f, &scale, 1) || !get(f, &voff, 1) || !get(f, ids, 3))
+        return set_error(HCG_EIO, std::string(path) + ": truncated header");
     hcg_scheme s{};
     s.d_full = hdr[1];
     s.curves = hdr[2];
     s.bits_per_dim = hdr[3];
     s.curve_kind = hdr[4];
     s.dist_scale = scale;
+    s.view_offset = voff;
     s.dtype = hdr[6];
     if (s.curves == 0 || s.curves > 4096 || hdr[5] > 1u << 20) return set_error(HCG_EIO, std::string(path) + ": corrupt header");
     std::vector<uint32_t> off(s.curves + 1), asg(hdr[5]);
@@ -1151,6 +1157,52 @@ hcg_status hcg_sorted(const hcg_index* ix, uint32_t curve, uint64_t* out_ids, ui
         HCG_TRY_CUDA(cudaMemcpyAsync(h.data(), full, h.size() * 8, cudaMemcpyDeviceToHost, st));
         HCG_TRY_CUDA(cudaStreamSynchronize(st));
         HCG_TRY(deliver(out_words, h));
+    }
+    return HCG_OK;
+}
+
+hcg_status hcg_sorted_range(const hcg_index* ix, uint32_t curve, uint64_t begin, uint64_t count, uint64_t* out_ids,
+                            void* stream) {
+    HCG_TRY(check_index(ix));
+    if (curve >= ix->C) return set_error(HCG_EINVAL, "curve out of range");
+    if (begin > ix->n || count > ix->n - begin) return set_error(HCG_EINVAL, "range beyond the subindex");
+    if (count == 0) return HCG_OK;
+    if (!out_ids) return set_error(HCG_EINVAL, "null buffer");
+    DeviceGuard g(ix->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    Scratch sc(st);
+    uint32_t* d = sc.alloc<uint32_t>(count);
+    if (!d) return set_error(HCG_ENOMEM, "range buffer");
+    HCG_TRY_CUDA(cudaMemcpyAsync(d, ix->slots[curve] + begin, count * 4, cudaMemcpyDeviceToDevice, st));
+    if (ix->idtab) launch_map(d, count, ix->idtab, st);  // physical row -> id slot
+    HCG_TRY(check_launch("id map"));
+    std::vector<uint32_t> sl(count);
+    HCG_TRY_CUDA(cudaMemcpyAsync(sl.data(), d, count * 4, cudaMemcpyDeviceToHost, st));
+    HCG_TRY_CUDA(cudaStreamSynchronize(st));
+    std::vector<uint64_t> ids(count);
+    for (uint64_t i = 0; i < count; ++i) ids[i] = ix->id_base + uint64_t(sl[i]) * ix->id_stride;
+    return deliver(out_ids, ids);
+}
+
+hcg_status hcg_describe(const hcg_index* ix, hcg_scheme* out, uint32_t* assign_off, uint32_t* assign,
+                        uint32_t* assign_len) {
+    HCG_TRY(check_index(ix));
+    if (!out || !assign_len) return set_error(HCG_EINVAL, "null argument");
+    *assign_len = uint32_t(ix->assign.size());
+    std::memset(out, 0, sizeof(*out));
+    out->d_full = ix->d_full;
+    out->curves = ix->C;
+    out->bits_per_dim = ix->m;
+    out->curve_kind = ix->kind;
+    std::memcpy(out->cell_lut, ix->lut, sizeof(ix->lut));
+    out->dist_scale = ix->dist_scale;
+    out->dtype = ix->dtype;
+    out->view_offset = ix->view_offset;
+    if (assign_off && assign) {
+        std::memcpy(assign_off, ix->off.data(), ix->off.size() * 4);
+        std::memcpy(assign, ix->assign.data(), ix->assign.size() * 4);
+        out->assign_off = assign_off;
+        out->assign = assign;
     }
     return HCG_OK;
 }

@@ -213,6 +213,7 @@ class MulticurvesIndex:
             s.cell_lut[b] = int(lut[b])
         s.dist_scale = float(view.scale) if dtype == "u8" else 1.0
         s.dtype = HCG_U8 if dtype == "u8" else HCG_F32
+        s.view_offset = float(view.offset) if dtype == "u8" else 0.0
         self._scheme_c = s
         h = C.c_void_p()
         check(lib().hcg_build(C.byref(s), _ptr(rows), n, id_base, id_stride, device,
@@ -233,14 +234,25 @@ class MulticurvesIndex:
         check(lib().hcg_save(self._h, os.fsencode(path)))
 
     @classmethod
-    def load(cls, path: str, scheme: ProjectionScheme, view: View, device: int = 0, id_base: int = 0,
-             id_stride: int = 1) -> "MulticurvesIndex":
-        """multicurves.hpp:98.  The file carries the scheme; `scheme`/`view` are
-        the caller's description of it (for distances and the Python mirror)."""
+    def load(cls, path: str, scheme: ProjectionScheme | None = None, view: View | None = None, device: int = 0,
+             id_base: int = 0, id_stride: int = 1) -> "MulticurvesIndex":
+        """multicurves.hpp:98.  The file carries the scheme and the view; when
+        `scheme` / `view` are omitted they are read back from the index."""
         h = C.c_void_p()
         check(lib().hcg_load(os.fsencode(path), device, None, C.byref(h)))
-        obj = cls(None, scheme, view, device, id_base, id_stride, _handle=h)
-        return obj
+        if scheme is None or view is None:
+            s = HcgScheme()
+            n_asg = C.c_uint32()
+            check(lib().hcg_describe(h, C.byref(s), None, None, C.byref(n_asg)))
+            off = (C.c_uint32 * (s.curves + 1))()
+            asg = (C.c_uint32 * max(n_asg.value, 1))()
+            check(lib().hcg_describe(h, C.byref(s), off, asg, C.byref(n_asg)))
+            if scheme is None:
+                scheme = ProjectionScheme(s.d_full, s.bits_per_dim, s.curve_kind, 0,
+                                          [[int(asg[i]) for i in range(off[c], off[c + 1])] for c in range(s.curves)])
+            if view is None:
+                view = View(float(s.view_offset), float(s.dist_scale), "loaded")
+        return cls(None, scheme, view, device, id_base, id_stride, _handle=h)
 
     # -- lifetime
     def close(self) -> None:
@@ -349,8 +361,10 @@ class MulticurvesIndex:
     def retrieve_candidates(self, query, c: int, depth: int) -> np.ndarray:
         """Ids of the window on curve c (multicurves.hpp:83-85), in key order."""
         _, b, e = self.windows(query, depth)
-        ids = self.subindex(c)
-        return ids[int(b[0, c]):int(e[0, c])]
+        begin, end = int(b[0, c]), int(e[0, c])
+        out = np.zeros(max(end - begin, 1), np.uint64)
+        check(lib().hcg_sorted_range(self._h, c, begin, end - begin, _ptr(out), None))
+        return out[:end - begin]
 
     def candidates(self, queries, probe_depth: int):
         """Deduplicated candidate ids per query (list of sorted arrays)."""

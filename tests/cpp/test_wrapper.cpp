@@ -2,7 +2,10 @@
 // libhcg.so against the CPU oracle (oracle/liboracle.so, test infrastructure).
 // Prints "wrapper ok" and exits 0 on bit-identical NeighborLists.
 #include <cstdio>
+#include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <string>
 #include <cstdlib>
 #include <limits>
 #include <vector>
@@ -111,6 +114,35 @@ int main() {
             fidx.search(qv, {k, depth});
             ++bad;
         } catch (const std::invalid_argument&) {
+        }
+        // retrieve_candidates (one curve's window, key order) within the union
+        {
+            Vec qv{0, std::vector<float>(fq.begin(), fq.begin() + d)};
+            const auto w0 = fidx.retrieve_candidates(qv, 0, 64);
+            const auto un = fidx.candidate_union(qv, 64);
+            if (w0.size() != 64) ++bad;
+            for (auto id : w0)
+                if (!std::binary_search(un.begin(), un.end(), id)) ++bad;
+        }
+        // save / load (scheme and view come back from the file) and insert
+        {
+            const std::string path = "/tmp/hcb_wrapper_test.hcg";
+            fidx.save(path);
+            hcb::MulticurvesIndex back = hcb::MulticurvesIndex::load(path);
+            Vec qv{0, std::vector<float>(fq.begin(), fq.begin() + d)};
+            if (back.search(qv, {k, depth}) != fidx.search(qv, {k, depth})) ++bad;
+            if (back.size() != n || back.scheme().curves() != C) ++bad;
+            Vec nv{n, std::vector<float>(fq.begin(), fq.begin() + d)};  // the query itself, id n
+            back.insert(nv);
+            const hcb::NeighborList nl = back.search(qv, {1, depth});
+            if (back.size() != n + 1 || nl.empty() || nl[0].id != n || nl[0].distance != 0.0) ++bad;
+            try {  // ids must continue densely
+                Vec gap{n + 5, std::vector<float>(d, 1.0f)};
+                back.insert(gap);
+                ++bad;
+            } catch (const std::invalid_argument&) {
+            }
+            std::remove(path.c_str());
         }
         orc_free(fo);
     }

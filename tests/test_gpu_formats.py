@@ -83,3 +83,25 @@ def test_load_rejects_garbage(tmp_path):
     p.write_bytes(b"not an index at all")
     with pytest.raises(H.HcgIOError):
         H.MulticurvesIndex.load(str(p), H.default_scheme(128, 8), H.RAW)
+
+
+def test_load_recovers_scheme_and_view(tmp_path):
+    """hcg_describe: a saved index loads without the caller restating its
+    scheme or view (multicurves.hpp:98 takes only the path)."""
+    import paper_1209_0410_b200 as H
+    from oracle import pyoracle as P
+    rows = P.gen_rows(0, 3000)
+    qs = P.gen_queries(0, 20, 3000)
+    scheme = H.default_scheme(128, 8, 16)
+    gi = H.MulticurvesIndex(rows, scheme, H.LIFTED)
+    path = str(tmp_path / "x.hcg")
+    gi.save(path)
+    back = H.MulticurvesIndex.load(path)
+    assert back.scheme.assignment == scheme.assignment and back.scheme.bits_per_dim == 16
+    assert back.view.offset == 1.0 and back.view.scale == 1.0 / 256
+    a, b = gi.search_batch(qs, 10, 100), back.search_batch(qs, 10, 100)
+    for x, y in zip(a, b):
+        assert np.asarray(x).tobytes() == np.asarray(y).tobytes()
+    assert gi.search(qs[0], H.SearchParams(10, 100)) == back.search(qs[0], H.SearchParams(10, 100))
+    np.testing.assert_array_equal(back.retrieve_candidates(qs[3], 2, 50), gi.subindex(2)[
+        int(gi.windows(qs[3], 50)[1][0, 2]):int(gi.windows(qs[3], 50)[2][0, 2])])
