@@ -8,7 +8,8 @@ from ._lib import HcgError, HcgInvalidArgument, HcgIOError, LIB_PATH, lib  # noq
 from .multicurves import (  # noqa: F401
     HILBERT, LIFTED, RAW, ZORDER, MulticurvesIndex, Neighbor, ProjectionScheme, SearchParams, View,
     binomial_tail, default_scheme, gen_queries, gen_rows, make_lut, merge_packed, miss_bound,
-    plan_depth, read_vectors, recall_at, shard_probe_depth, write_vectors,
+    plan_depth, read_search_csv, read_vectors, recall_at, shard_probe_depth, write_search_csv,
+    write_vectors,
 )
 
 __version__ = "0.1.0"

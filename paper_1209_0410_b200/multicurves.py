@@ -503,9 +503,43 @@ def recall_at(found_ids, true_ids, k: int) -> float:
     return hits / (k * max(len(f), 1))
 
 
+def write_search_csv(path: str, ids, distances, lens, query_ids=None) -> int:
+    """cmd_search's result file: one `query_id,rank,neighbor_id,distance`
+    row per neighbour, rank 0-based within the query's (distance, id)-ordered
+    list, distance the rooted double printed with 17 significant digits (round
+    trips exactly).  The reference pins the columns, not rank base or number
+    format.  Returns the number of rows written."""
+    ids = np.asarray(ids.cpu() if _is_torch(ids) else ids)
+    dist = np.asarray(distances.cpu() if _is_torch(distances) else distances, dtype=np.float64)
+    lens = np.asarray(lens.cpu() if _is_torch(lens) else lens)
+    qids = np.arange(len(lens)) if query_ids is None else np.asarray(query_ids)
+    rows = 0
+    with open(path, "w") as f:
+        f.write("query_id,rank,neighbor_id,distance\n")
+        for q in range(len(lens)):
+            for r in range(int(lens[q])):
+                f.write(f"{int(qids[q])},{r},{int(ids[q, r])},{float(dist[q, r]):.17g}\n")
+                rows += 1
+    return rows
+
+
+def read_search_csv(path: str):
+    """Parse write_search_csv output: list of (query_id, rank, neighbor_id, distance)."""
+    out = []
+    with open(path) as f:
+        header = f.readline().strip()
+        if header != "query_id,rank,neighbor_id,distance":
+            raise HcgInvalidArgument(-1, f"{path}: not a search CSV")
+        for line in f:
+            a, b, c, d = line.strip().split(",")
+            out.append((int(a), int(b), int(c), float(d)))
+    return out
+
+
 __all__ = [
     "View", "RAW", "LIFTED", "ProjectionScheme", "default_scheme", "SearchParams", "Neighbor",
     "MulticurvesIndex", "merge_packed", "binomial_tail", "miss_bound", "plan_depth",
+    "write_search_csv", "read_search_csv",
     "shard_probe_depth", "gen_rows", "gen_queries", "make_lut", "recall_at", "ZORDER", "HILBERT",
     "read_vectors", "write_vectors",
 ]

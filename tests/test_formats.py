@@ -89,3 +89,19 @@ def test_float_fvecs_round_trip_and_reference_reader(tmp_path):
         H.read_vectors(str(p), "fvecs", dtype="f32")
     with pytest.raises(H.HcgInvalidArgument):
         H.read_vectors(path, "bvecs", dtype="f32")
+
+
+def test_search_csv_round_trip(tmp_path):
+    """cmd_search's `query_id,rank,neighbor_id,distance` rows (SPEC.md:531-533):
+    one row per neighbour in list order; doubles round-trip exactly."""
+    ids = np.array([[7, 3, 2**64 - 1], [1, 2, 5]], np.uint64)
+    d = np.array([[0.0, np.sqrt(2.0), np.inf], [1.0 / 3, 2.5, 1e-300]])
+    lens = np.array([2, 3], np.uint32)
+    p = str(tmp_path / "r.csv")
+    assert H.write_search_csv(p, ids, d, lens, query_ids=[10, 11]) == 5
+    rows = H.read_search_csv(p)
+    assert [r[:3] for r in rows] == [(10, 0, 7), (10, 1, 3), (11, 0, 1), (11, 1, 2), (11, 2, 5)]
+    assert [r[3] for r in rows] == [0.0, np.sqrt(2.0), 1.0 / 3, 2.5, 1e-300]
+    (tmp_path / "bad.csv").write_text("a,b\n")
+    with pytest.raises(H.HcgInvalidArgument):
+        H.read_search_csv(str(tmp_path / "bad.csv"))
