@@ -468,6 +468,26 @@ def plan_depth(Phi: int, shards: int, target: float) -> int:
     return int(lib().hcg_plan_depth(Phi, shards, target))
 
 
+def monte_carlo_miss(Phi: int, shards: int, phi: int, trials: int, seed: int = 0) -> float:
+    """fraction of trials in which two independent
+    Multinomial(Phi, uniform over `shards`) allocations (the two halves of the
+    sequential window) put more than phi entries into some shard.  Validates
+    miss_bound empirically (§4.2 proof model)."""
+    if trials < 1:
+        raise HcgInvalidArgument(-1, "trials must be >= 1")
+    rng = np.random.default_rng(seed)
+    p = np.full(shards, 1.0 / shards)
+    misses = 0
+    left = trials
+    while left:
+        b = min(left, 1 << 18)
+        lo = rng.multinomial(Phi, p, size=b)
+        hi = rng.multinomial(Phi, p, size=b)
+        misses += int(((lo > phi).any(axis=1) | (hi > phi).any(axis=1)).sum())
+        left -= b
+    return misses / trials
+
+
 def shard_probe_depth(depth: int, shards: int, target: float = 0.02) -> int:
     """Per-shard probe depth 2*phi* for a sequential depth D (Phi = ceil(D/2),
     SPEC.md:329) at a miss-probability target."""
@@ -539,7 +559,7 @@ def read_search_csv(path: str):
 __all__ = [
     "View", "RAW", "LIFTED", "ProjectionScheme", "default_scheme", "SearchParams", "Neighbor",
     "MulticurvesIndex", "merge_packed", "binomial_tail", "miss_bound", "plan_depth",
-    "write_search_csv", "read_search_csv",
+    "write_search_csv", "read_search_csv", "monte_carlo_miss",
     "shard_probe_depth", "gen_rows", "gen_queries", "make_lut", "recall_at", "ZORDER", "HILBERT",
     "read_vectors", "write_vectors",
 ]
