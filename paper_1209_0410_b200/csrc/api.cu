@@ -33,6 +33,8 @@ struct hcg_index {
     hcg::CurveDev* d_curves = nullptr;
     std::vector<uint64_t*> keys;
     std::vector<uint32_t*> slots;
+    std::vector<uint64_t*> samples;  // per curve: every kSampleStride-th key (locate's upper levels)
+    std::vector<uint64_t> sample_bytes;
     uint32_t** d_slot_ptrs = nullptr;
     uint64_t bytes = 0;
 };
@@ -205,6 +207,7 @@ void release(hcg_index* ix) {
     cudaFree(ix->d_slot_ptrs);
     for (auto* p : ix->keys) cudaFree(p);
     for (auto* p : ix->slots) cudaFree(p);
+    for (auto* p : ix->samples) cudaFree(p);
     delete ix;
 }
 
@@ -477,6 +480,25 @@ hcg_status reorder_rows(hcg_index* ix, cudaStream_t st) {
 }
 
 hcg_status publish_tables(hcg_index* ix, cudaStream_t st) {
+    // sampled keys for the two-level lower_bound (derived data, rebuilt here)
+    ix->samples.resize(ix->C, nullptr);
+    ix->sample_bytes.resize(ix->C, 0);
+    for (uint32_t c = 0; c < ix->C; ++c) {
+        CurveDev& cv = ix->curves[c];
+        dev_free(ix->samples[c], ix->sample_bytes[c], &ix->bytes);
+        ix->samples[c] = nullptr;
+        ix->sample_bytes[c] = 0;
+        cv.samples = nullptr;
+        cv.n_samples = 0;
+        if (ix->n < 4 * uint64_t(kSampleStride) || !ix->keys[c]) continue;
+        const uint64_t ns = (ix->n + kSampleStride - 1) / kSampleStride;
+        HCG_TRY(dev_alloc(&ix->samples[c], size_t(ns) * cv.ws, &ix->bytes));
+        ix->sample_bytes[c] = size_t(ns) * cv.ws * 8;
+        launch_sample(ix->keys[c], ns, cv.ws, ix->samples[c], st);
+        HCG_TRY(check_launch("key samples"));
+        cv.samples = ix->samples[c];
+        cv.n_samples = uint32_t(ns);
+    }
     uint32_t maxws = 1;
     for (auto& cv : ix->curves) maxws = std::max(maxws, cv.ws);
     ix->wsmax = pow2_bucket(maxws, 1, 16);

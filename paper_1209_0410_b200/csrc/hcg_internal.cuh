@@ -50,7 +50,10 @@ struct CurveDev {
     uint32_t w;     // full key words = ceil(dims * m / 64)
     uint32_t dims;  // projected dimensions feeding this curve
     uint32_t off;   // offset of this curve's slots in the assignment table
+    const uint64_t* samples;  // every kSampleStride-th key (ws words each): the L2-resident upper levels
+    uint32_t n_samples;
 };
+constexpr uint32_t kSampleStride = 64;
 
 // ---------------------------------------------------------------- keys ----
 // Skilling's axes->transpose on m-bit coordinates held in registers; the
@@ -105,9 +108,67 @@ __device__ __forceinline__ void key_shl(uint64_t (&k)[WMAX], int s) {
 // Curve key of one projected point: plane j (MSB first) of coordinate i lands
 // at key bit width-1-(j*d+i) (reference: proj/src/curve.cpp:62-75).
 // cells: the m-bit quantized coordinates (LUT output).
+// The default scheme's shape, 16 dims per curve at m = 8 or 16, with the
+// loops unrolled at compile time: the Skilling transform on constants and the
+// bit-plane interleave as a 16 x 16 bit-matrix transpose (4 block-swap
+// stages) -- T[b] bit i = bit b of x[i]; plane b = brev16(T[b]) sits at key
+// bits [16 b, 16 b + 16), the same key as the generic loop below.
+template <int M, int WMAX>
+__device__ __forceinline__ void make_key_d16(uint32_t (&x)[16], int kind, uint64_t (&key)[WMAX]) {
+    if (kind == HCG_HILBERT) {
+#pragma unroll
+        for (uint32_t q = 1u << (M - 1); q > 1; q >>= 1) {
+            const uint32_t low = q - 1;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const bool set = (x[i] & q) != 0;
+                const uint32_t t = (x[0] ^ x[i]) & low;
+                const uint32_t x0 = x[0] ^ (set ? low : t);
+                if (i != 0) x[i] ^= set ? 0u : t;
+                x[0] = x0;
+            }
+        }
+#pragma unroll
+        for (int i = 1; i < 16; ++i) x[i] ^= x[i - 1];
+        uint32_t fix = 0;
+#pragma unroll
+        for (uint32_t q = 1u << (M - 1); q > 1; q >>= 1) fix ^= (x[15] & q) ? q - 1 : 0u;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) x[i] ^= fix;
+    }
+#pragma unroll
+    for (int j = 8; j >= 1; j >>= 1) {
+        const uint32_t mask = j == 8 ? 0x00FFu : j == 4 ? 0x0F0Fu : j == 2 ? 0x3333u : 0x5555u;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            if (i & j) continue;
+            const uint32_t t = ((x[i] >> j) ^ x[i + j]) & mask;
+            x[i] ^= t << j;
+            x[i + j] ^= t;
+        }
+    }
+#pragma unroll
+    for (int w = 0; w < WMAX; ++w) key[w] = 0;
+#pragma unroll
+    for (int b = 0; b < M; ++b) {
+        const uint64_t plane = __brev(x[b]) >> 16;
+        if (b / 4 < WMAX) key[b / 4] |= plane << (16 * (b % 4));
+    }
+}
+
 template <int DMAX, int WMAX>
 __device__ __forceinline__ void make_key(uint32_t (&x)[DMAX], int d, int m, int kind,
                                          uint64_t (&key)[WMAX]) {
+    if constexpr (DMAX == 16 && WMAX >= 4) {
+        if (d == 16 && m == 16) {
+            make_key_d16<16, WMAX>(x, kind, key);
+            return;
+        }
+        if (d == 16 && m == 8) {
+            make_key_d16<8, WMAX>(x, kind, key);
+            return;
+        }
+    }
     if (kind == HCG_HILBERT && d > 1) hilbert_transpose<DMAX>(x, d, m);
 #pragma unroll
     for (int w = 0; w < WMAX; ++w) key[w] = 0;

@@ -116,6 +116,24 @@ __global__ void __launch_bounds__(128, MINB) k_locate(LocateArgs a) {
             lo += __popc(__ballot_sync(kFull, less));
         } else {
             uint64_t len = a.n;
+            if (cv.samples) {
+                // two levels: lower_bound over the sampled keys (small, L2-resident),
+                // then within one stride of the full array (a few DRAM sectors)
+                uint64_t j = 0, sl = cv.n_samples;
+                while (sl > 0) {
+                    const uint64_t half = sl >> 1;
+                    if (suffix_cmp<WSMAX>(cv.samples + (j + half) * wsu, qs, ws) < 0) {
+                        j += half + 1;
+                        sl -= half + 1;
+                    } else {
+                        sl = half;
+                    }
+                }
+                // keys at positions <= (j-1)*S are < qs; the key at j*S (if any) is >= qs
+                lo = j == 0 ? 0 : (j - 1) * kSampleStride + 1;
+                const uint64_t hi = j * kSampleStride < a.n ? j * kSampleStride : a.n;
+                len = hi > lo ? hi - lo : 0;
+            }
             while (len > 0) {
                 const uint64_t half = len >> 1;
                 const uint64_t mid = lo + half;

@@ -269,6 +269,11 @@ def test_large_batch_paths(view, m, k):
     gi = H.MulticurvesIndex(rows, H.default_scheme(128, 8, m), view)
     oi = _oracle(rows, view, 8, m, H.HILBERT)
     _check_search(gi, oi, view, qs, k, 350)
+    if k == 10:  # the sorted two-phase locate of large batches
+        r, b, e = gi.windows(qs, 350)
+        orr, ob, oe = oi.windows(view.floats(qs), 350)
+        np.testing.assert_array_equal(r, orr)
+        np.testing.assert_array_equal(b, ob)
 
 
 def test_concurrent_searches_from_threads():
