@@ -490,11 +490,14 @@ hcg_status publish_tables(hcg_index* ix, cudaStream_t st) {
         ix->sample_bytes[c] = 0;
         cv.samples = nullptr;
         cv.n_samples = 0;
-        if (ix->n < 4 * uint64_t(kSampleStride) || !ix->keys[c]) continue;
-        const uint64_t ns = (ix->n + kSampleStride - 1) / kSampleStride;
+        static const uint32_t stride = getenv("HCG_SAMPLE_STRIDE") ? uint32_t(atoi(getenv("HCG_SAMPLE_STRIDE")))
+                                                                   : kSampleStride;
+        if (stride < 2 || ix->n < 4 * uint64_t(stride) || !ix->keys[c]) continue;
+        const uint64_t ns = (ix->n + stride - 1) / stride;
         HCG_TRY(dev_alloc(&ix->samples[c], size_t(ns) * cv.ws, &ix->bytes));
         ix->sample_bytes[c] = size_t(ns) * cv.ws * 8;
-        launch_sample(ix->keys[c], ns, cv.ws, ix->samples[c], st);
+        cv.sample_stride = stride;
+        launch_sample(ix->keys[c], ns, cv.ws, stride, ix->samples[c], st);
         HCG_TRY(check_launch("key samples"));
         cv.samples = ix->samples[c];
         cv.n_samples = uint32_t(ns);

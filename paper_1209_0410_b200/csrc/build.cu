@@ -281,11 +281,12 @@ __global__ void k_map(uint32_t* __restrict__ v, uint64_t n, const uint32_t* __re
 }
 
 // samples[j] = keys[j * kSampleStride] (ws words each)
-__global__ void k_sample(const uint64_t* __restrict__ keys, uint64_t n_samples, uint32_t ws, uint64_t* __restrict__ out) {
+__global__ void k_sample(const uint64_t* __restrict__ keys, uint64_t n_samples, uint32_t ws, uint32_t stride,
+                         uint64_t* __restrict__ out) {
     const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n_samples * ws) return;
     const uint64_t j = i / ws, w = i - j * ws;
-    out[i] = keys[j * kSampleStride * ws + w];
+    out[i] = keys[j * stride * ws + w];
 }
 
 __global__ void k_iota(uint32_t* v, uint64_t n, uint32_t base) {
@@ -435,8 +436,9 @@ void launch_map(uint32_t* v, uint64_t n, const uint32_t* map, cudaStream_t st) {
     if (n) k_map<<<blocks_for(n, 256), 256, 0, st>>>(v, n, map);
 }
 
-void launch_sample(const uint64_t* keys, uint64_t n_samples, uint32_t ws, uint64_t* out, cudaStream_t st) {
-    if (n_samples) k_sample<<<blocks_for(n_samples * ws, 256), 256, 0, st>>>(keys, n_samples, ws, out);
+void launch_sample(const uint64_t* keys, uint64_t n_samples, uint32_t ws, uint32_t stride, uint64_t* out,
+                   cudaStream_t st) {
+    if (n_samples) k_sample<<<blocks_for(n_samples * ws, 256), 256, 0, st>>>(keys, n_samples, ws, stride, out);
 }
 void launch_iota(uint32_t* v, uint64_t n, uint32_t base, cudaStream_t st) {
     if (n) k_iota<<<blocks_for(n, 256), 256, 0, st>>>(v, n, base);

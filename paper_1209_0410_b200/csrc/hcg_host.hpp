@@ -36,7 +36,8 @@ void launch_permute_rows(const uint8_t* src, const uint32_t* perm, uint64_t n, u
                          cudaStream_t st);
 void launch_invert(const uint32_t* perm, uint64_t n, uint32_t* inv, cudaStream_t st);
 void launch_map(uint32_t* v, uint64_t n, const uint32_t* map, cudaStream_t st);
-void launch_sample(const uint64_t* keys, uint64_t n_samples, uint32_t ws, uint64_t* out, cudaStream_t st);
+void launch_sample(const uint64_t* keys, uint64_t n_samples, uint32_t ws, uint32_t stride, uint64_t* out,
+                   cudaStream_t st);
 void launch_iota(uint32_t* v, uint64_t n, uint32_t base, cudaStream_t st);
 void launch_offset(const uint32_t* in, uint32_t* out, uint64_t n, uint32_t base, cudaStream_t st);
 void launch_rank_merge(const uint64_t* ak, const uint32_t* as, uint64_t na, const uint64_t* bk, const uint32_t* bs,

@@ -130,8 +130,9 @@ __global__ void __launch_bounds__(128, MINB) k_locate(LocateArgs a) {
                     }
                 }
                 // keys at positions <= (j-1)*S are < qs; the key at j*S (if any) is >= qs
-                lo = j == 0 ? 0 : (j - 1) * kSampleStride + 1;
-                const uint64_t hi = j * kSampleStride < a.n ? j * kSampleStride : a.n;
+                const uint64_t S = cv.sample_stride;
+                lo = j == 0 ? 0 : (j - 1) * S + 1;
+                const uint64_t hi = j * S < a.n ? j * S : a.n;
                 len = hi > lo ? hi - lo : 0;
             }
             while (len > 0) {
