@@ -1123,8 +1123,10 @@ hcg_status refine_dispatch(const RefineArgs& a_in, void* scratch, size_t* scratc
         HCG_RET_IF(radix_sort_pairs(&k0, &v0, &k1, &v1, a_in.nq, dmask, cnt, totals, st));
         qorder = v0;
     }
-    // 4 CTAs/SM: measured best (5-6 spill and lose ~15 %)
-    auto gk = k_gather<R, CR, R <= 4 ? 4 : 2>;
+    // 3 CTAs/SM (72 registers): with rows and batches in curve-0 order fewer
+    // queries in flight share more of their rows in L2 -- 4.70 ms vs 4.89 at
+    // 4 CTAs/SM (1-2: 4.70, 5: spills); before the reorder 4 was best
+    auto gk = k_gather<R, CR, R <= 4 ? 3 : 2>;
     static bool cfg_u[64] = {};
     if (smem_union) HCG_RET_IF(opt_in_smem(k_union, device, cfg_u));
     int g_per_sm = 1;
