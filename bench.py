@@ -398,6 +398,12 @@ def run_ours(a):
                 "bytes_per_query_B_q": round(bytes_q, 1),
                 "unique_candidates_per_query": round(float(U.mean()), 1),
                 "step_hbm_gbs": round(Q * a.steps / (ms_total * 1e-3) * bytes_q / 1e9, 1),
+                # frac can exceed 1: the algorithmic bytes count every candidate row as a
+                # DRAM read, while rows stored and queried in curve-0 order are partly
+                # served from L2 (see traffic); dram_gbs is the ncu DRAM traffic per launch
+                # over this run's launch time
+                "dram_gbs": (round(traffic["traffic_bytes"] / (gather_ms * 1e-3) / 1e9, 1)
+                             if isinstance(traffic, dict) and traffic.get("traffic_bytes") else None),
             },
             "cpu_baseline": cpu,
             "parity_vs_reference": parity,
