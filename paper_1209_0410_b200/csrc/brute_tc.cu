@@ -407,12 +407,14 @@ int device_sms() {
 template <int KT>
 hcg_status launch_tc(const BruteArgs& a, const TcPlan& p, const CUtensorMap& mq, const CUtensorMap& mx,
                      const uint32_t* xn, uint64_t* part, cudaStream_t st) {
-    static bool cfg = false;
-    if (!cfg) {
+    static bool cfg[64] = {};  // the opt-in is per device
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 64 || !cfg[dev]) {
         if (cudaFuncSetAttribute(k_brute_tc<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemBytes)) !=
             cudaSuccess)
             return set_error(HCG_ECUDA, "brute_tc: shared memory opt-in failed");
-        cfg = true;
+        if (dev < 64) cfg[dev] = true;
     }
     k_brute_tc<KT><<<p.qtiles * p.chunks, kThreads, kSmemBytes, st>>>(mq, mx, a.queries, xn, a.nq, a.n, a.k, p.chunks,
                                                                        p.tiles_per_chunk, part, a.idtab);
