@@ -309,3 +309,17 @@ def test_concurrent_searches_from_threads():
     for i in range(4):
         for a, b in zip(got[i], want[i]):
             np.testing.assert_array_equal(a, b)
+
+
+def test_chunked_batches_match_small_batches():
+    """A batch whose candidate lists exceed the 2 GB list budget is searched
+    in chunks (no batch order); results equal searching slices of it."""
+    import torch
+    n, nq, depth = 200_000, 60_000, 2000  # 8 curves x 2000 -> 16K ids per query: 3 chunks
+    rows = H.gen_rows(0, n)
+    qs = H.gen_queries(0, nq, n)
+    gi = H.MulticurvesIndex(rows, H.default_scheme(128, 8, 16), H.LIFTED)
+    ids, sq, ln = gi.search_batch(qs, 10, depth)
+    for s in (0, 25_000, 59_000):
+        i2, s2, l2 = gi.search_batch(qs[s:s + 1000].contiguous(), 10, depth)
+        assert torch.equal(ids[s:s + 1000], i2) and torch.equal(sq[s:s + 1000], s2) and torch.equal(ln[s:s + 1000], l2)
