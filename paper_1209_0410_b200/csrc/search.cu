@@ -1057,9 +1057,13 @@ hcg_status union_reg_dispatch(const RefineArgs& a, uint32_t* lists, uint32_t* co
     return union_reg_launch<32, NT>(a, lists, counts, lstride, tb, device, st);
 }
 
-// 256-thread CTAs measured best (128: +15 %, 512: +18 %, 1024: +75 % union time).
+// 256-thread CTAs measured best at T = 2800 (128: +15 %, 512: +18 %, 1024: +75 % union time).
 hcg_status launch_union_reg(const RefineArgs& a, uint32_t* lists, uint32_t* counts, uint32_t lstride, uint32_t tb,
                             int device, cudaStream_t st) {
+    // small candidate sets (the sharded per-shard depths): 128-thread CTAs,
+    // union at T = 640 / 1072 / 1808: 0.42 / 0.67 / 1.06 ms vs 0.55 / 0.73 /
+    // 0.98 ms with 256 threads
+    if (a.C * a.take <= 1280 && 128 % a.C == 0) return union_reg_dispatch<128>(a, lists, counts, lstride, tb, device, st);
     return union_reg_dispatch<256>(a, lists, counts, lstride, tb, device, st);
 }
 
