@@ -1,0 +1,90 @@
+"""Randomised parity: schemes, sizes, depths, k and views drawn at random
+(seeded), each search bit-exact against the oracle.  Reaches the rarely used
+paths (uneven assignments, wide keys, JMAX 16-32 unions, shared-memory and
+global-table unions, 128-thread unions, CTA and warp gathers, k up to 256)."""
+import numpy as np
+import pytest
+
+from oracle import pyoracle as P
+from hcg_testutil import gpu_available
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device")]
+
+import paper_1209_0410_b200 as H  # noqa: E402
+
+
+def _random_scheme(rng, d_full, curves):
+    perm = rng.permutation(d_full)
+    cuts = np.sort(rng.choice(np.arange(1, d_full), curves - 1, replace=False)) if curves > 1 else []
+    parts = np.split(perm, cuts)
+    return [sorted(int(x) for x in p) for p in parts]
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_random_configurations(seed):
+    rng = np.random.default_rng(1000 + seed)
+    d_full = int(rng.choice([16, 24, 64, 100, 128]))
+    m = int(rng.choice([4, 8, 12, 16]))
+    curves = int(rng.integers(1, min(d_full, 16) + 1))
+    assignment = _random_scheme(rng, d_full, curves)
+    if max(len(a) for a in assignment) * m > 1024 or max(len(a) for a in assignment) > 128:
+        pytest.skip("key wider than HC_MAX_KEY_BITS")
+    kind = int(rng.integers(0, 2))
+    view = H.LIFTED if rng.random() < 0.5 else H.RAW
+    n = int(rng.integers(1, 30_000))
+    nq = int(rng.choice([1, 7, 300, 3000, 5000]))
+    depth = int(rng.choice([1, 3, 50, 350, 1000, 3000]))
+    k = int(rng.choice([1, 10, 33, 100, 256]))
+    rows = rng.integers(0, 256, (n, d_full), dtype=np.uint8)
+    if n > 50:
+        rows[n // 2:n // 2 + 20] = rows[0]  # ties
+    qs = rng.integers(0, 256, (nq, d_full), dtype=np.uint8)
+    scheme = H.ProjectionScheme(d_full, m, kind, 0, assignment)
+    gi = H.MulticurvesIndex(rows, scheme, view)
+    off = np.cumsum([0] + [len(a) for a in assignment]).astype(np.uint32)
+    asg = np.concatenate([np.asarray(a, np.uint32) for a in assignment])
+    oi = P.Oracle(view.floats(rows), curves, m, kind, off=off, assign=asg)
+    ids, sq, ln = gi.search_batch(qs, k, depth)
+    oids, odist, oln = oi.search(view.floats(qs), k, depth)
+    np.testing.assert_array_equal(ln, oln)
+    d = gi.rooted(sq)
+    for q in range(nq):
+        L = int(ln[q])
+        np.testing.assert_array_equal(ids[q, :L], oids[q, :L])
+        assert d[q, :L].tobytes() == odist[q, :L].tobytes()
+    for q in range(min(nq, 3)):
+        np.testing.assert_array_equal(gi.candidates(qs[q], depth)[0], oi.candidates(view.floats(qs[q]), depth))
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_configurations_f32(seed):
+    """The same over float rows: keys / candidates exact, ids exact, distances
+    within 1e-12 relative (tree vs sequential double sums)."""
+    rng = np.random.default_rng(5000 + seed)
+    d_full = int(rng.choice([16, 24, 64, 100, 128]))
+    m = int(rng.choice([8, 16, 32]))
+    curves = int(rng.integers(1, min(d_full, 16) + 1))
+    assignment = _random_scheme(rng, d_full, curves)
+    if max(len(a) for a in assignment) * m > 1024:
+        pytest.skip("key wider than HC_MAX_KEY_BITS")
+    kind = int(rng.integers(0, 2))
+    n = int(rng.integers(1, 20_000))
+    nq = int(rng.choice([1, 64, 3000, 17_000]))
+    depth = int(rng.choice([1, 50, 350, 2000]))
+    k = int(rng.choice([1, 10, 64]))
+    rows = (rng.standard_normal((n, d_full)) * rng.choice([1e-3, 1.0, 1e3])).astype(np.float32)
+    qs = (rng.standard_normal((nq, d_full)) * 1.0).astype(np.float32)
+    scheme = H.ProjectionScheme(d_full, m, kind, 0, assignment)
+    gi = H.MulticurvesIndex(rows, scheme)
+    off = np.cumsum([0] + [len(a) for a in assignment]).astype(np.uint32)
+    asg = np.concatenate([np.asarray(a, np.uint32) for a in assignment])
+    oi = P.Oracle(rows, curves, m, kind, off=off, assign=asg)
+    ids, sq, ln = gi.search_batch(qs, k, depth)
+    oids, odist, oln = oi.search(qs, k, depth)
+    np.testing.assert_array_equal(ln, oln)
+    d = gi.rooted(sq)
+    for q in range(nq):
+        L = int(ln[q])
+        np.testing.assert_array_equal(ids[q, :L], oids[q, :L])
+        np.testing.assert_allclose(d[q, :L], odist[q, :L], rtol=1e-12, atol=0)
