@@ -348,6 +348,22 @@ struct WarpTopK {
             m &= __ballot_sync(kFull, cand < thr);
         }
     }
+
+    // offer() for candidate streams that may repeat a value (the same row
+    // reached through two curves): a value already held is not inserted again.
+    __device__ __forceinline__ void offer_unique(uint64_t cand, int lane) {
+        unsigned m = __ballot_sync(kFull, cand < thr);
+        while (m) {
+            const int src = __ffs(m) - 1;
+            const uint64_t x = __shfl_sync(kFull, cand, src);
+            bool held = false;
+#pragma unroll
+            for (int r = 0; r < R; ++r) held |= a[r] == x;
+            if (!__any_sync(kFull, held)) insert(x, lane);
+            m &= ~(1u << src);
+            m &= __ballot_sync(kFull, cand < thr);
+        }
+    }
 };
 
 // Warp top-k over (u64 key, u32 slot) pairs for f32 indexes: key = the bits of

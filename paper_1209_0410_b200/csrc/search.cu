@@ -476,6 +476,88 @@ __device__ __forceinline__ void gather_list(const RefineArgs& a, const uint32_t*
     }
 }
 
+// K3c without the union (k <= 32, rows in curve-0 order): the warp walks the
+// query's C windows directly -- entry e is position e % take of curve
+// e / take -- and offers every row; a row reached through two curves gives
+// the same (distance, id) key twice and offer_unique keeps one.  Costs the
+// duplicate rows (~16 % of the windows, partly L2 hits) instead of the union
+// kernel and the lists' round trip.
+template <int R, int CR>
+__device__ __forceinline__ void gather_windows(const RefineArgs& a, const uint32_t* begins_q, const uint4 (&qv)[CR],
+                                               int lane, WarpTopK<R>& tk) {
+    const int l8 = lane & 7, grp = lane >> 3;
+    const uint32_t chunks = a.pitch >> 4;
+    const uint32_t take = a.take, n = a.C * take;
+    // (curve, position) of this lane-group's 8 entries, advanced by 32 per pass
+    uint32_t cc[8], pp[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+        const uint32_t e = uint32_t(grp * 8 + r);
+        cc[r] = e / take;
+        pp[r] = e - cc[r] * take;
+    }
+    auto entry = [&](int r) -> uint32_t {
+        return cc[r] < a.C ? __ldg(a.slots[cc[r]] + __ldg(begins_q + cc[r]) + pp[r]) : kEmpty;
+    };
+    uint32_t nx[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) nx[r] = entry(r);
+    for (uint32_t base = 0; base < n; base += 32) {
+        uint4 v[8][CR];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+#pragma unroll
+            for (int t = 0; t < CR; ++t) {
+                const uint32_t ch = l8 + 8 * t;
+                v[r][t] = (nx[r] != kEmpty && ch < chunks) ? ldg_stream(a.rows + uint64_t(nx[r]) * a.pitch + ch * 16)
+                                                           : make_uint4(0, 0, 0, 0);
+            }
+        }
+        uint32_t me = nx[0];
+#pragma unroll
+        for (int r = 1; r < 8; ++r)
+            if (r == l8) me = nx[r];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            pp[r] += 32;
+            while (pp[r] >= take && cc[r] < a.C) {
+                pp[r] -= take;
+                ++cc[r];
+            }
+            nx[r] = entry(r);
+        }
+        uint32_t acc[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            acc[r] = 0;
+#pragma unroll
+            for (int t = 0; t < CR; ++t) acc[r] = sad2_16(v[r][t], qv[t], acc[r]);
+        }
+        const bool b2 = l8 & 4, b1 = l8 & 2, b0 = l8 & 1;
+        uint32_t s4[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const uint32_t send = b2 ? acc[i] : acc[i + 4];
+            const uint32_t keep = b2 ? acc[i + 4] : acc[i];
+            s4[i] = keep + __shfl_xor_sync(kFull, send, 4);
+        }
+        uint32_t s2[2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const uint32_t send = b1 ? s4[i] : s4[i + 2];
+            const uint32_t keep = b1 ? s4[i + 2] : s4[i];
+            s2[i] = keep + __shfl_xor_sync(kFull, send, 2);
+        }
+        const uint32_t S = (b0 ? s2[1] : s2[0]) + __shfl_xor_sync(kFull, b0 ? s2[0] : s2[1], 1);
+        uint32_t sl = me;
+        if (a.idtab) {
+            const bool pre = me != kEmpty && S <= uint32_t(tk.thr >> 32);
+            if (__any_sync(kFull, pre) && pre) sl = __ldg(a.idtab + me);
+        }
+        tk.offer_unique(me != kEmpty ? ((uint64_t(S) << 32) | sl) : kNone, lane);
+    }
+}
+
 template <int CR>
 __device__ __forceinline__ void load_query(const RefineArgs& a, uint32_t q, int lane, uint4 (&qv)[CR]) {
     const uint32_t chunks = a.pitch >> 4;
@@ -504,6 +586,28 @@ __global__ void __launch_bounds__(kRefineThreads, MINB) k_gather(RefineArgs a, c
         tk.init(int(a.k));
         gather_list<R, CR>(a, lists + uint64_t(q) * lstride, n, 0, 32, qv, lane, tk);
         write_result<R>(a, qq, tk, lane, n);
+    }
+}
+
+// K3c without the union: one warp per query over the raw windows.
+template <int R, int CR, int MINB>
+__global__ void __launch_bounds__(kRefineThreads, MINB) k_gather_nu(RefineArgs a) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t qstep = gridDim.x * (kRefineThreads / 32);
+    for (uint32_t q = (blockIdx.x * kRefineThreads + threadIdx.x) >> 5; q < a.nq; q += qstep) {
+        const uint32_t qq = a.qorder ? __ldg(a.qorder + q) : q;
+        uint4 qv[CR];
+        load_query<CR>(a, qq, lane, qv);
+        WarpTopK<R> tk;
+        tk.init(int(a.k));
+        gather_windows<R, CR>(a, a.begins + uint64_t(qq) * a.C, qv, lane, tk);
+        uint32_t valid = 0;
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+            valid += (uint32_t(lane) * R + r < a.k && tk.a[r] != kNone) ? 1u : 0u;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) valid += __shfl_xor_sync(kFull, valid, o);
+        write_result<R>(a, qq, tk, lane, valid);
     }
 }
 
@@ -1137,6 +1241,24 @@ hcg_status refine_dispatch(const RefineArgs& a_in, void* scratch, size_t* scratc
     if (smem_union) HCG_RET_IF(opt_in_smem(k_union, device, cfg_u));
     int g_per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_per_sm, gk, kRefineThreads, 0);
+    static const bool no_union_path = getenv("HCG_NO_UNIONLESS") != nullptr;
+    if constexpr (R == 1) {
+        // k <= 32 and large batches: skip the union, walk the windows directly
+        if (!no_union_path && a_in.mode != kOutCandidates && a_in.dtype == HCG_U8 && a_in.nq >= 16384 &&
+            a_in.idtab != nullptr) {
+            RefineArgs a = a_in;
+            a.qorder = qorder;
+            auto nk = k_gather_nu<R, CR, 3>;
+            int per_sm = 1;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nk, kRefineThreads, 0);
+            const uint32_t blocks = std::min<uint32_t>((a.nq + 7) / 8, uint32_t(sms * std::max(per_sm, 1)));
+            count_launches(1);
+            nk<<<blocks, kRefineThreads, 0, st>>>(a);
+            HCG_RET_IF(check_launch("k_gather_nu"));
+            if (a.ev_mid) cudaEventRecord(a.ev_mid, st);
+            return HCG_OK;
+        }
+    }
     for (uint32_t q0 = 0; q0 < a_in.nq; q0 += chunk) {
         RefineArgs a = a_in;
         a.qorder = qorder;
