@@ -289,11 +289,22 @@ def run_ours(a):
         tg.append(mg)
     U = sidx.local.candidate_counts(batches[a.warmup], shard_depth).astype(np.float64)
     take = min(shard_depth, sidx.local.size())
-    # k_gather reads each unique row (128 B) + its list entry (4 B), the query
-    # (128 B) and the count, and writes k (id, sqdist) pairs + len.
-    bytes_gather = float(U.sum() * (128 + 4) + Q * (128 + 4 + 12 * k + 4))
-    # k_union reads C windows of ids + C begins and writes the unique list.
-    bytes_union = float(Q * (4 * C * take + 4 * C) + U.sum() * 4)
+    # Which K3c runs (the library's dispatch, search.cu refine_dispatch): for
+    # k <= 32 and batches >= 16K on a reordered index the union is skipped and
+    # k_gather_nu walks the windows; otherwise k_union_reg + k_gather.
+    unionless = k <= 32 and Q >= 16384 and os.environ.get("HCG_NO_UNIONLESS") is None
+    if unionless:
+        # k_gather_nu reads the C windows of ids, each unique row once (repeats
+        # reached through a second curve are re-reads, not algorithmic), the
+        # query, and writes k (id, sqdist) pairs + len.
+        bytes_gather = float(U.sum() * 128 + Q * (4 * C * take + 4 * C + 128 + 12 * k + 4))
+        bytes_union = 0.0
+    else:
+        # k_gather reads each unique row (128 B) + its list entry (4 B), the query
+        # (128 B) and the count, and writes k (id, sqdist) pairs + len.
+        bytes_gather = float(U.sum() * (128 + 4) + Q * (128 + 4 + 12 * k + 4))
+        # k_union reads C windows of ids + C begins and writes the unique list.
+        bytes_union = float(Q * (4 * C * take + 4 * C) + U.sum() * 4)
     gather_ms = statistics.median(tg)
     union_ms = statistics.median(tu)
     peak, peak_src = measured_peak_gbs()
@@ -388,12 +399,16 @@ def run_ours(a):
             "roofline": {
                 "bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
-                "kernel": "k_gather (gather of the unique candidate rows + exact L2 + top-k)",
+                "kernel": ("k_gather_nu (walk of the C windows + gather of their rows + exact L2 + top-k, "
+                           "repeats dropped in the top-k; no separate union)" if unionless else
+                           "k_gather (gather of the unique candidate rows + exact L2 + top-k)"),
                 "algorithmic_bytes_per_launch": bytes_gather,
                 "launch_ms": round(gather_ms, 4),
-                "other_kernels_ms": {"k_locate": round(statistics.median(tl), 4),
-                                     "k_union": round(union_ms, 4)},
-                "k_union_algorithmic_gbs": round(bytes_union / max(union_ms, 1e-9) / 1e6, 1),
+                "other_kernels_ms": ({"k_locate": round(statistics.median(tl), 4),
+                                      "batch_order_sort": round(union_ms, 4)} if unionless else
+                                     {"k_locate": round(statistics.median(tl), 4), "k_union": round(union_ms, 4)}),
+                "k_union_algorithmic_gbs": (round(bytes_union / max(union_ms, 1e-9) / 1e6, 1)
+                                            if not unionless else None),
                 "peak_source": peak_src,
                 "bytes_per_query_B_q": round(bytes_q, 1),
                 "unique_candidates_per_query": round(float(U.mean()), 1),

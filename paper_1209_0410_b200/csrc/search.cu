@@ -1252,10 +1252,10 @@ hcg_status refine_dispatch(const RefineArgs& a_in, void* scratch, size_t* scratc
             int per_sm = 1;
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nk, kRefineThreads, 0);
             const uint32_t blocks = std::min<uint32_t>((a.nq + 7) / 8, uint32_t(sms * std::max(per_sm, 1)));
+            if (a.ev_mid) cudaEventRecord(a.ev_mid, st);  // timed split: (batch order) | fused gather
             count_launches(1);
             nk<<<blocks, kRefineThreads, 0, st>>>(a);
             HCG_RET_IF(check_launch("k_gather_nu"));
-            if (a.ev_mid) cudaEventRecord(a.ev_mid, st);
             return HCG_OK;
         }
     }
