@@ -1,7 +1,8 @@
 """Randomised parity: schemes, sizes, depths, k and views drawn at random
 (seeded), each search bit-exact against the oracle.  Reaches the rarely used
 paths (uneven assignments, wide keys, JMAX 16-32 unions, shared-memory and
-global-table unions, 128-thread unions, CTA and warp gathers, k up to 256)."""
+global-table unions, 128-thread unions, CTA and warp gathers, the union-less
+gather for large batches, k up to 256)."""
 import numpy as np
 import pytest
 
@@ -88,3 +89,42 @@ def test_random_configurations_f32(seed):
         L = int(ln[q])
         np.testing.assert_array_equal(ids[q, :L], oids[q, :L])
         np.testing.assert_allclose(d[q, :L], odist[q, :L], rtol=1e-12, atol=0)
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_random_configurations_large_batch(seed):
+    """>= 16K queries with k <= 32: the union-less gather (k_gather_nu walks the
+    C windows and drops repeated candidates in the top-k) over random schemes,
+    row widths, depths (windows past both ends included) and views."""
+    rng = np.random.default_rng(9000 + seed)
+    d_full = int(rng.choice([16, 24, 64, 100, 128]))
+    m = int(rng.choice([8, 16]))
+    curves = int(rng.integers(1, min(d_full, 16) + 1))
+    assignment = _random_scheme(rng, d_full, curves)
+    if max(len(a) for a in assignment) * m > 1024:
+        pytest.skip("key wider than HC_MAX_KEY_BITS")
+    kind = int(rng.integers(0, 2))
+    view = H.LIFTED if rng.random() < 0.5 else H.RAW
+    n = int(rng.integers(1, 12_000))
+    nq = int(rng.choice([16_384, 17_001]))
+    depth = int(rng.choice([1, 3, 50, 350, 2000]))
+    k = int(rng.choice([1, 10, 32]))
+    rows = rng.integers(0, 256, (n, d_full), dtype=np.uint8)
+    if n > 50:
+        rows[n // 2:n // 2 + 20] = rows[0]  # ties and repeats across curves
+    qs = rng.integers(0, 256, (nq, d_full), dtype=np.uint8)
+    qs[:64] = rows[rng.integers(0, n, 64)]  # self queries
+    scheme = H.ProjectionScheme(d_full, m, kind, 0, assignment)
+    gi = H.MulticurvesIndex(rows, scheme, view)
+    off = np.cumsum([0] + [len(a) for a in assignment]).astype(np.uint32)
+    asg = np.concatenate([np.asarray(a, np.uint32) for a in assignment])
+    oi = P.Oracle(view.floats(rows), curves, m, kind, off=off, assign=asg)
+    ids, sq, ln = gi.search_batch(qs, k, depth)
+    oids, odist, oln = oi.search(view.floats(qs), k, depth)
+    np.testing.assert_array_equal(ln, oln)
+    d = gi.rooted(sq)
+    for q in range(nq):
+        L = int(ln[q])
+        np.testing.assert_array_equal(ids[q, :L], oids[q, :L])
+        assert d[q, :L].tobytes() == odist[q, :L].tobytes()
+        assert (ids[q, L:] == np.uint64(2**64 - 1)).all()
