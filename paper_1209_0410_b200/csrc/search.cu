@@ -1248,9 +1248,14 @@ hcg_status refine_dispatch(const RefineArgs& a_in, void* scratch, size_t* scratc
             a_in.idtab != nullptr) {
             RefineArgs a = a_in;
             a.qorder = qorder;
-            auto nk = k_gather_nu<R, CR, 3>;
+            // HCG_NU_MINB / HCG_NU_PER_SM: tuning knobs (register budget and
+            // resident CTAs per SM = queries in flight sharing L2)
+            static const int nu_minb = getenv("HCG_NU_MINB") ? atoi(getenv("HCG_NU_MINB")) : 3;
+            static const int nu_cap = getenv("HCG_NU_PER_SM") ? atoi(getenv("HCG_NU_PER_SM")) : 0;
+            auto nk = nu_minb == 2 ? k_gather_nu<R, CR, 2> : nu_minb == 4 ? k_gather_nu<R, CR, 4> : k_gather_nu<R, CR, 3>;
             int per_sm = 1;
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nk, kRefineThreads, 0);
+            if (nu_cap > 0) per_sm = std::min(per_sm, nu_cap);
             const uint32_t blocks = std::min<uint32_t>((a.nq + 7) / 8, uint32_t(sms * std::max(per_sm, 1)));
             if (a.ev_mid) cudaEventRecord(a.ev_mid, st);  // timed split: (batch order) | fused gather
             count_launches(1);
