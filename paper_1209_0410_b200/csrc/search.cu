@@ -590,11 +590,11 @@ __global__ void __launch_bounds__(kRefineThreads, MINB) k_gather(RefineArgs a, c
 }
 
 // K3c without the union: one warp per query over the raw windows.
-template <int R, int CR, int MINB>
-__global__ void __launch_bounds__(kRefineThreads, MINB) k_gather_nu(RefineArgs a) {
+template <int R, int CR, int MINB, int NT = kRefineThreads>
+__global__ void __launch_bounds__(NT, MINB) k_gather_nu(RefineArgs a) {
     const int lane = threadIdx.x & 31;
-    const uint32_t qstep = gridDim.x * (kRefineThreads / 32);
-    for (uint32_t q = (blockIdx.x * kRefineThreads + threadIdx.x) >> 5; q < a.nq; q += qstep) {
+    const uint32_t qstep = gridDim.x * (NT / 32);
+    for (uint32_t q = (blockIdx.x * NT + threadIdx.x) >> 5; q < a.nq; q += qstep) {
         const uint32_t qq = a.qorder ? __ldg(a.qorder + q) : q;
         uint4 qv[CR];
         load_query<CR>(a, qq, lane, qv);
@@ -1252,14 +1252,19 @@ hcg_status refine_dispatch(const RefineArgs& a_in, void* scratch, size_t* scratc
             // resident CTAs per SM = queries in flight sharing L2)
             static const int nu_minb = getenv("HCG_NU_MINB") ? atoi(getenv("HCG_NU_MINB")) : 3;
             static const int nu_cap = getenv("HCG_NU_PER_SM") ? atoi(getenv("HCG_NU_PER_SM")) : 0;
-            auto nk = nu_minb == 2 ? k_gather_nu<R, CR, 2> : nu_minb == 4 ? k_gather_nu<R, CR, 4> : k_gather_nu<R, CR, 3>;
+            // HCG_NU_MINB=6: 128-thread CTAs, 6 per SM (same 24 warps, finer tail)
+            const int nt = nu_minb == 6 ? 128 : kRefineThreads;
+            auto nk = nu_minb == 2   ? k_gather_nu<R, CR, 2>
+                      : nu_minb == 4 ? k_gather_nu<R, CR, 4>
+                      : nu_minb == 6 ? k_gather_nu<R, CR, 6, 128>
+                                     : k_gather_nu<R, CR, 3>;
             int per_sm = 1;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nk, kRefineThreads, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nk, nt, 0);
             if (nu_cap > 0) per_sm = std::min(per_sm, nu_cap);
-            const uint32_t blocks = std::min<uint32_t>((a.nq + 7) / 8, uint32_t(sms * std::max(per_sm, 1)));
+            const uint32_t blocks = std::min<uint32_t>((a.nq + nt / 32 - 1) / (nt / 32), uint32_t(sms * std::max(per_sm, 1)));
             if (a.ev_mid) cudaEventRecord(a.ev_mid, st);  // timed split: (batch order) | fused gather
             count_launches(1);
-            nk<<<blocks, kRefineThreads, 0, st>>>(a);
+            nk<<<blocks, nt, 0, st>>>(a);
             HCG_RET_IF(check_launch("k_gather_nu"));
             return HCG_OK;
         }
