@@ -1242,9 +1242,10 @@ hcg_status refine_dispatch(const RefineArgs& a_in, void* scratch, size_t* scratc
     int g_per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_per_sm, gk, kRefineThreads, 0);
     static const bool no_union_path = getenv("HCG_NO_UNIONLESS") != nullptr;
-    if constexpr (R == 1) {
+    static const bool nu_r2 = getenv("HCG_NU_R2") != nullptr;  // A/B: union-less for 32 < k <= 64
+    if constexpr (R <= 2) {
         // k <= 32 and large batches: skip the union, walk the windows directly
-        if (!no_union_path && a_in.mode != kOutCandidates && a_in.dtype == HCG_U8 && a_in.nq >= 16384 &&
+        if (!no_union_path && (R == 1 || nu_r2) && a_in.mode != kOutCandidates && a_in.dtype == HCG_U8 && a_in.nq >= 16384 &&
             a_in.idtab != nullptr) {
             RefineArgs a = a_in;
             a.qorder = qorder;
