@@ -240,6 +240,52 @@ hcg_status hcg_brute_force_f32(const hcg_index* index, const float* queries, uin
                                uint64_t* out_ids, double* out_sqdist, uint32_t* out_len,
                                void* stream);
 
+/* ---- sharded search over G GPUs: the hypershard module (
+ * PAPER.md:743-822) ----
+ * Global id i lives on shard i mod G at local slot i / G (partition,
+ * SPEC.md:357-365).  A search gives every shard the whole query batch
+ * (broadcast), runs each shard's search at the per-shard
+ * probe depth (IHLS stage; depth from hcg_plan_depth), all-gathers
+ * the packed (sqdist << 32 | id) top-k lists with NCCL over NVLink
+ * (B x k x 8 bytes per shard) and merges them by (distance, id), truncated to
+ * k (aggregate).  Results equal the reference's sharded
+ * search: per-shard MulticurvesIndex::search then the aggregate merge.
+ * u8 indexes only (ids < 2^32).  NCCL is loaded at run time (an already
+ * loaded libnccl.so.2 first, then $HCG_NCCL_LIB, then the system's). */
+typedef struct hcg_shard_group hcg_shard_group;
+typedef struct hcg_nccl_id { char internal[128]; } hcg_nccl_id; /* an ncclUniqueId */
+
+/* One process driving G GPUs: shard r is built on devices[r] from rows
+ * r, r + G, ... of `rows` (n_total x d_full bytes, host or device memory);
+ * communicators from ncclCommInitAll.  Results land on devices[0]. */
+hcg_status hcg_shard_group_build(const hcg_scheme* scheme, const uint8_t* rows, uint64_t n_total, uint32_t G,
+                                 const int* devices, hcg_shard_group** out);
+/* The same over G already-built shards (shard r built with id_base r,
+ * id_stride G, one per device); the group takes ownership on success. */
+hcg_status hcg_shard_group_adopt(uint32_t G, hcg_index* const* shards, hcg_shard_group** out);
+/* One process per GPU: rank `rank` of G joins with its local shard (id_base
+ * rank, id_stride G; the caller keeps ownership) through the NCCL id rank 0
+ * made with hcg_nccl_unique_id and shared with every rank.  Collective: all
+ * G ranks call it together. */
+hcg_status hcg_nccl_unique_id(hcg_nccl_id* out);
+hcg_status hcg_shard_group_join(const hcg_nccl_id* id, uint32_t rank, uint32_t G, hcg_index* local,
+                                hcg_shard_group** out);
+hcg_status hcg_shard_group_free(hcg_shard_group* group);
+uint32_t hcg_shard_group_shards(const hcg_shard_group* group);
+/* Global top-k of nq queries (hcg_search's layout and padding).  queries and
+ * outputs: host memory or device memory (of devices[0] / the rank's device;
+ * queries may also sit on another GPU).  `stream` belongs to devices[0] (the
+ * rank's device); the call is stream-ordered against it and synchronises only
+ * when an output is host memory.  Per-process mode: collective, every rank
+ * passes the same batch and receives the same result. */
+hcg_status hcg_shard_group_search(hcg_shard_group* group, const uint8_t* queries, uint32_t nq, uint32_t k,
+                                  uint32_t shard_depth, uint64_t* out_ids, uint32_t* out_sqdist, uint32_t* out_len,
+                                  void* stream);
+
+/* CUDA device of an index, and its id map (id of slot s = base + s * stride). */
+int hcg_index_device(const hcg_index* index);
+hcg_status hcg_index_ids(const hcg_index* index, uint64_t* id_base, uint64_t* id_stride);
+
 /* ---- probe-depth planner (equivalence module, host math) ---- */
 /* P[Bin(trials, p) > phi]. */
 double hcg_binomial_tail(uint32_t trials, double p, uint32_t phi);

@@ -18,7 +18,7 @@ ROOT = os.path.dirname(HERE)
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
                      "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]
-CU = ["build.cu", "search.cu", "brute_tc.cu", "datagen.cu", "api.cu"]
+CU = ["build.cu", "search.cu", "brute_tc.cu", "datagen.cu", "api.cu", "shard.cu"]
 CPP = ["planner.cpp", "io.cpp"]
 HEADERS = ["hcg_internal.cuh", "hcg_host.hpp"]
 
@@ -73,7 +73,7 @@ def build(verbose: bool = False, ptxas_info: bool = False) -> str:
     flavor = "debug" if debug else "release"
     if _stale(LIB, objs) or not os.path.exists(stamp) or open(stamp).read() != flavor:
         tmp = LIB + ".tmp"
-        run([_nvcc(), "-shared"] + ARCH + ["-cudart", "static", "-o", tmp] + objs)
+        run([_nvcc(), "-shared"] + ARCH + ["-cudart", "static", "-o", tmp] + objs + ["-ldl"])
         os.replace(tmp, LIB)
         with open(stamp, "w") as f:
             f.write(flavor)

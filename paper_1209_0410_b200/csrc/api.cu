@@ -37,6 +37,7 @@ struct hcg_index {
     std::vector<uint64_t> sample_bytes;
     uint32_t** d_slot_ptrs = nullptr;
     uint64_t bytes = 0;
+    bool broken = false;  // a failed table upload after an insert: every call is refused
 };
 
 namespace hcg {
@@ -193,6 +194,7 @@ int pow2_bucket(uint32_t v, int lo, int hi) {
 
 hcg_status check_index(const hcg_index* ix) {
     if (!ix) return set_error(HCG_EINVAL, "null index");
+    if (ix->broken) return set_error(HCG_ECUDA, "index unusable after a failed device table upload");
     return HCG_OK;
 }
 
@@ -250,6 +252,20 @@ hcg_status validate_scheme(const hcg_scheme* s) {
     for (bool cv : covered)
         if (!cv) return set_error(HCG_EINVAL, "input dimension not covered by any curve");
     if (s->dtype == HCG_F32) return HCG_OK;  // cells computed on the device; the table is unused
+    // A u8 index scores the integer S = sum (b1 - b2)^2 and reports
+    // sqrt(S) * scale.  That equals the reference's sqrt of its double sum
+    // (vecio.cpp:87-95) over the floats offset + b * scale exactly when those
+    // floats are exact and scale is a power of two (then every term, partial
+    // sum and the root scale without rounding).  Other views are rejected.
+    int e2 = 0;
+    if (std::frexp(s->dist_scale, &e2) != 0.5)
+        return set_error(HCG_EINVAL, "u8 view: dist_scale must be a power of two (exact rooted distances)");
+    const float voff = std::isfinite(s->view_offset) ? s->view_offset : 0.0f;
+    for (int b = 0; b < 256; ++b) {
+        const double v = double(voff) + double(b) * s->dist_scale;
+        if (double(float(v)) != v)
+            return set_error(HCG_EINVAL, "u8 view: offset + b * scale is not exact in float32 for b = " + std::to_string(b));
+    }
     const uint64_t lim = s->bits_per_dim == 32 ? (1ull << 32) : (1ull << s->bits_per_dim);
     for (int b = 0; b < 256; ++b)
         if (s->cell_lut[b] >= lim) return set_error(HCG_EINVAL, "cell_lut entry exceeds 2^m");
@@ -295,11 +311,11 @@ hcg_status keygen_reduce(const hcg_index* ix, uint32_t c, const uint8_t* rows, u
 // K2: stable LSD radix sort of `count` keys (SoA, W words) by their bits
 // [0, hv] (only the 8-bit digits that vary over `oa`), then pack the sorted
 // suffixes (AoS, ws words) into *keys_out and slot_base + position into
-// *slots_out (both allocated here, owned by the index).
+// *slots_out (both allocated here; their bytes are added to *bytes).
 // init_order (optional): the sort's input sequence as positions into soa --
 // the id order of a physically permuted index, so that equal keys stay in id
 // order and the output holds physical positions.
-hcg_status sort_suffix(hcg_index* ix, const uint64_t* soa, uint64_t count, uint32_t W, const std::vector<uint64_t>& oa,
+hcg_status sort_suffix(uint64_t* bytes, const uint64_t* soa, uint64_t count, uint32_t W, const std::vector<uint64_t>& oa,
                        uint32_t hv, uint64_t slot_base, Scratch& sc, uint64_t** keys_out, uint32_t** slots_out,
                        const uint32_t* init_order = nullptr) {
     const int hw = int(hv >> 6), hb = int(hv & 63);
@@ -333,31 +349,55 @@ hcg_status sort_suffix(hcg_index* ix, const uint64_t* soa, uint64_t count, uint3
         kb = k;
         ka = k_alt;
     }
-    HCG_TRY(dev_alloc(keys_out, size_t(count) * ws, &ix->bytes));
-    HCG_TRY(dev_alloc(slots_out, count, &ix->bytes));
+    HCG_TRY(dev_alloc(keys_out, size_t(count) * ws, bytes));
+    HCG_TRY(dev_alloc(slots_out, count, bytes));
     launch_pack_suffix(soa, v, count, int(ws), below, *keys_out, st);
     launch_offset(v, *slots_out, count, uint32_t(slot_base), st);
     return check_launch("pack suffix");
 }
 
-// Build curve c over all rows: K1 keys, common-prefix detection, K2 sort.
-hcg_status build_curve(hcg_index* ix, uint32_t c, cudaStream_t st, const uint32_t* init_order = nullptr) {
-    const uint64_t n = ix->n;
+void dev_free(void* p, size_t bytes, uint64_t* total) {
+    if (p) {
+        cudaFree(p);
+        *total -= std::min<uint64_t>(*total, bytes);
+    }
+}
+
+// A curve's sorted arrays under construction: nothing of the index changes
+// until every curve of a build / insert succeeded (then commit_curve swaps
+// them in); on failure drop() frees them.
+struct CurveOut {
+    uint64_t* keys = nullptr;
+    uint32_t* slots = nullptr;
+    CurveDev cv{};
+    uint64_t n = 0;
+    uint64_t bytes = 0;
+    void drop() {
+        dev_free(keys, size_t(n) * cv.ws * 8, &bytes);
+        dev_free(slots, size_t(n) * 4, &bytes);
+        keys = nullptr;
+        slots = nullptr;
+    }
+};
+
+// Curve c over `n` rows (`rows`, the index's pitch): K1 keys, common-prefix
+// detection, K2 sort.
+hcg_status build_curve_into(const hcg_index* ix, uint32_t c, const uint8_t* rows, uint64_t n, cudaStream_t st,
+                            const uint32_t* init_order, CurveOut* out) {
     const uint32_t d = ix->off[c + 1] - ix->off[c];
     const uint32_t W = (d * ix->m + 63) / 64;
-    CurveDev& cv = ix->curves[c];
+    CurveDev& cv = out->cv;
     std::memset(&cv, 0, sizeof(cv));
     cv.w = W;
     cv.dims = d;
     cv.off = ix->off[c];
-    if (n == 0) {
-        cv.ws = 1;
-        return HCG_OK;
-    }
+    cv.ws = 1;
+    out->n = n;
+    if (n == 0) return HCG_OK;
     Scratch sc(st);
     uint64_t* soa = nullptr;
     std::vector<uint64_t> oa;
-    HCG_TRY(keygen_reduce(ix, c, ix->rows, n, sc, &soa, oa));
+    HCG_TRY(keygen_reduce(ix, c, rows, n, sc, &soa, oa));
     int hv = 0;
     for (int w = int(W) - 1; w >= 0; --w) {
         const uint64_t vary = oa[w] ^ oa[W + w];
@@ -372,32 +412,54 @@ hcg_status build_curve(hcg_index* ix, uint32_t c, cudaStream_t st, const uint32_
     cv.ws = uint32_t(hw + 1);
     for (uint32_t w = 0; w < W; ++w)
         cv.prefix[w] = int(w) > hw ? oa[w] : (int(w) == hw ? (oa[w] & above) : 0ull);
-    HCG_TRY(sort_suffix(ix, soa, n, W, oa, cv.hv, 0, sc, &ix->keys[c], &ix->slots[c], init_order));
-    cv.keys = ix->keys[c];
-    cv.slots = ix->slots[c];
+    HCG_TRY(sort_suffix(&out->bytes, soa, n, W, oa, cv.hv, 0, sc, &out->keys, &out->slots, init_order));
+    cv.keys = out->keys;
+    cv.slots = out->slots;
     HCG_TRY_CUDA(cudaStreamSynchronize(st));
     return HCG_OK;
 }
 
-void dev_free(void* p, size_t bytes, uint64_t* total) {
-    if (p) {
-        cudaFree(p);
-        *total -= std::min<uint64_t>(*total, bytes);
-    }
+// Swap a finished curve into the index (frees the curve's previous arrays).
+void commit_curve(hcg_index* ix, uint32_t c, uint64_t n_prev, CurveOut& o) {
+    dev_free(ix->keys[c], size_t(n_prev) * ix->curves[c].ws * 8, &ix->bytes);
+    dev_free(ix->slots[c], size_t(n_prev) * 4, &ix->bytes);
+    ix->keys[c] = o.keys;
+    ix->slots[c] = o.slots;
+    ix->curves[c] = o.cv;
+    ix->bytes += o.bytes;
+    o.keys = nullptr;
+    o.slots = nullptr;
+    o.bytes = 0;
 }
 
-// Insert `nb` rows (already appended to ix->rows at slots n_old..) into curve
-// c.  When the new keys share the curve's common prefix, they are sorted on
-// their own and rank-merged into the resident arrays (stable: resident
-// entries first on equal keys, i.e. id order); otherwise the curve is rebuilt.
-hcg_status insert_curve(hcg_index* ix, uint32_t c, uint64_t n_old, uint64_t nb, cudaStream_t st) {
-    CurveDev& cv = ix->curves[c];
-    if (n_old == 0) return build_curve(ix, c, st);
+hcg_status build_curve(hcg_index* ix, uint32_t c, cudaStream_t st) {
+    CurveOut o;
+    const hcg_status rc = build_curve_into(ix, c, ix->rows, ix->n, st, nullptr, &o);
+    if (rc != HCG_OK) {
+        cudaStreamSynchronize(st);
+        o.drop();
+        return rc;
+    }
+    commit_curve(ix, c, 0, o);
+    return HCG_OK;
+}
+
+// Curve c after appending `nb` rows to the index's n_old: `rows` is the new
+// n_old + nb row buffer, `idtab` the new id table (null: identity).  When the
+// new keys share the curve's common prefix they are sorted on their own and
+// rank-merged into the resident arrays (stable: resident entries first on
+// equal keys, i.e. id order); otherwise the curve is rebuilt over all rows.
+// The index itself is not modified.
+hcg_status insert_curve_into(const hcg_index* ix, uint32_t c, const uint8_t* rows, uint64_t n_old, uint64_t nb,
+                             const uint32_t* idtab, cudaStream_t st, CurveOut* out) {
+    const uint64_t n_new = n_old + nb;
+    if (n_old == 0) return build_curve_into(ix, c, rows, n_new, st, nullptr, out);
+    const CurveDev& cv = ix->curves[c];
     const uint32_t W = cv.w;
     Scratch sc(st);
     uint64_t* soa = nullptr;
     std::vector<uint64_t> oa;
-    HCG_TRY(keygen_reduce(ix, c, ix->rows + uint64_t(n_old) * ix->pitch, nb, sc, &soa, oa));
+    HCG_TRY(keygen_reduce(ix, c, rows + uint64_t(n_old) * ix->pitch, nb, sc, &soa, oa));
     const int hw = int(cv.hv >> 6), hb = int(cv.hv & 63);
     const uint64_t above = hb == 63 ? 0ull : (~0ull << (hb + 1));
     bool compatible = true;
@@ -406,38 +468,33 @@ hcg_status insert_curve(hcg_index* ix, uint32_t c, uint64_t n_old, uint64_t nb, 
         if ((oa[w] & m) != cv.prefix[w] || (oa[W + w] & m) != cv.prefix[w]) compatible = false;
     }
     if (!compatible) {
-        dev_free(ix->keys[c], size_t(n_old) * cv.ws * 8, &ix->bytes);
-        dev_free(ix->slots[c], size_t(n_old) * 4, &ix->bytes);
-        ix->keys[c] = nullptr;
-        ix->slots[c] = nullptr;
-        if (!ix->idtab) return build_curve(ix, c, st);
+        if (!idtab) return build_curve_into(ix, c, rows, n_new, st, nullptr, out);
         // permuted rows: sort in id order (inverse of idtab) so ties keep id order
-        Scratch sc2(st);
-        uint32_t* inv = sc2.alloc<uint32_t>(ix->n);
+        uint32_t* inv = sc.alloc<uint32_t>(n_new);
         if (!inv) return set_error(HCG_ENOMEM, "inverse permutation");
-        launch_invert(ix->idtab, ix->n, inv, st);
+        launch_invert(idtab, n_new, inv, st);
         HCG_TRY(check_launch("invert"));
-        return build_curve(ix, c, st, inv);
+        return build_curve_into(ix, c, rows, n_new, st, inv, out);
     }
+    uint64_t tmp_bytes = 0;
     uint64_t* nk = nullptr;
     uint32_t* ns = nullptr;
-    HCG_TRY(sort_suffix(ix, soa, nb, W, oa, cv.hv, n_old, sc, &nk, &ns));
-    uint64_t* mk = nullptr;
-    uint32_t* ms = nullptr;
-    HCG_TRY(dev_alloc(&mk, size_t(n_old + nb) * cv.ws, &ix->bytes));
-    HCG_TRY(dev_alloc(&ms, n_old + nb, &ix->bytes));
-    launch_rank_merge(ix->keys[c], ix->slots[c], n_old, nk, ns, nb, int(cv.ws), mk, ms, st);
-    HCG_TRY(check_launch("rank merge"));
-    HCG_TRY_CUDA(cudaStreamSynchronize(st));
-    dev_free(ix->keys[c], size_t(n_old) * cv.ws * 8, &ix->bytes);
-    dev_free(ix->slots[c], size_t(n_old) * 4, &ix->bytes);
-    dev_free(nk, size_t(nb) * cv.ws * 8, &ix->bytes);
-    dev_free(ns, size_t(nb) * 4, &ix->bytes);
-    ix->keys[c] = mk;
-    ix->slots[c] = ms;
-    cv.keys = mk;
-    cv.slots = ms;
-    return HCG_OK;
+    hcg_status rc = sort_suffix(&tmp_bytes, soa, nb, W, oa, cv.hv, n_old, sc, &nk, &ns);
+    out->cv = cv;
+    out->n = n_new;
+    if (rc == HCG_OK) rc = dev_alloc(&out->keys, size_t(n_new) * cv.ws, &out->bytes);
+    if (rc == HCG_OK) rc = dev_alloc(&out->slots, n_new, &out->bytes);
+    if (rc == HCG_OK) {
+        launch_rank_merge(ix->keys[c], ix->slots[c], n_old, nk, ns, nb, int(cv.ws), out->keys, out->slots, st);
+        rc = check_launch("rank merge");
+    }
+    if (rc == HCG_OK && cudaStreamSynchronize(st) != cudaSuccess) rc = set_error(HCG_ECUDA, "rank merge");
+    cudaStreamSynchronize(st);
+    dev_free(nk, size_t(nb) * cv.ws * 8, &tmp_bytes);
+    dev_free(ns, size_t(nb) * 4, &tmp_bytes);
+    out->cv.keys = out->keys;
+    out->cv.slots = out->slots;
+    return rc;
 }
 
 // Upload the curve table and slot pointers (after build / insert / load).
@@ -658,6 +715,16 @@ hcg_status run_refine(const hcg_index* ix, Scratch& sc, const RefineArgs& a_in) 
     return rc;
 }
 
+// v holds each of 0 .. v.size()-1 exactly once.
+bool is_permutation_of_n(const std::vector<uint32_t>& v) {
+    std::vector<uint8_t> seen(v.size(), 0);
+    for (uint32_t x : v) {
+        if (x >= v.size() || seen[x]) return false;
+        seen[x] = 1;
+    }
+    return true;
+}
+
 // Copy a host-side vector to a user buffer that may be host or device memory.
 template <class T>
 hcg_status deliver(T* user, const std::vector<T>& v) {
@@ -767,6 +834,13 @@ uint32_t hcg_key_words(const hcg_index* ix, uint32_t c) { return ix && c < ix->C
 uint64_t hcg_device_bytes(const hcg_index* ix) { return ix ? ix->bytes : 0; }
 uint64_t hcg_launch_count(void) { return hcg::g_launches.load(); }
 uint32_t hcg_index_dtype(const hcg_index* ix) { return ix ? ix->dtype : 0; }
+int hcg_index_device(const hcg_index* ix) { return ix ? ix->device : -1; }
+hcg_status hcg_index_ids(const hcg_index* ix, uint64_t* id_base, uint64_t* id_stride) {
+    HCG_TRY(check_index(ix));
+    if (id_base) *id_base = ix->id_base;
+    if (id_stride) *id_stride = ix->id_stride;
+    return HCG_OK;
+}
 
 hcg_status hcg_insert(hcg_index* ix, const uint8_t* rows, uint64_t nb, void* stream) {
     HCG_TRY(check_index(ix));
@@ -776,47 +850,64 @@ hcg_status hcg_insert(hcg_index* ix, const uint8_t* rows, uint64_t nb, void* str
     if (n_new >= (1ull << 32)) return set_error(HCG_ECAPACITY, "more than 2^32-1 rows in one index");
     DeviceGuard g(ix->device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    // Stage everything (rows, id table, every curve) first; the index is
+    // only touched once all of it succeeded, so a failure leaves it as it was.
+    uint64_t staged = 0;
     uint8_t* nr = nullptr;
-    HCG_TRY(dev_alloc(&nr, size_t(n_new) * ix->pitch, &ix->bytes));
-    if (n_old) HCG_TRY_CUDA(cudaMemcpyAsync(nr, ix->rows, size_t(n_old) * ix->pitch, cudaMemcpyDeviceToDevice, st));
-    if (ix->pitch != ix->row_bytes)
-        HCG_TRY_CUDA(cudaMemsetAsync(nr + size_t(n_old) * ix->pitch, 0, size_t(nb) * ix->pitch, st));
-    HCG_TRY_CUDA(cudaMemcpy2DAsync(nr + size_t(n_old) * ix->pitch, ix->pitch, rows, ix->row_bytes, ix->row_bytes, nb,
-                                   cudaMemcpyDefault, st));
-    HCG_TRY_CUDA(cudaStreamSynchronize(st));
+    uint32_t* nt = nullptr;
+    std::vector<CurveOut> outs(ix->C);
+    auto fail = [&](hcg_status rc) {
+        cudaStreamSynchronize(st);
+        for (auto& o : outs) o.drop();
+        dev_free(nr, size_t(n_new) * ix->pitch, &staged);
+        dev_free(nt, size_t(n_new) * 4, &staged);
+        return rc;
+    };
+    if (dev_alloc(&nr, size_t(n_new) * ix->pitch, &staged) != HCG_OK) return fail(HCG_ENOMEM);
+    if ((n_old && cudaMemcpyAsync(nr, ix->rows, size_t(n_old) * ix->pitch, cudaMemcpyDeviceToDevice, st) != cudaSuccess) ||
+        (ix->pitch != ix->row_bytes &&
+         cudaMemsetAsync(nr + size_t(n_old) * ix->pitch, 0, size_t(nb) * ix->pitch, st) != cudaSuccess) ||
+        cudaMemcpy2DAsync(nr + size_t(n_old) * ix->pitch, ix->pitch, rows, ix->row_bytes, ix->row_bytes, nb,
+                          cudaMemcpyDefault, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+        return fail(set_error(HCG_ECUDA, std::string("copy rows: ") + cudaGetErrorString(cudaGetLastError())));
     if (ix->dtype == HCG_F32) {  // reject NaN / Inf before the index changes (curve.cpp:167)
         Scratch sc(st);
         unsigned* bad = sc.alloc<unsigned>(1);
         unsigned h = 0;
-        hcg_status rc = bad ? HCG_OK : set_error(HCG_ENOMEM, "flag");
-        if (rc == HCG_OK && (cudaMemsetAsync(bad, 0, 4, st) != cudaSuccess)) rc = set_error(HCG_ECUDA, "memset");
-        if (rc == HCG_OK) launch_check_finite(nr + size_t(n_old) * ix->pitch, nb, ix->pitch, ix->d_full, bad, st);
-        if (rc == HCG_OK && (cudaMemcpyAsync(&h, bad, 4, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
-                             cudaStreamSynchronize(st) != cudaSuccess))
-            rc = set_error(HCG_ECUDA, "finite check");
-        if (rc == HCG_OK && h) rc = set_error(HCG_ENONFINITE, "non-finite component");
-        if (rc != HCG_OK) {
-            dev_free(nr, size_t(n_new) * ix->pitch, &ix->bytes);
-            return rc;
-        }
+        if (!bad) return fail(set_error(HCG_ENOMEM, "flag"));
+        if (cudaMemsetAsync(bad, 0, 4, st) != cudaSuccess) return fail(set_error(HCG_ECUDA, "memset"));
+        launch_check_finite(nr + size_t(n_old) * ix->pitch, nb, ix->pitch, ix->d_full, bad, st);
+        if (cudaMemcpyAsync(&h, bad, 4, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+            cudaStreamSynchronize(st) != cudaSuccess)
+            return fail(set_error(HCG_ECUDA, "finite check"));
+        if (h) return fail(set_error(HCG_ENONFINITE, "non-finite component"));
     }
     if (ix->idtab) {  // appended rows sit at physical = id slot
-        uint32_t* nt = nullptr;
-        if (dev_alloc(&nt, n_new, &ix->bytes) != HCG_OK) {
-            dev_free(nr, size_t(n_new) * ix->pitch, &ix->bytes);
-            return set_error(HCG_ENOMEM, "id table");
-        }
-        HCG_TRY_CUDA(cudaMemcpyAsync(nt, ix->idtab, n_old * 4, cudaMemcpyDeviceToDevice, st));
+        if (dev_alloc(&nt, n_new, &staged) != HCG_OK) return fail(set_error(HCG_ENOMEM, "id table"));
+        if (cudaMemcpyAsync(nt, ix->idtab, n_old * 4, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+            return fail(set_error(HCG_ECUDA, "copy id table"));
         launch_iota(nt + n_old, nb, uint32_t(n_old), st);
-        HCG_TRY_CUDA(cudaStreamSynchronize(st));
+        if (check_launch("iota") != HCG_OK || cudaStreamSynchronize(st) != cudaSuccess)
+            return fail(set_error(HCG_ECUDA, "id table"));
+    }
+    for (uint32_t c = 0; c < ix->C; ++c) {
+        const hcg_status rc = insert_curve_into(ix, c, nr, n_old, nb, nt, st, &outs[c]);
+        if (rc != HCG_OK) return fail(rc);
+    }
+    // commit
+    for (uint32_t c = 0; c < ix->C; ++c) commit_curve(ix, c, n_old, outs[c]);
+    dev_free(ix->rows, size_t(std::max<uint64_t>(n_old, 1)) * ix->pitch, &ix->bytes);
+    ix->rows = nr;
+    if (nt) {
         dev_free(ix->idtab, size_t(n_old) * 4, &ix->bytes);
         ix->idtab = nt;
     }
-    dev_free(ix->rows, size_t(std::max<uint64_t>(n_old, 1)) * ix->pitch, &ix->bytes);
-    ix->rows = nr;
+    ix->bytes += staged;
     ix->n = n_new;
-    for (uint32_t c = 0; c < ix->C; ++c) HCG_TRY(insert_curve(ix, c, n_old, nb, st));
-    return publish_tables(ix, st);
+    const hcg_status rc = publish_tables(ix, st);
+    if (rc != HCG_OK) ix->broken = true;  // device tables may be stale: refuse further use
+    return rc;
 }
 
 
@@ -927,6 +1018,7 @@ hcg_status hcg_load(const char* path, int device, void* stream, hcg_index** out)
     if (has_idtab && ix->n) {
         std::vector<uint32_t> idt(ix->n);
         if (!get(f, idt.data(), idt.size())) return fail(set_error(HCG_EIO, std::string(path) + ": truncated id table"));
+        if (!is_permutation_of_n(idt)) return fail(set_error(HCG_EIO, std::string(path) + ": id table is not a permutation"));
         if (dev_alloc(&ix->idtab, ix->n, &ix->bytes) != HCG_OK ||
             cudaMemcpy(ix->idtab, idt.data(), ix->n * 4, cudaMemcpyHostToDevice) != cudaSuccess)
             return fail(set_error(HCG_ECUDA, "upload id table"));
@@ -949,6 +1041,9 @@ hcg_status hcg_load(const char* path, int device, void* stream, hcg_index** out)
             std::vector<uint32_t> sl(ix->n);
             if (!get(f, k.data(), k.size()) || !get(f, sl.data(), sl.size()))
                 return fail(set_error(HCG_EIO, std::string(path) + ": truncated curve arrays"));
+            // every slot is a row of this index, each row once: a corrupt file
+            // must not turn into out-of-bounds row gathers
+            if (!is_permutation_of_n(sl)) return fail(set_error(HCG_EIO, std::string(path) + ": corrupt slot array"));
             hcg_status rc;
             if ((rc = dev_alloc(&ix->keys[c], k.size(), &ix->bytes)) != HCG_OK) return fail(rc);
             if ((rc = dev_alloc(&ix->slots[c], sl.size(), &ix->bytes)) != HCG_OK) return fail(rc);

@@ -214,17 +214,6 @@ __device__ __forceinline__ uint32_t sad2_16(const uint4& a, const uint4& b, uint
     return acc;
 }
 
-// Squared L2 of 4 floats accumulated in double: the reference's terms
-// (double(a) - double(b))^2 (vecio.cpp:87-95), tree-summed.
-__device__ __forceinline__ double sq4_f64(const uint4& a, const uint4& b, double acc) {
-    double d;
-    d = double(__uint_as_float(a.x)) - double(__uint_as_float(b.x)); acc = fma(d, d, acc);
-    d = double(__uint_as_float(a.y)) - double(__uint_as_float(b.y)); acc = fma(d, d, acc);
-    d = double(__uint_as_float(a.z)) - double(__uint_as_float(b.z)); acc = fma(d, d, acc);
-    d = double(__uint_as_float(a.w)) - double(__uint_as_float(b.w)); acc = fma(d, d, acc);
-    return acc;
-}
-
 __device__ __forceinline__ uint4 ldg_stream(const void* p) {
     uint4 r;
     asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"

@@ -482,12 +482,15 @@ __device__ __forceinline__ void gather_list(const RefineArgs& a, const uint32_t*
 // the same (distance, id) key twice and offer_unique keeps one.  Costs the
 // duplicate rows (~16 % of the windows, partly L2 hits) instead of the union
 // kernel and the lists' round trip.
-template <int R, int CR>
+// SMALLC (C <= 32): lane c holds curve c's window start pointer (slots[c] +
+// begin), fetched once per query and broadcast with a shuffle, so an entry
+// costs one dependent load (the slot) instead of three (pointer, begin, slot).
+template <int R, int CR, bool SMALLC>
 __device__ __forceinline__ void gather_windows(const RefineArgs& a, const uint32_t* begins_q, const uint4 (&qv)[CR],
                                                int lane, WarpTopK<R>& tk) {
     const int l8 = lane & 7, grp = lane >> 3;
     const uint32_t chunks = a.pitch >> 4;
-    const uint32_t take = a.take, n = a.C * take;
+    const uint32_t take = a.take, n = a.C * take, C = a.C;
     // (curve, position) of this lane-group's 8 entries, advanced by 32 per pass
     uint32_t cc[8], pp[8];
 #pragma unroll
@@ -496,8 +499,16 @@ __device__ __forceinline__ void gather_windows(const RefineArgs& a, const uint32
         cc[r] = e / take;
         pp[r] = e - cc[r] * take;
     }
+    unsigned long long wstart = 0;
+    if (SMALLC && uint32_t(lane) < C)
+        wstart = reinterpret_cast<unsigned long long>(a.slots[lane] + __ldg(begins_q + lane));
     auto entry = [&](int r) -> uint32_t {
-        return cc[r] < a.C ? __ldg(a.slots[cc[r]] + __ldg(begins_q + cc[r]) + pp[r]) : kEmpty;
+        if constexpr (SMALLC) {
+            const uint32_t* w = reinterpret_cast<const uint32_t*>(__shfl_sync(kFull, wstart, int(cc[r] & 31)));
+            return cc[r] < C ? __ldg(w + pp[r]) : kEmpty;
+        } else {
+            return cc[r] < C ? __ldg(a.slots[cc[r]] + __ldg(begins_q + cc[r]) + pp[r]) : kEmpty;
+        }
     };
     uint32_t nx[8];
 #pragma unroll
@@ -590,7 +601,7 @@ __global__ void __launch_bounds__(kRefineThreads, MINB) k_gather(RefineArgs a, c
 }
 
 // K3c without the union: one warp per query over the raw windows.
-template <int R, int CR, int MINB, int NT = kRefineThreads>
+template <int R, int CR, int MINB, bool SMALLC, int NT = kRefineThreads>
 __global__ void __launch_bounds__(NT, MINB) k_gather_nu(RefineArgs a) {
     const int lane = threadIdx.x & 31;
     const uint32_t qstep = gridDim.x * (NT / 32);
@@ -600,7 +611,7 @@ __global__ void __launch_bounds__(NT, MINB) k_gather_nu(RefineArgs a) {
         load_query<CR>(a, qq, lane, qv);
         WarpTopK<R> tk;
         tk.init(int(a.k));
-        gather_windows<R, CR>(a, a.begins + uint64_t(qq) * a.C, qv, lane, tk);
+        gather_windows<R, CR, SMALLC>(a, a.begins + uint64_t(qq) * a.C, qv, lane, tk);
         uint32_t valid = 0;
 #pragma unroll
         for (int r = 0; r < R; ++r)
@@ -643,80 +654,91 @@ __global__ void __launch_bounds__(NW * 32) k_gather_cta(RefineArgs a, const uint
 }
 
 // ------------------------------------------------------- K3c, f32 rows ----
-// Float descriptors (the reference's native component type): a row is up to
-// 512 B = 32 16-B chunks, so the whole WARP reads one row per load (lane =
-// chunk, 4 full 128-B lines) and keeps 8 rows in flight.  Per-lane partials
-// are double ((double(a) - double(b))^2, vecio.cpp:87-95); a reduce-scatter
-// over lane bits 4,3,2 and an all-reduce over bits 1,0 leave row
-// 4*b4 + 2*b3 + b2 in lane group (lane >> 2), whose lane 0 offers
-// (double bits, slot) to the pair top-k.  The summation is a fixed tree:
-// distances agree with the reference's sequential sum to ~1e-15 relative and
-// identical rows get identical distances.
+// Float descriptors (the reference's native component type), scored exactly
+// as squared_distance (vecio.cpp:87-95) does: acc = 0; for i in index order
+// acc += (double(a_i) - double(b_i))^2, each subtract, multiply and add
+// rounded on its own (no FMA contraction) -- the same double, bit for bit,
+// so ids and (distance, id) tie order match the reference by construction.
+// A sequential sum needs one lane per row: a warp stages 32 rows (lane =
+// 16-B chunk, coalesced cp.async) into its shared-memory tile, chunk c of row
+// r at chunk position c ^ (r & 7) so that the 8 lanes of an LDS.128 phase hit
+// distinct banks, then lane r sums row r in index order and offers
+// (double bits, slot) to the pair top-k.  Padding components are zero on both
+// sides and add exact zeros.
+constexpr uint32_t kF32Rows = 32;  // rows per warp pass (one per lane)
+
+__device__ __forceinline__ uint32_t f32_tile_stride(uint32_t pitch) { return (pitch + 127u) & ~127u; }
+// Shared bytes per warp: the 32-row tile + the query row.
+__host__ __device__ __forceinline__ uint32_t f32_warp_smem(uint32_t pitch) {
+    return kF32Rows * ((pitch + 127u) & ~127u) + pitch;
+}
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* src) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+}
+
+__device__ __forceinline__ double sq_term(float a, float b) {
+    const double d = __dsub_rn(double(a), double(b));
+    return __dmul_rn(d, d);
+}
+
 template <bool DIRECT>
 __device__ __forceinline__ uint32_t f32_entry(const uint32_t* list, uint32_t e, uint32_t n) {
     if (DIRECT) return e < n ? e : kEmpty;
     return e < n ? __ldcg(list + e) : kEmpty;
 }
 
-// Scores entries [start, start + 8), [start + step, ...) of a list (DIRECT:
+// Query row q -> the warp's query buffer (qs, pitch bytes).
+__device__ __forceinline__ void stage_query_f32(const uint8_t* queries, uint32_t pitch, uint32_t q, uint8_t* qs,
+                                                int lane) {
+    __syncwarp();  // the previous query's reads are done
+    for (uint32_t c = lane; c < (pitch >> 4); c += 32)
+        *reinterpret_cast<uint4*>(qs + c * 16) = *reinterpret_cast<const uint4*>(queries + uint64_t(q) * pitch + c * 16);
+    __syncwarp();
+}
+
+// Scores entries [start, start + 32), [start + step, ...) of a list (DIRECT:
 // the entries are the row slots themselves, i.e. rows [start, n)).
 template <int R, bool DIRECT>
 __device__ __forceinline__ void gather_list_f32(const uint8_t* rows, uint32_t pitch, const uint32_t* list, uint32_t n,
-                                                uint32_t start, uint32_t step, const uint4& qv, int lane,
-                                                WarpTopK2<R>& tk, const uint32_t* idtab) {
-    const uint32_t chunks = pitch >> 4;
-    const bool has = uint32_t(lane) < chunks;
-    uint32_t cur = lane < 8 ? f32_entry<DIRECT>(list, start + lane, n) : kEmpty;
+                                                uint32_t start, uint32_t step, const uint8_t* qs, uint8_t* tile,
+                                                int lane, WarpTopK2<R>& tk, const uint32_t* idtab) {
+    const uint32_t chunks = pitch >> 4, rstride = f32_tile_stride(pitch);
+    const uint8_t* mine_row = tile + uint32_t(lane) * rstride;
+    const uint32_t swz = uint32_t(lane) & 7;
     for (uint32_t base = start; base < n; base += step) {
-        uint32_t nx[8];
-#pragma unroll
-        for (int r = 0; r < 8; ++r) nx[r] = __shfl_sync(kFull, cur, r);
-        uint4 v[8];
-#pragma unroll
-        for (int r = 0; r < 8; ++r)
-            v[r] = (nx[r] != kEmpty && has) ? ldg_stream(rows + uint64_t(nx[r]) * pitch + uint32_t(lane) * 16)
-                                            : make_uint4(0, 0, 0, 0);
-        cur = lane < 8 ? f32_entry<DIRECT>(list, base + step + lane, n) : kEmpty;
-        double acc[8];
-#pragma unroll
-        for (int r = 0; r < 8; ++r) acc[r] = sq4_f64(v[r], qv, 0.0);
-        const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
-        double s4[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const double send = b4 ? acc[i] : acc[i + 4];
-            const double keep = b4 ? acc[i + 4] : acc[i];
-            s4[i] = keep + __shfl_xor_sync(kFull, send, 16);
+        const uint32_t me = f32_entry<DIRECT>(list, base + lane, n);
+#pragma unroll 4
+        for (int r = 0; r < int(kF32Rows); ++r) {
+            const uint32_t row = __shfl_sync(kFull, me, r);
+            if (row != kEmpty)
+                for (uint32_t c = lane; c < chunks; c += 32)
+                    cp_async16(tile + r * rstride + ((c ^ (r & 7)) << 4), rows + uint64_t(row) * pitch + c * 16);
         }
-        double s2[2];
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-            const double send = b3 ? s4[i] : s4[i + 2];
-            const double keep = b3 ? s4[i + 2] : s4[i];
-            s2[i] = keep + __shfl_xor_sync(kFull, send, 8);
+        cp_async_commit();
+        cp_async_wait_all();
+        __syncwarp();
+        double acc = 0.0;
+        if (me != kEmpty) {
+            for (uint32_t c = 0; c < chunks; ++c) {
+                const float4 v = *reinterpret_cast<const float4*>(mine_row + ((c ^ swz) << 4));
+                const float4 q = *reinterpret_cast<const float4*>(qs + (c << 4));
+                acc = __dadd_rn(acc, sq_term(v.x, q.x));
+                acc = __dadd_rn(acc, sq_term(v.y, q.y));
+                acc = __dadd_rn(acc, sq_term(v.z, q.z));
+                acc = __dadd_rn(acc, sq_term(v.w, q.w));
+            }
         }
-        double S = (b2 ? s2[1] : s2[0]) + __shfl_xor_sync(kFull, b2 ? s2[0] : s2[1], 4);
-        S += __shfl_xor_sync(kFull, S, 2);
-        S += __shfl_xor_sync(kFull, S, 1);
-        const int row = (b4 ? 4 : 0) + (b3 ? 2 : 0) + (b2 ? 1 : 0);
-        uint32_t me = nx[0];
-#pragma unroll
-        for (int r = 1; r < 8; ++r)
-            if (r == row) me = nx[r];
-        const bool offer = (lane & 3) == 0 && me != kEmpty;
-        const uint64_t sb = uint64_t(__double_as_longlong(S));
+        __syncwarp();  // tile reads done before the next pass overwrites it
+        const uint64_t sb = uint64_t(__double_as_longlong(acc));
         uint32_t sl = me;
         if (idtab) {  // physical row -> id slot for rows that can enter the top-k
-            const bool pre = offer && sb <= tk.ta;
+            const bool pre = me != kEmpty && sb <= tk.ta;
             if (__any_sync(kFull, pre) && pre) sl = __ldg(idtab + me);
         }
-        tk.offer(offer ? sb : kNone, offer ? sl : 0xFFFFFFFFu, lane);
+        tk.offer(me != kEmpty ? sb : kNone, me != kEmpty ? sl : 0xFFFFFFFFu, lane);
     }
-}
-
-__device__ __forceinline__ uint4 load_query_f32(const uint8_t* queries, uint32_t pitch, uint32_t q, int lane) {
-    return uint32_t(lane) < (pitch >> 4) ? *reinterpret_cast<const uint4*>(queries + uint64_t(q) * pitch + lane * 16)
-                                         : make_uint4(0, 0, 0, 0);
 }
 
 template <int R>
@@ -736,18 +758,23 @@ __device__ __forceinline__ void write_result_f32(const RefineArgs& a, uint32_t q
 }
 
 template <int R>
-__global__ void __launch_bounds__(kRefineThreads, 4) k_gather_f32(RefineArgs a, const uint32_t* __restrict__ lists,
-                                                                  const uint32_t* __restrict__ counts,
-                                                                  uint32_t lstride) {
-    const int lane = threadIdx.x & 31;
+__global__ void __launch_bounds__(kRefineThreads) k_gather_f32(RefineArgs a, const uint32_t* __restrict__ lists,
+                                                               const uint32_t* __restrict__ counts,
+                                                               uint32_t lstride) {
+    extern __shared__ __align__(128) uint8_t f32_smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t rstride = f32_tile_stride(a.pitch);
+    uint8_t* tile = f32_smem + warp * f32_warp_smem(a.pitch);
+    uint8_t* qs = tile + kF32Rows * rstride;
     const uint32_t qstep = gridDim.x * (kRefineThreads / 32);
     for (uint32_t q = (blockIdx.x * kRefineThreads + threadIdx.x) >> 5; q < a.nq; q += qstep) {
         const uint32_t n = __ldcg(counts + q);
         const uint32_t qq = a.qorder ? __ldg(a.qorder + q) : q;  // list q holds query qq
-        const uint4 qv = load_query_f32(a.queries, a.pitch, qq, lane);
+        stage_query_f32(a.queries, a.pitch, qq, qs, lane);
         WarpTopK2<R> tk;
         tk.init(int(a.k));
-        gather_list_f32<R, false>(a.rows, a.pitch, lists + uint64_t(q) * lstride, n, 0, 8, qv, lane, tk, a.idtab);
+        gather_list_f32<R, false>(a.rows, a.pitch, lists + uint64_t(q) * lstride, n, 0, kF32Rows, qs, tile, lane, tk,
+                                  a.idtab);
         write_result_f32<R>(a, qq, tk, lane, n);
     }
 }
@@ -774,33 +801,50 @@ __device__ __forceinline__ void merge_warps_f32(WarpTopK2<R>& tk, uint64_t* ma, 
 template <int R, int NW>
 __global__ void __launch_bounds__(NW * 32) k_gather_cta_f32(RefineArgs a, const uint32_t* __restrict__ lists,
                                                             const uint32_t* __restrict__ counts, uint32_t lstride) {
+    extern __shared__ __align__(128) uint8_t f32_smem[];
     __shared__ uint64_t ma[NW * 32 * R];
     __shared__ uint32_t mb[NW * 32 * R];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t rstride = f32_tile_stride(a.pitch);
+    uint8_t* tile = f32_smem + warp * f32_warp_smem(a.pitch);
+    uint8_t* qs = tile + kF32Rows * rstride;
     for (uint32_t q = blockIdx.x; q < a.nq; q += gridDim.x) {
         const uint32_t n = __ldcg(counts + q);
-        const uint4 qv = load_query_f32(a.queries, a.pitch, a.qorder ? __ldg(a.qorder + q) : q, lane);
+        const uint32_t qq = a.qorder ? __ldg(a.qorder + q) : q;
+        stage_query_f32(a.queries, a.pitch, qq, qs, lane);
         WarpTopK2<R> tk;
         tk.init(int(a.k));
-        gather_list_f32<R, false>(a.rows, a.pitch, lists + uint64_t(q) * lstride, n, warp * 8, NW * 8, qv, lane, tk,
-                                  a.idtab);
+        gather_list_f32<R, false>(a.rows, a.pitch, lists + uint64_t(q) * lstride, n, warp * kF32Rows, NW * kF32Rows,
+                                  qs, tile, lane, tk, a.idtab);
         merge_warps_f32<R, NW>(tk, ma, mb, a.k, lane, warp);
-        if (warp == 0) write_result_f32<R>(a, a.qorder ? __ldg(a.qorder + q) : q, tk, lane, n);
+        if (warp == 0) write_result_f32<R>(a, qq, tk, lane, n);
         __syncthreads();
     }
+}
+
+template <class K>
+hcg_status f32_smem_opt_in(K kern, size_t smem) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess)
+        return set_error(HCG_ECAPACITY, "f32 gather: shared-memory tile too large");
+    return HCG_OK;
 }
 
 template <int R>
 hcg_status gather_f32_launch(const RefineArgs& a, const uint32_t* lists, const uint32_t* counts, uint32_t lstride,
                              int sms, cudaStream_t st) {
+    const size_t wsm = f32_warp_smem(a.pitch);
     if (a.nq * 2 < uint32_t(sms) * 16 * 8) {
-        k_gather_cta_f32<R, 8><<<a.nq, 256, 0, st>>>(a, lists, counts, lstride);
+        auto kern = k_gather_cta_f32<R, 8>;
+        HCG_RET_IF(f32_smem_opt_in(kern, 8 * wsm));
+        kern<<<a.nq, 256, 8 * wsm, st>>>(a, lists, counts, lstride);
         return check_launch("k_gather_cta_f32");
     }
-    // 4 CTAs/SM (64 registers): f32 rows are latency-bound at low occupancy --
-    // 10M x 100K: 29.4 ms at 2 CTAs/SM, 22.3 at 3, 21.4 at 4
-    const uint32_t blocks = std::min<uint32_t>((a.nq + 7) / 8, uint32_t(sms) * 4);
-    k_gather_f32<R><<<blocks, kRefineThreads, 0, st>>>(a, lists, counts, lstride);
+    auto kern = k_gather_f32<R>;
+    HCG_RET_IF(f32_smem_opt_in(kern, 8 * wsm));
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRefineThreads, 8 * wsm);
+    const uint32_t blocks = std::min<uint32_t>((a.nq + 7) / 8, uint32_t(sms) * uint32_t(std::max(per_sm, 1)));
+    kern<<<blocks, kRefineThreads, 8 * wsm, st>>>(a, lists, counts, lstride);
     return check_launch("k_gather_f32");
 }
 
@@ -1107,6 +1151,21 @@ __global__ void __launch_bounds__(kRefineThreads) k_union_cas(RefineArgs a, uint
 namespace {
 int r_bucket(uint32_t k) { return k <= 32 ? 1 : k <= 64 ? 2 : k <= 128 ? 4 : 8; }
 
+// Device attributes of the refine launches, queried once per device.
+struct DevInfo {
+    int sms = 0;
+};
+const DevInfo& dev_info(int device) {
+    static DevInfo info[64];
+    DevInfo& d = info[device & 63];
+    if (d.sms == 0) {
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+        d.sms = sms;
+    }
+    return d;
+}
+
 template <class K>
 hcg_status opt_in_smem(K kern, int device, bool* configured) {
     if (device < 64 && !configured[device]) {
@@ -1119,10 +1178,9 @@ hcg_status opt_in_smem(K kern, int device, bool* configured) {
 }
 
 uint32_t persistent_grid(const void* kern, size_t smem, int device, uint32_t nq) {
-    int sms = 148, per_sm = 1;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRefineThreads, smem);
-    return std::min<uint32_t>(nq, uint32_t(sms * std::max(per_sm, 1)));
+    return std::min<uint32_t>(nq, uint32_t(dev_info(device).sms * std::max(per_sm, 1)));
 }
 
 size_t union_smem_bytes(uint32_t C, uint32_t T, uint32_t tb) {
@@ -1139,10 +1197,13 @@ hcg_status union_reg_launch(const RefineArgs& a, uint32_t* lists, uint32_t* coun
     const size_t smem = (size_t(8) << tb) + size_t(a.C) * 12 + 4 * (NT / 32) + 64;
     static bool cfg[64] = {};
     HCG_RET_IF(opt_in_smem(kern, device, cfg));
-    int sms = 148, per_sm = 1;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem);
-    const uint32_t grid = std::min<uint32_t>(a.nq, uint32_t(sms * std::max(per_sm, 1)));
+    static int per_sm_cache[64][32] = {};  // by device and table bits (the smem size)
+    int& per_sm = per_sm_cache[device & 63][tb & 31];
+    if (per_sm == 0) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem);
+        per_sm = std::max(per_sm, 1);
+    }
+    const uint32_t grid = std::min<uint32_t>(a.nq, uint32_t(dev_info(device).sms * per_sm));
     kern<<<grid, NT, smem, st>>>(a, lists, counts, lstride, tb);
     return check_launch("k_union_reg");
 }
@@ -1176,12 +1237,28 @@ hcg_status launch_union_reg(const RefineArgs& a, uint32_t* lists, uint32_t* coun
 // Query chunk so the per-call list scratch stays within kListBudget.
 constexpr size_t kListBudget = size_t(2) << 30;
 
+// Largest candidate walk C x take a query may have (the union's hash table
+// is sized from it; 2^27 entries keeps every table index in 32 bits).
+constexpr uint64_t kMaxWalk = uint64_t(1) << 27;
+
+// The union-less K3c (k_gather_nu) serves k <= 32, u8 rows in curve-0
+// order and batches of >= 16K queries; everything else runs the separate
+// union (K3b) + K3c.  One predicate for the scratch query and the launch.
+template <int R>
+bool unionless_path(const RefineArgs& a) {
+    static const bool off = getenv("HCG_NO_UNIONLESS") != nullptr;  // A/B: separate union for every k
+    return R == 1 && !off && a.mode != kOutCandidates && a.dtype == HCG_U8 && a.nq >= 16384 && a.idtab != nullptr;
+}
+
 template <int R, int CR>
 hcg_status refine_dispatch(const RefineArgs& a_in, void* scratch, size_t* scratch_bytes, int device, cudaStream_t st) {
+    if (uint64_t(a_in.C) * a_in.take > kMaxWalk)
+        return set_error(HCG_ECAPACITY, "candidate walk curves x probe depth exceeds 2^27 entries");
     const uint32_t T = a_in.C * a_in.take;
     uint32_t tb = 5;
     while ((uint64_t(1) << tb) * 7 < uint64_t(T) * 10) ++tb;
     if (tb > 28) return set_error(HCG_ECAPACITY, "candidate set too large");
+    const bool nu = unionless_path<R>(a_in);
     const uint32_t lstride = (T + 31) & ~31u;  // 128-B aligned per-query lists
     // the shared-memory union's tag table at <= ~0.35 load factor
     const uint32_t utb = std::min<uint32_t>(tb + 1, 16);
@@ -1189,19 +1266,19 @@ hcg_status refine_dispatch(const RefineArgs& a_in, void* scratch, size_t* scratc
     const bool smem_union = T <= kUnionMaxT && usmem <= 160 * 1024;
     static const bool force_smem_union = getenv("HCG_UNION_SMEM") != nullptr;
     const bool reg_union = T <= 32u * 256 && (size_t(8) << tb) <= 128 * 1024 && !force_smem_union;
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    const int sms = dev_info(device).sms;
     const uint32_t chunk = uint32_t(std::max<size_t>(1, std::min<size_t>(a_in.nq, kListBudget / (size_t(lstride) * 4))));
     const uint32_t cas_ctas = uint32_t(sms) * 4;
-    const size_t lists_bytes = size_t(chunk) * lstride * 4;
-    const size_t counts_bytes = (size_t(chunk) * 4 + 255) & ~size_t(255);
-    const size_t table_bytes = smem_union ? 0 : (size_t(cas_ctas) << tb) * 4;
+    // the union-less walk reads the windows in place: no lists, counts or tables
+    const size_t lists_bytes = nu ? 0 : size_t(chunk) * lstride * 4;
+    const size_t counts_bytes = nu ? 0 : (size_t(chunk) * 4 + 255) & ~size_t(255);
+    const size_t table_bytes = (nu || smem_union) ? 0 : (size_t(cas_ctas) << tb) * 4;
     // Large batches run in curve-0 window order: queries processed at the
     // same time share candidate rows (rows are stored in curve-0 order), so
     // part of the gather hits L2 (measured 5.15 -> 4.75 ms at 100K queries).
     static const bool no_qsort = getenv("HCG_NO_QSORT") != nullptr;
-    const bool qsort = !no_qsort && reg_union && a_in.mode != kOutCandidates && a_in.nq >= 16384 &&
-                       chunk >= a_in.nq && a_in.idtab != nullptr;  // both gathers map list q -> qorder[q]
+    const bool qsort = !no_qsort && (nu || reg_union) && a_in.mode != kOutCandidates && a_in.nq >= 16384 &&
+                       (nu || chunk >= a_in.nq) && a_in.idtab != nullptr;  // both gathers map list q -> qorder[q]
     const size_t qsort_bytes = qsort ? size_t(a_in.nq) * 24 + radix_counts_bytes(a_in.nq) + 256 : 0;
     if (!scratch) {
         *scratch_bytes = lists_bytes + counts_bytes + table_bytes + qsort_bytes;
@@ -1239,33 +1316,30 @@ hcg_status refine_dispatch(const RefineArgs& a_in, void* scratch, size_t* scratc
     auto gk = k_gather<R, CR, R <= 4 ? 3 : 2>;
     static bool cfg_u[64] = {};
     if (smem_union) HCG_RET_IF(opt_in_smem(k_union, device, cfg_u));
-    int g_per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_per_sm, gk, kRefineThreads, 0);
-    static const bool no_union_path = getenv("HCG_NO_UNIONLESS") != nullptr;
-    static const bool nu_r2 = getenv("HCG_NU_R2") != nullptr;  // A/B: union-less for 32 < k <= 64
-    if constexpr (R <= 2) {
-        // k <= 32 and large batches: skip the union, walk the windows directly
-        if (!no_union_path && (R == 1 || nu_r2) && a_in.mode != kOutCandidates && a_in.dtype == HCG_U8 && a_in.nq >= 16384 &&
-            a_in.idtab != nullptr) {
+    static int g_per_sm_cache[64] = {};
+    int& g_per_sm = g_per_sm_cache[device & 63];
+    if (g_per_sm == 0) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_per_sm, gk, kRefineThreads, 0);
+        g_per_sm = std::max(g_per_sm, 1);
+    }
+    if constexpr (R == 1) {
+        // k <= 32 and large batches: skip the union, walk the windows directly.
+        // 3 CTAs/SM (72 registers): 2 leaves DRAM latency uncovered, 4 forces
+        // 64 registers and spills the top-k (profiles/r01_nu_occupancy_ab.txt).
+        if (nu) {
             RefineArgs a = a_in;
             a.qorder = qorder;
-            // HCG_NU_MINB / HCG_NU_PER_SM: tuning knobs (register budget and
-            // resident CTAs per SM = queries in flight sharing L2)
-            static const int nu_minb = getenv("HCG_NU_MINB") ? atoi(getenv("HCG_NU_MINB")) : 3;
-            static const int nu_cap = getenv("HCG_NU_PER_SM") ? atoi(getenv("HCG_NU_PER_SM")) : 0;
-            // HCG_NU_MINB=6: 128-thread CTAs, 6 per SM (same 24 warps, finer tail)
-            const int nt = nu_minb == 6 ? 128 : kRefineThreads;
-            auto nk = nu_minb == 2   ? k_gather_nu<R, CR, 2>
-                      : nu_minb == 4 ? k_gather_nu<R, CR, 4>
-                      : nu_minb == 6 ? k_gather_nu<R, CR, 6, 128>
-                                     : k_gather_nu<R, CR, 3>;
-            int per_sm = 1;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nk, nt, 0);
-            if (nu_cap > 0) per_sm = std::min(per_sm, nu_cap);
-            const uint32_t blocks = std::min<uint32_t>((a.nq + nt / 32 - 1) / (nt / 32), uint32_t(sms * std::max(per_sm, 1)));
+            auto nk = a.C <= 32 ? k_gather_nu<R, CR, 3, true> : k_gather_nu<R, CR, 3, false>;
+            static int per_sm_cache[64][2] = {};
+            int& per_sm = per_sm_cache[device & 63][a.C <= 32 ? 1 : 0];
+            if (per_sm == 0) {
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nk, kRefineThreads, 0);
+                per_sm = std::max(per_sm, 1);
+            }
+            const uint32_t blocks = std::min<uint32_t>((a.nq + 7) / 8, uint32_t(sms * per_sm));
             if (a.ev_mid) cudaEventRecord(a.ev_mid, st);  // timed split: (batch order) | fused gather
             count_launches(1);
-            nk<<<blocks, nt, 0, st>>>(a);
+            nk<<<blocks, kRefineThreads, 0, st>>>(a);
             HCG_RET_IF(check_launch("k_gather_nu"));
             return HCG_OK;
         }
@@ -1471,20 +1545,23 @@ static hcg_status brute_launch(const BruteArgs& a, uint64_t* scratch, cudaStream
     return check_launch("k_brute");
 }
 
-// f32 rows: warp per (query, chunk of rows) through the gather path, then a
-// pair merge over the chunks.  Scratch: chunks x nq x k (u64 key, u32 slot).
+// f32 rows: warp per (query, chunk of rows) through the exact gather path,
+// then a pair merge over the chunks.  Scratch: chunks x nq x k (u64 key, u32 slot).
 template <int R>
 __global__ void __launch_bounds__(256) k_brute_f32(BruteArgs a, uint64_t* __restrict__ part_a,
                                                    uint32_t* __restrict__ part_b) {
+    extern __shared__ __align__(128) uint8_t f32_smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t chunk = blockIdx.x, q = blockIdx.y * 8 + warp;
     if (q >= a.nq) return;
+    uint8_t* tile = f32_smem + warp * f32_warp_smem(a.pitch);
+    uint8_t* qs = tile + kF32Rows * f32_tile_stride(a.pitch);
     const uint64_t r0 = uint64_t(chunk) * kBruteChunk;
     const uint32_t r1 = uint32_t(min(a.n, r0 + kBruteChunk));
-    const uint4 qv = load_query_f32(a.queries, a.pitch, q, lane);
+    stage_query_f32(a.queries, a.pitch, q, qs, lane);
     WarpTopK2<R> tk;
     tk.init(int(a.k));
-    gather_list_f32<R, true>(a.rows, a.pitch, nullptr, r1, uint32_t(r0), 8, qv, lane, tk, a.idtab);
+    gather_list_f32<R, true>(a.rows, a.pitch, nullptr, r1, uint32_t(r0), kF32Rows, qs, tile, lane, tk, a.idtab);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const uint32_t e = uint32_t(lane) * R + r;
@@ -1535,7 +1612,9 @@ static hcg_status brute_f32_launch(const BruteArgs& a, uint64_t* scratch, uint64
     const uint32_t chunks = uint32_t((a.n + kBruteChunk - 1) / kBruteChunk);
     uint64_t* pa = scratch;
     uint32_t* pb = reinterpret_cast<uint32_t*>(scratch + uint64_t(chunks) * a.nq * a.k);
-    k_brute_f32<R><<<dim3(chunks, (a.nq + 7) / 8), 256, 0, st>>>(a, pa, pb);
+    const size_t smem = 8 * size_t(f32_warp_smem(a.pitch));
+    HCG_RET_IF(f32_smem_opt_in(k_brute_f32<R>, smem));
+    k_brute_f32<R><<<dim3(chunks, (a.nq + 7) / 8), 256, smem, st>>>(a, pa, pb);
     HCG_RET_IF(check_launch("k_brute_f32"));
     k_merge_f32<R><<<unsigned((uint64_t(a.nq) * 32 + 255) / 256), 256, 0, st>>>(pa, pb, chunks, a, out_ids, out_sq,
                                                                                  out_len);

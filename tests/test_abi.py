@@ -139,3 +139,27 @@ def test_planner_host_functions():
     assert H.miss_bound(10, 1, 5) == 1.0
     with pytest.raises(ValueError):
         H.binomial_tail(10, 1.5, 3)
+
+
+@pytest.mark.parametrize("offset,scale,ok", [
+    (0.0, 1.0, True),            # raw bytes
+    (1.0, 1.0 / 256, True),      # lifted
+    (-64.0, 0.5, True),          # any exact power-of-two view
+    (0.0, 0.1, False),           # not a power of two: sqrt(S) * scale would round differently
+    (0.0, 3.0, False),
+    (1e8, 1.0, False),           # 1e8 + b is not exact in float32
+])
+def test_u8_view_must_be_exact(offset, scale, ok):
+    """A u8 index reports sqrt(S) * scale for the integer S; that is the
+    reference's rooted double only for views whose floats are exact and whose
+    scale is a power of two, so other views are rejected up front (before any
+    device work, so this runs without a GPU)."""
+    s = _scheme()
+    s.dist_scale = scale
+    s.view_offset = offset
+    rc = _build_rc(s)
+    if ok:
+        assert rc in (_lib.HCG_OK, _lib.HCG_ENODEV)
+    else:
+        assert rc == _lib.HCG_EINVAL
+        assert b"u8 view" in H.lib().hcg_last_error()

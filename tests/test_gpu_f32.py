@@ -2,11 +2,11 @@
 type, quantized on the device by float_to_ordinal >> (32 - m)
 (curve.cpp:166-174) and scored in double (vecio.cpp:87-95).
 
-Keys, sorted subindexes, windows and candidate sets are bit-exact against the
-oracle.  Distances: the GPU sums the same double terms in a fixed tree order,
-the reference sequentially, so rooted distances agree to rtol 1e-12 (exactly
-when every partial sum is exact, e.g. integer-valued components -- checked
-bit-for-bit below) and top-k ids agree exactly.
+Keys, sorted subindexes, windows, candidate sets, top-k ids and rooted
+distances are all bit-exact against the oracle: the GPU sums the reference's
+double terms (double(a) - double(b))^2 sequentially in index order with
+separately rounded subtract / multiply / add, the same double as
+squared_distance (vecio.cpp:87-95), so near-ties order as the reference orders them.
 """
 import os
 
@@ -22,7 +22,6 @@ pytestmark = [pytest.mark.gpu,
 import paper_1209_0410_b200 as H  # noqa: E402
 from paper_1209_0410_b200._lib import HcgError  # noqa: E402
 
-RTOL = 1e-12  # f64 tree sum vs the reference's sequential f64 sum
 
 
 def float_rows(n, d, seed, scale=40.0):
@@ -41,7 +40,7 @@ def _oracle(rows, curves, m, kind):
     return P.Oracle(rows, curves, m, kind)
 
 
-def _check_search(gi, oi, qs, k, depth, exact=False):
+def _check_search(gi, oi, qs, k, depth, exact=True):
     ids, sq, ln = gi.search_batch(qs, k, depth)
     oids, odist, oln = oi.search(qs, k, depth)
     np.testing.assert_array_equal(ln, oln)
@@ -49,10 +48,7 @@ def _check_search(gi, oi, qs, k, depth, exact=False):
     for q in range(qs.shape[0]):
         L = int(ln[q])
         np.testing.assert_array_equal(ids[q, :L], oids[q, :L])
-        if exact:
-            assert d[q, :L].tobytes() == odist[q, :L].tobytes(), (q, d[q, :L], odist[q, :L])
-        else:
-            np.testing.assert_allclose(d[q, :L], odist[q, :L], rtol=RTOL, atol=0)
+        assert d[q, :L].tobytes() == odist[q, :L].tobytes(), (q, d[q, :L], odist[q, :L])
         assert (ids[q, L:] == np.uint64(2**64 - 1)).all()
         assert np.isinf(sq[q, L:]).all()
 
@@ -131,7 +127,7 @@ def test_f32_brute_force(k):
     oids, odist, oln = P.brute_force(rows, qs, k)
     np.testing.assert_array_equal(ln, oln)
     np.testing.assert_array_equal(ids, oids)
-    np.testing.assert_allclose(gi.rooted(sq), odist, rtol=RTOL, atol=0)
+    assert gi.rooted(sq).tobytes() == odist.tobytes()
 
 
 def test_f32_small_batch_paths_and_device_buffers():
@@ -235,3 +231,38 @@ def test_f32_large_batch():
     gi = H.MulticurvesIndex(rows, H.default_scheme(128, 8, 16))
     oi = _oracle(rows, 8, 16, H.HILBERT)
     _check_search(gi, oi, qs, 10, 300)
+
+
+def test_f32_sequential_sum_near_ties():
+    """Rows whose squared distances depend on the summation order: with
+    (2^27, 1, 1, ...) against a zero query, the reference's sequential sum
+    (vecio.cpp:90-93) absorbs every 1 into 2^54 (ulp 4), so the row ties
+    with (2^27, 0, 0, ...) and the lower id wins; any other order (e.g. a
+    tree) would add the ones up and put it second."""
+    d = 128
+    rng = np.random.default_rng(11)
+    rows = (rng.standard_normal((300, d)) * 5e7).astype(np.float32)  # far: d^2 ~ 3e17 > 2^54
+    crafted = np.zeros((4, d), np.float32)
+    crafted[:, 0] = np.float32(2.0 ** 27)
+    crafted[0, 1:] = 1.0       # id 100: sequential sum 2^54
+    crafted[1, 1:] = 0.0       # id 101: 2^54 exactly
+    crafted[2, 1:5] = 3.0      # id 102: 2^54 + 9 + ... rounds
+    crafted[3, 1:] = -1.0      # id 103: same as 100
+    rows[100:104] = crafted
+    q = np.zeros((1, d), np.float32)
+    scheme = H.default_scheme(d, 1, 8)
+    gi = H.MulticurvesIndex(rows, scheme)
+    oi = P.Oracle(rows, 1, 8, H.HILBERT)
+    for fn in ("search", "brute"):
+        if fn == "search":
+            ids, sq, ln = gi.search_batch(q, 8, 1000)
+            oids, odist, oln = oi.search(q, 8, 1000)
+        else:
+            ids, sq, ln = gi.brute_force(q, 8)
+            oids, odist, oln = P.brute_force(rows, q, 8)
+        np.testing.assert_array_equal(ids, oids)
+        assert gi.rooted(sq).tobytes() == odist.tobytes()
+    ids, sq, _ = gi.brute_force(q, 8)
+    pos = {int(i): r for r, i in enumerate(ids[0])}
+    assert sq[0, pos[100]] == sq[0, pos[101]] == 2.0 ** 54  # the ones were absorbed
+    assert pos[100] < pos[101] < pos[103]

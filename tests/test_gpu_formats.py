@@ -105,3 +105,52 @@ def test_load_recovers_scheme_and_view(tmp_path):
     assert gi.search(qs[0], H.SearchParams(10, 100)) == back.search(qs[0], H.SearchParams(10, 100))
     np.testing.assert_array_equal(back.retrieve_candidates(qs[3], 2, 50), gi.subindex(2)[
         int(gi.windows(qs[3], 50)[1][0, 2]):int(gi.windows(qs[3], 50)[2][0, 2])])
+
+
+@pytest.mark.parametrize("view,m", [(H.LIFTED, 16), (H.RAW, 8)])
+def test_insert_then_large_batch_search(view, m):
+    """An inserted index searched with >= 16K queries runs the union-less
+    k_gather_nu, which maps physical rows back to ids through the id table
+    that inserts extend (appended rows sit at physical = id slot): results
+    equal the oracle over all rows and a fresh build of the union."""
+    rows = P.gen_rows(0, 9000)
+    qs = P.gen_queries(0, 20000, 9000)
+    sch = H.default_scheme(128, 8, m)
+    inc = H.MulticurvesIndex(rows[:6000], sch, view)
+    inc.insert(rows[6000:7500])
+    inc.insert(rows[7500:])
+    full = H.MulticurvesIndex(rows, sch, view)
+    for k, depth in ((10, 350), (1, 40), (32, 1000)):
+        gi, gs, gl = inc.search_batch(qs, k, depth)
+        fi, fs, fl = full.search_batch(qs, k, depth)
+        np.testing.assert_array_equal(gi, fi)
+        np.testing.assert_array_equal(gs, fs)
+        np.testing.assert_array_equal(gl, fl)
+    oi = P.Oracle(view.floats(rows), 8, m)
+    oids, odist, oln = oi.search(view.floats(qs), 10, 350)
+    gi, gs, gl = inc.search_batch(qs, 10, 350)
+    np.testing.assert_array_equal(gl, oln)
+    np.testing.assert_array_equal(gi, oids)
+    assert inc.rooted(gs).tobytes() == odist.tobytes()
+
+
+@pytest.mark.parametrize("how", ["out_of_range", "duplicate"])
+def test_load_rejects_corrupt_slots(tmp_path, how):
+    """A slot array that is not a permutation of the rows fails with
+    HCG_EIO instead of becoming out-of-bounds row gathers."""
+    rows = P.gen_rows(0, 2000)
+    gi = H.MulticurvesIndex(rows, H.default_scheme(128, 4, 8), H.RAW)
+    path = tmp_path / "x.hcg"
+    gi.save(str(path))
+    raw = bytearray(path.read_bytes())
+    # the last curve's slots are the 2000 u32 right before the 8-byte trailer
+    end = len(raw) - 8
+    slots = np.frombuffer(bytes(raw[end - 4 * 2000:end]), np.uint32).copy()
+    if how == "out_of_range":
+        slots[17] = 2000
+    else:
+        slots[17] = slots[18]
+    raw[end - 4 * 2000:end] = slots.tobytes()
+    path.write_bytes(bytes(raw))
+    with pytest.raises(H.HcgIOError):
+        H.MulticurvesIndex.load(str(path))
