@@ -9,9 +9,9 @@
 //     hcb::NeighborList nl = idx.search(q, {10, 350});
 //
 // and gets the same NeighborLists from the B200.  The default view keeps the
-// float components as they are (HCG_F32: same ids and tie order, distances
-// within 1e-12 relative -- the double terms are summed in a tree instead of
-// sequentially).  Byte-valued data can instead be stored as one byte per
+// float components as they are (HCG_F32: the reference's double squared
+// distances bit for bit -- sequential sums in index order -- so the same ids,
+// distances and tie order).  Byte-valued data can instead be stored as one byte per
 // component through View::raw() (bvecs) or View::lifted() (1 + b/256): a 4x
 // smaller row, exact integer distances, bit-identical NeighborLists.  The dataset and
 // query types are templates: anything with hc::Dataset / hc::FeatureVector's
@@ -102,6 +102,29 @@ void append_floats(const Vec& v, std::uint32_t dims, std::vector<float>& out) {
     if (v.components.size() != dims) throw std::invalid_argument("dimension mismatch");
     out.insert(out.end(), v.components.begin(), v.components.end());
 }
+
+// The hcg_scheme of a ProjectionScheme seen through a view (owns the assignment arrays).
+struct CScheme {
+    std::vector<std::uint32_t> off{0}, asg;
+    hcg_scheme s{};
+    CScheme(const ProjectionScheme& scheme, const View& view) {
+        for (const auto& slots : scheme.assignment) {
+            asg.insert(asg.end(), slots.begin(), slots.end());
+            off.push_back(static_cast<std::uint32_t>(asg.size()));
+        }
+        s.d_full = scheme.d_full;
+        s.curves = scheme.curves();
+        s.bits_per_dim = scheme.bits_per_dim;
+        s.curve_kind = static_cast<std::uint32_t>(scheme.curve_kind);
+        s.assign_off = off.data();
+        s.assign = asg.data();
+        s.dist_scale = view.f32 ? 1.0 : view.scale;
+        s.dtype = view.f32 ? HCG_F32 : HCG_U8;
+        s.view_offset = view.f32 ? 0.0f : view.offset;
+        if (!view.f32) check(hcg_make_lut(view.offset, view.scale, scheme.bits_per_dim, s.cell_lut));
+    }
+    CScheme(const CScheme&) = delete;
+};
 
 inline void check_params(const SearchParams& p) {
     if (p.k < 1 || p.probe_depth < 1) throw std::invalid_argument("invalid search params");
@@ -317,27 +340,113 @@ class MulticurvesIndex {
 
     void build(const void* rows, std::uint64_t n, int device, std::uint64_t id_base = 0,
                std::uint64_t id_stride = 1) {
-        std::vector<std::uint32_t> off{0}, asg;
-        for (const auto& slots : scheme_.assignment) {
-            asg.insert(asg.end(), slots.begin(), slots.end());
-            off.push_back(static_cast<std::uint32_t>(asg.size()));
-        }
-        hcg_scheme s{};
-        s.d_full = scheme_.d_full;
-        s.curves = scheme_.curves();
-        s.bits_per_dim = scheme_.bits_per_dim;
-        s.curve_kind = static_cast<std::uint32_t>(scheme_.curve_kind);
-        s.assign_off = off.data();
-        s.assign = asg.data();
-        s.dist_scale = view_.f32 ? 1.0 : view_.scale;
-        s.dtype = view_.f32 ? HCG_F32 : HCG_U8;
-        s.view_offset = view_.f32 ? 0.0f : view_.offset;
-        if (!view_.f32) detail::check(hcg_make_lut(view_.offset, view_.scale, scheme_.bits_per_dim, s.cell_lut));
-        detail::check(hcg_build(&s, static_cast<const std::uint8_t*>(rows), n, id_base, id_stride, device, nullptr,
+        detail::CScheme cs(scheme_, view_);
+        detail::check(hcg_build(&cs.s, static_cast<const std::uint8_t*>(rows), n, id_base, id_stride, device, nullptr,
                                 &ix_));
     }
 
     hcg_index* ix_ = nullptr;
+    ProjectionScheme scheme_;
+    View view_;
+};
+
+// The hypershard module on the GPUs of one process: global
+// id i lives on shard i mod G (devices[i mod G]) at local slot i / G; a search
+// runs every shard at the per-shard probe depth, all-gathers the packed top-k
+// lists with NCCL over NVLink and merges them by (distance, id), truncated to
+// k (aggregate) -- the reference's per-shard
+// MulticurvesIndex::search + aggregate, bit for bit.  Byte views only.
+class ShardedIndex {
+  public:
+    ShardedIndex() = default;
+
+    // n x d_full view bytes (host or device memory), shard r built on devices[r].
+    ShardedIndex(const std::uint8_t* rows, std::uint64_t n, ProjectionScheme scheme, View view,
+                 const std::vector<int>& devices)
+        : scheme_(std::move(scheme)), view_(view) {
+        if (view_.f32) throw std::invalid_argument("sharded indexes store byte views");
+        detail::CScheme cs(scheme_, view_);
+        detail::check(hcg_shard_group_build(&cs.s, rows, n, static_cast<std::uint32_t>(devices.size()),
+                                            devices.data(), &g_));
+    }
+
+    template <class Dataset>
+    ShardedIndex(const Dataset& ds, ProjectionScheme scheme, View view, const std::vector<int>& devices)
+        : scheme_(std::move(scheme)), view_(view) {
+        if (view_.f32) throw std::invalid_argument("sharded indexes store byte views");
+        std::vector<std::uint8_t> rows;
+        rows.reserve(ds.vectors.size() * scheme_.d_full);
+        for (std::size_t i = 0; i < ds.vectors.size(); ++i) {
+            if (ds.vectors[i].id != i) throw std::invalid_argument("dataset ids must be 0..n-1 in order (vecio.hpp:22)");
+            detail::append_bytes(ds.vectors[i], scheme_.d_full, view_, rows);
+        }
+        detail::CScheme cs(scheme_, view_);
+        detail::check(hcg_shard_group_build(&cs.s, rows.data(), ds.vectors.size(),
+                                            static_cast<std::uint32_t>(devices.size()), devices.data(), &g_));
+    }
+
+    // One process per GPU: rank `rank` of G joins with its shard (built with
+    // id_base rank, id_stride G); every rank calls this with the same id.
+    static ShardedIndex join(const hcg_nccl_id& id, std::uint32_t rank, std::uint32_t G, MulticurvesIndex& local,
+                             View view) {
+        ShardedIndex s;
+        s.scheme_ = local.scheme();
+        s.view_ = view;
+        detail::check(hcg_shard_group_join(&id, rank, G, local.handle(), &s.g_));
+        return s;
+    }
+
+    ShardedIndex(const ShardedIndex&) = delete;
+    ShardedIndex& operator=(const ShardedIndex&) = delete;
+    ShardedIndex(ShardedIndex&& o) noexcept { *this = std::move(o); }
+    ShardedIndex& operator=(ShardedIndex&& o) noexcept {
+        std::swap(g_, o.g_);
+        std::swap(scheme_, o.scheme_);
+        std::swap(view_, o.view_);
+        return *this;
+    }
+    ~ShardedIndex() {
+        if (g_) hcg_shard_group_free(g_);
+    }
+
+    std::uint32_t shards() const { return g_ ? hcg_shard_group_shards(g_) : 0; }
+    hcg_shard_group* handle() const { return g_; }
+
+    // Per-shard probe depth 2 phi* for a sequential depth D: the smallest phi
+    // with miss bound <= target for Phi = ceil(D / 2) (SPEC.md:286-329,
+    // PAPER.md:883-907).
+    static std::size_t plan_depth(std::size_t depth, std::uint32_t shards, double target = 0.02) {
+        return 2 * std::size_t(hcg_plan_depth(static_cast<std::uint32_t>((depth + 1) / 2), shards, target));
+    }
+
+    // Batched search; p.probe_depth is the per-shard depth.
+    std::vector<NeighborList> search_bytes(const std::uint8_t* queries, std::uint32_t nq, const SearchParams& p,
+                                           void* stream = nullptr) const {
+        detail::check_params(p);
+        const std::uint32_t k = static_cast<std::uint32_t>(p.k);
+        std::vector<std::uint64_t> ids(std::size_t(nq) * k);
+        std::vector<std::uint32_t> sq(std::size_t(nq) * k), len(nq);
+        detail::check(hcg_shard_group_search(g_, queries, nq, k, static_cast<std::uint32_t>(p.probe_depth),
+                                             ids.data(), sq.data(), len.data(), stream));
+        std::vector<NeighborList> out(nq);
+        for (std::uint32_t q = 0; q < nq; ++q) {
+            out[q].resize(len[q]);
+            for (std::uint32_t i = 0; i < len[q]; ++i)
+                out[q][i] = {ids[std::size_t(q) * k + i],
+                             std::sqrt(double(sq[std::size_t(q) * k + i])) * double(view_.scale)};
+        }
+        return out;
+    }
+
+    template <class FeatureVector>
+    NeighborList search(const FeatureVector& q, const SearchParams& p) const {
+        std::vector<std::uint8_t> qb;
+        detail::append_bytes(q, scheme_.d_full, view_, qb);
+        return search_bytes(qb.data(), 1, p).front();
+    }
+
+  private:
+    hcg_shard_group* g_ = nullptr;
     ProjectionScheme scheme_;
     View view_;
 };

@@ -297,6 +297,9 @@ def ref() -> C.CDLL:
         L.ref_build.restype = C.c_void_p
         L.ref_build.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, _u8p, C.c_uint64,
                                 C.c_int, C.POINTER(C.c_int)]
+        L.ref_build_ids.restype = C.c_void_p
+        L.ref_build_ids.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, _u8p, C.c_uint64,
+                                    C.c_int, C.c_uint64, C.c_uint64, C.POINTER(C.c_int)]
         L.ref_free.argtypes = [C.c_void_p]
         L.ref_sorted.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p, C.c_void_p]
         L.ref_windows.argtypes = [C.c_void_p, _u8p, C.c_uint64, C.c_uint64, _u64p, _u64p, _u64p]
@@ -318,13 +321,20 @@ def ref_error() -> str:
 class RefIndex:
     """hc::MulticurvesIndex from the reference TUs, over byte rows in a view."""
 
-    def __init__(self, rows_u8: np.ndarray, curves: int, m: int, kind: int = HILBERT, view: int = RAW):
+    def __init__(self, rows_u8: np.ndarray, curves: int, m: int, kind: int = HILBERT, view: int = RAW,
+                 id_base: int = 0, id_stride: int = 1):
+        """id_base / id_stride: row i has id id_base + i * id_stride (one shard
+        of the id mod G partition)."""
         rows = np.ascontiguousarray(rows_u8, np.uint8)
         self.n, self.d = rows.shape
         self.curves = curves
         self.view = view
         err = C.c_int()
-        self.h = ref().ref_build(self.d, curves, m, kind, rows, self.n, view, C.byref(err))
+        if id_base == 0 and id_stride == 1:
+            self.h = ref().ref_build(self.d, curves, m, kind, rows, self.n, view, C.byref(err))
+        else:
+            self.h = ref().ref_build_ids(self.d, curves, m, kind, rows, self.n, view, id_base, id_stride,
+                                         C.byref(err))
         if not self.h:
             raise ValueError(f"ref_build: {ref_error()}")
 
@@ -374,3 +384,44 @@ class RefIndex:
         if ref().ref_brute_force(self.h, qs, nq, k, ids, dist, ln, threads or nthreads()):
             raise ValueError(ref_error())
         return ids, dist, ln
+
+
+def merge_shard_lists(parts, k: int):
+    """Hypershard aggregate over per-shard (ids, dist, len) results: (distance,
+    id) order, truncated to k, vectorised over queries."""
+    nq = parts[0][0].shape[0]
+    ids = np.concatenate([p[0][:, :k] for p in parts], axis=1)
+    dist = np.concatenate([p[1][:, :k] for p in parts], axis=1)
+    valid = np.concatenate([np.arange(k)[None, :] < p[2][:, None] for p in parts], axis=1)
+    dist = np.where(valid, dist, np.inf)
+    ids = np.where(valid, ids, np.uint64(2**64 - 1))
+    oi = np.zeros((nq, k), np.uint64)
+    od = np.zeros((nq, k), np.float64)
+    ln = np.minimum(valid.sum(axis=1), k).astype(np.uint32)
+    for q in range(nq):
+        order = np.lexsort((ids[q], dist[q]))[:k]
+        oi[q] = ids[q, order]
+        od[q] = dist[q, order]
+    return oi, od, ln
+
+
+def ref_sharded_search(n_total: int, shards: int, qs_u8: np.ndarray, curves: int, m: int, kind: int, view: int,
+                       k: int, depths, threads: int | None = None):
+    """The reference's sharded search on the generator's rows: shard r holds
+    global ids r, r + G, ..., each shard is an
+    hc::MulticurvesIndex built from the reference TUs and searched at the
+    per-shard depth, and the per-shard lists are merged by (distance, id).
+    One shard is resident at a time.  depths: int or list; returns the merged
+    (ids, dist, len) per depth (a dict for a list)."""
+    ds = [depths] if isinstance(depths, int) else list(depths)
+    parts = {d: [] for d in ds}
+    for r in range(shards):
+        cnt = 0 if r >= n_total else (n_total - r + shards - 1) // shards
+        rows = gen_rows(r, cnt, threads, stride=shards)
+        ri = RefIndex(rows, curves, m, kind, view, id_base=r, id_stride=shards)
+        del rows
+        for d in ds:
+            parts[d].append(ri.search(qs_u8, k, d, threads))
+        del ri
+    out = {d: merge_shard_lists(parts[d], k) for d in ds}
+    return out[ds[0]] if isinstance(depths, int) else out

@@ -276,6 +276,24 @@ void* ref_build(std::uint32_t dim, std::uint32_t curves, std::uint32_t m, std::u
     return out;
 }
 
+// The same over one shard of an id mod G partition: row i
+// carries the global id id_base + i * id_stride.
+void* ref_build_ids(std::uint32_t dim, std::uint32_t curves, std::uint32_t m, std::uint32_t kind,
+                    const std::uint8_t* rows, std::uint64_t n, int view, std::uint64_t id_base,
+                    std::uint64_t id_stride, int* err) {
+    RefIndex* out = nullptr;
+    *err = guard([&] {
+        hc::Dataset ds;
+        ds.dims = dim;
+        ds.vectors.resize(n);
+        for (std::uint64_t i = 0; i < n; ++i)
+            ds.vectors[i] = make_vec(rows + i * dim, dim, view, id_base + i * id_stride);
+        auto scheme = hc::default_scheme(dim, curves, m, kind ? hc::CurveKind::Hilbert : hc::CurveKind::ZOrder, 0);
+        out = new RefIndex{hc::MulticurvesIndex(ds, scheme), dim, view};
+    });
+    return out;
+}
+
 void ref_free(void* h) { delete static_cast<RefIndex*>(h); }
 
 // keys_out: n x words (LS word first), ids_out: n.

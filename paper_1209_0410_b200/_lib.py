@@ -38,6 +38,8 @@ EXPORTS = [
     "hcg_candidates", "hcg_brute_force", "hcg_binomial_tail", "hcg_miss_bound",
     "hcg_search_f32", "hcg_brute_force_f32", "hcg_index_dtype", "hcg_launch_count", "hcg_sorted_range", "hcg_describe", "hcg_plan_depth", "hcg_gen_rows", "hcg_gen_queries", "hcg_insert", "hcg_save", "hcg_load",
     "hcg_read_vectors", "hcg_write_vectors", "hcg_free_buffer",
+    "hcg_nccl_unique_id", "hcg_shard_group_build", "hcg_shard_group_adopt", "hcg_shard_group_join",
+    "hcg_shard_group_free", "hcg_shard_group_shards", "hcg_shard_group_search", "hcg_index_device", "hcg_index_ids",
 ]
 
 
@@ -54,6 +56,10 @@ class HcgScheme(C.Structure):
         ("dtype", C.c_uint32),
         ("view_offset", C.c_float),
     ]
+
+
+class HcgNcclId(C.Structure):
+    _fields_ = [("internal", C.c_uint8 * 128)]
 
 
 class HcgError(RuntimeError):
@@ -130,11 +136,24 @@ def lib() -> C.CDLL:
     L.hcg_write_vectors.argtypes = [C.c_char_p, u32, C.c_float, C.c_float, vp, u64, u32]
     L.hcg_free_buffer.argtypes = [vp]
     L.hcg_free_buffer.restype = None
+    L.hcg_nccl_unique_id.argtypes = [P(HcgNcclId)]
+    L.hcg_shard_group_build.argtypes = [P(HcgScheme), vp, u64, u32, P(C.c_int), P(vp)]
+    L.hcg_shard_group_adopt.argtypes = [u32, P(vp), P(vp)]
+    L.hcg_shard_group_join.argtypes = [P(HcgNcclId), u32, u32, vp, P(vp)]
+    L.hcg_shard_group_free.argtypes = [vp]
+    L.hcg_shard_group_shards.restype = u32
+    L.hcg_shard_group_shards.argtypes = [vp]
+    L.hcg_shard_group_search.argtypes = [vp, vp, u32, u32, u32, vp, vp, vp, vp]
+    L.hcg_index_device.restype = C.c_int
+    L.hcg_index_device.argtypes = [vp]
+    L.hcg_index_ids.argtypes = [vp, P(u64), P(u64)]
     for name in ("hcg_make_lut", "hcg_default_assignment", "hcg_build", "hcg_free", "hcg_search",
                  "hcg_search_timed", "hcg_search_packed", "hcg_merge_packed", "hcg_keys", "hcg_sorted", "hcg_windows",
                  "hcg_candidates", "hcg_brute_force", "hcg_search_f32", "hcg_brute_force_f32", "hcg_sorted_range",
                  "hcg_describe", "hcg_gen_rows", "hcg_gen_queries", "hcg_insert",
-                 "hcg_save", "hcg_load", "hcg_read_vectors", "hcg_write_vectors"):
+                 "hcg_save", "hcg_load", "hcg_read_vectors", "hcg_write_vectors", "hcg_nccl_unique_id",
+                 "hcg_shard_group_build", "hcg_shard_group_adopt", "hcg_shard_group_join", "hcg_shard_group_free",
+                 "hcg_shard_group_search", "hcg_index_ids"):
         getattr(L, name).restype = C.c_int
     del u8
     _lib = L

@@ -98,6 +98,32 @@ def make_lut(view: View, bits_per_dim: int) -> np.ndarray:
     return np.frombuffer(lut, dtype=np.uint32).copy()
 
 
+def c_scheme(scheme: "ProjectionScheme", view: View, dtype: str = "u8") -> HcgScheme:
+    """The hcg_scheme of a ProjectionScheme seen through `view` (the assignment
+    arrays stay alive with the returned struct)."""
+    off = [0]
+    flat = []
+    for slots in scheme.assignment:
+        flat += list(slots)
+        off.append(len(flat))
+    s = HcgScheme()
+    s._off = (C.c_uint32 * len(off))(*off)
+    s._asg = (C.c_uint32 * max(len(flat), 1))(*flat)
+    s.d_full = scheme.d_full
+    s.curves = scheme.curves()
+    s.bits_per_dim = scheme.bits_per_dim
+    s.curve_kind = scheme.curve_kind
+    s.assign_off = s._off
+    s.assign = s._asg
+    lut = make_lut(view, scheme.bits_per_dim)
+    for b in range(256):
+        s.cell_lut[b] = int(lut[b])
+    s.dist_scale = float(view.scale) if dtype == "u8" else 1.0
+    s.dtype = HCG_U8 if dtype == "u8" else HCG_F32
+    s.view_offset = float(view.offset) if dtype == "u8" else 0.0
+    return s
+
+
 # ----------------------------------------------------------------- buffers ----
 def _torch():
     import torch
@@ -194,26 +220,7 @@ class MulticurvesIndex:
         rows = (_u8_2d(rows, d, dtype) if (rows is not None and len(rows))
                 else np.zeros((0, d), np.uint8 if dtype == "u8" else np.float32))
         n = rows.shape[0]
-        off = [0]
-        flat = []
-        for slots in scheme.assignment:
-            flat += list(slots)
-            off.append(len(flat))
-        self._off = (C.c_uint32 * len(off))(*off)
-        self._asg = (C.c_uint32 * max(len(flat), 1))(*flat)
-        s = HcgScheme()
-        s.d_full = d
-        s.curves = scheme.curves()
-        s.bits_per_dim = scheme.bits_per_dim
-        s.curve_kind = scheme.curve_kind
-        s.assign_off = self._off
-        s.assign = self._asg
-        lut = make_lut(view, scheme.bits_per_dim)
-        for b in range(256):
-            s.cell_lut[b] = int(lut[b])
-        s.dist_scale = float(view.scale) if dtype == "u8" else 1.0
-        s.dtype = HCG_U8 if dtype == "u8" else HCG_F32
-        s.view_offset = float(view.offset) if dtype == "u8" else 0.0
+        s = c_scheme(scheme, view, dtype)
         self._scheme_c = s
         h = C.c_void_p()
         check(lib().hcg_build(C.byref(s), _ptr(rows), n, id_base, id_stride, device,
@@ -561,5 +568,5 @@ __all__ = [
     "MulticurvesIndex", "merge_packed", "binomial_tail", "miss_bound", "plan_depth",
     "write_search_csv", "read_search_csv", "monte_carlo_miss",
     "shard_probe_depth", "gen_rows", "gen_queries", "make_lut", "recall_at", "ZORDER", "HILBERT",
-    "read_vectors", "write_vectors",
+    "read_vectors", "write_vectors", "c_scheme",
 ]

@@ -11,12 +11,21 @@ aggregate : one NCCL all-gather of the packed (sqdist<<32 | gid) top-k lists
             (B x k x 8 bytes per rank), then the K4 merge kernel by
             (distance, id), truncated to k.  The exchange is
             the only device-to-device traffic of the path.
+
+The search runs inside libhcg (hcg_shard_group_*, csrc/shard.cu): the
+library owns the NCCL communicators and issues the all-gather itself;
+torch.distributed only carries the NCCL id at join time and the recall /
+parity side computations outside the timed path.
 """
 from __future__ import annotations
 
 import numpy as np
 
-from .multicurves import MulticurvesIndex, ProjectionScheme, View, gen_rows, merge_packed
+import ctypes as C
+
+from ._lib import HcgNcclId, check, lib
+from .multicurves import (MulticurvesIndex, ProjectionScheme, View, _empty_like_kind, _ptr, _stream, _u8_2d,
+                          c_scheme, gen_rows, merge_packed)
 
 
 def shard_rows(n_total: int, rank: int, world: int) -> int:
@@ -51,6 +60,87 @@ def pack(ids, sqdist, lens, k: int):
     return torch.where(valid, p, torch.full_like(p, -1))
 
 
+class ShardGroup:
+    """hcg_shard_group (include/hcg.h): the partition / aggregate inside
+    libhcg -- per-shard search, ncclAllGather of the packed top-k lists over
+    NVLink and the K4 merge, driven from C++.  No torch.distributed on the
+    search path; torch.distributed only hands the NCCL id to the ranks once
+    (join)."""
+
+    def __init__(self, handle, d_full: int, keep=()):
+        self._h = handle
+        self.d_full = d_full
+        self._keep = list(keep)
+
+    @classmethod
+    def build(cls, rows, scheme: ProjectionScheme, view: View, devices) -> "ShardGroup":
+        """One process, G = len(devices) GPUs: shard r (rows r, r+G, ...) on devices[r]."""
+        r = _u8_2d(rows, scheme.d_full)
+        s = c_scheme(scheme, view)
+        devs = (C.c_int * len(devices))(*devices)
+        h = C.c_void_p()
+        check(lib().hcg_shard_group_build(C.byref(s), _ptr(r), r.shape[0], len(devices), devs, C.byref(h)))
+        return cls(h, scheme.d_full)
+
+    @classmethod
+    def adopt(cls, shards) -> "ShardGroup":
+        """One process over already-built shards (shard r: id_base r, id_stride G,
+        one per GPU); the group takes them over (the Python objects are emptied)."""
+        G = len(shards)
+        arr = (C.c_void_p * G)(*[x._h.value if isinstance(x._h, C.c_void_p) else x._h for x in shards])
+        h = C.c_void_p()
+        check(lib().hcg_shard_group_adopt(G, arr, C.byref(h)))
+        for x in shards:
+            x._h = None
+        return cls(h, shards[0].scheme.d_full)
+
+    @classmethod
+    def join(cls, local: MulticurvesIndex, rank: int, world: int, pg=None) -> "ShardGroup":
+        """One process per GPU (collective): rank 0 makes the NCCL id, the
+        process group carries it to every rank, each joins with its shard."""
+        import torch
+        import torch.distributed as dist
+        nid = HcgNcclId()
+        if rank == 0:
+            check(lib().hcg_nccl_unique_id(C.byref(nid)))
+        backend = dist.get_backend(pg)
+        dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
+        t = torch.tensor(list(bytes(nid.internal)), dtype=torch.uint8, device=dev)
+        dist.broadcast(t, 0, group=pg)
+        C.memmove(C.addressof(nid), bytes(t.cpu().tolist()), 128)
+        h = C.c_void_p()
+        check(lib().hcg_shard_group_join(C.byref(nid), rank, world, local._h, C.byref(h)))
+        return cls(h, local.scheme.d_full, keep=[local])
+
+    def shards(self) -> int:
+        return int(lib().hcg_shard_group_shards(self._h))
+
+    def search(self, queries, k: int, shard_depth: int, out=None, stream=None):
+        """Global top-k (ids u64, sqdist u32, len u32) of a query batch."""
+        q = _u8_2d(queries, self.d_full)
+        nq = q.shape[0]
+        if out is None:
+            ids = _empty_like_kind(q, (nq, k), np.uint64)
+            sq = _empty_like_kind(q, (nq, k), np.uint32)
+            ln = _empty_like_kind(q, (nq,), np.uint32)
+        else:
+            ids, sq, ln = out
+        check(lib().hcg_shard_group_search(self._h, _ptr(q), nq, k, shard_depth, _ptr(ids), _ptr(sq), _ptr(ln),
+                                           _stream(stream, q)))
+        return ids, sq, ln
+
+    def close(self) -> None:
+        if self._h:
+            lib().hcg_shard_group_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class ShardedIndex:
     """One rank's share of a G-way sharded Multicurves index."""
 
@@ -60,6 +150,8 @@ class ShardedIndex:
         self.world = world
         self.group = group
         self._bufs = {}
+        # the search path: libhcg's shard group (NCCL inside the library)
+        self.shard_group = ShardGroup.join(local, rank, world, group) if world > 1 else None
 
     @classmethod
     def from_generator(cls, n_total: int, scheme: ProjectionScheme, view: View, rank: int, world: int,
@@ -90,11 +182,16 @@ class ShardedIndex:
         queries: [nq, d] uint8 CUDA tensor (the broadcast batch, same on every rank).
         Returns (ids u64, sqdist u32, len u32) CUDA tensors, identical on all ranks.
         """
+        if self.world == 1:
+            return self.local.search_batch(queries, k, shard_depth, out=out)
+        return self.shard_group.search(queries, k, shard_depth, out=out)
+
+    def search_torch(self, queries, k: int, shard_depth: int, out=None):
+        """The same aggregate through torch.distributed (packed search, all-gather
+        of the packed lists, K4): the pre-shard-group path, kept to cross-check."""
         import torch
         dev = queries.device
         nq = int(queries.shape[0])
-        if self.world == 1:
-            return self.local.search_batch(queries, k, shard_depth, out=out)
         packed = self._buf("packed", (nq, k), torch.uint64, dev)
         self.local.search_packed(queries, k, shard_depth, out=packed)
         gathered = self._buf("gathered", (self.world, nq, k), torch.uint64, dev)

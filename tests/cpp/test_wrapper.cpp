@@ -84,7 +84,7 @@ int main() {
     orc_free(oi);
 
     // Float descriptors through the default view (HCG_F32): arbitrary signed
-    // floats, ids exact, distances within 1e-12 relative of the oracle.
+    // floats, ids and distances bit-identical to the oracle.
     {
         std::srand(7);
         auto rnd = [] { return (float(std::rand()) / float(RAND_MAX) - 0.5f) * 200.0f; };
@@ -104,9 +104,7 @@ int main() {
             const hcb::NeighborList nl = fidx.search(qv, {k, depth});
             if (nl.size() != ol[q]) ++bad;
             for (size_t i = 0; i < nl.size() && i < ol[q]; ++i)
-                if (nl[i].id != oids[q * k + i] ||
-                    std::abs(nl[i].distance - od[q * k + i]) > 1e-12 * od[q * k + i])
-                    ++bad;
+                if (nl[i].id != oids[q * k + i] || nl[i].distance != od[q * k + i]) ++bad;
         }
         try {  // non-finite query component: invalid_argument (curve.cpp:167)
             Vec qv{0, std::vector<float>(d, 1.0f)};

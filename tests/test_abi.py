@@ -163,3 +163,22 @@ def test_u8_view_must_be_exact(offset, scale, ok):
     else:
         assert rc == _lib.HCG_EINVAL
         assert b"u8 view" in H.lib().hcg_last_error()
+
+
+def test_shard_group_validation_without_a_device():
+    """hcg_shard_group_*: argument checks come before NCCL or the device."""
+    L = H.lib()
+    h = C.c_void_p()
+    assert L.hcg_shard_group_adopt(0, None, C.byref(h)) == _lib.HCG_EINVAL
+    s = _scheme()
+    assert L.hcg_shard_group_build(C.byref(s), None, 10, 2, None, C.byref(h)) == _lib.HCG_EINVAL
+    devs = (C.c_int * 2)(0, 1)
+    s32 = _scheme()
+    s32.dtype = _lib.HCG_F32
+    assert L.hcg_shard_group_build(C.byref(s32), None, 0, 2, devs, C.byref(h)) == _lib.HCG_EINVAL
+    nid = _lib.HcgNcclId()
+    assert L.hcg_shard_group_join(C.byref(nid), 2, 2, None, C.byref(h)) == _lib.HCG_EINVAL
+    q = np.zeros((1, 128), np.uint8)
+    assert L.hcg_shard_group_search(None, q.ctypes.data, 1, 10, 10, None, None, None, None) == _lib.HCG_EINVAL
+    assert L.hcg_shard_group_shards(None) == 0
+    assert L.hcg_index_device(None) == -1

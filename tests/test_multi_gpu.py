@@ -1,5 +1,11 @@
-"""NCCL sharded search on >= 2 GPUs against the sharded CPU oracle (skipped on
-a 1-GPU box; the host-side protocol is covered on CPU by test_sharded_gloo)."""
+"""Sharded search on >= 2 GPUs (skipped on a 1-GPU box; the host-side
+protocol is covered on CPU by test_sharded_gloo):
+
+* one process per GPU (torchrun): libhcg's shard group joined per rank
+  (hcg_shard_group_join) against the sharded CPU oracle and the reference's
+  own TUs, and against the torch.distributed aggregate;
+* one process over all GPUs: hcb::ShardedIndex (C++, hcg_shard_group_build,
+  ncclCommInitAll) against the sharded oracle."""
 import os
 import subprocess
 import sys
@@ -19,13 +25,32 @@ def _ngpus():
         return 0
 
 
+needs2 = [pytest.mark.gpu, pytest.mark.skipif(not gpu_available() or _ngpus() < 2, reason="needs >= 2 GPUs")]
+
+
+@pytest.mark.parametrize("view", ["lifted", "raw"])
 @pytest.mark.gpu
 @pytest.mark.skipif(not gpu_available() or _ngpus() < 2, reason="needs >= 2 GPUs")
-def test_sharded_search_two_gpus():
+def test_sharded_search_per_rank_processes(view):
     g = min(_ngpus(), 4)
     out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={g}",
                           "--master-addr", "127.0.0.1", "--master-port", "29533",
-                          os.path.join(ROOT, "tools", "sharded_check.py")],
-                         capture_output=True, text=True, timeout=600, cwd=ROOT)
+                          os.path.join(ROOT, "tools", "sharded_check.py"), "--view", view],
+                         capture_output=True, text=True, timeout=900, cwd=ROOT)
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
     assert "sharded ok" in out.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not gpu_available() or _ngpus() < 2, reason="needs >= 2 GPUs")
+def test_cpp_shard_group_single_process():
+    binp = os.path.join(ROOT, "tests", "cpp", "test_shard_group.bin")
+    subprocess.run(["g++", "-std=c++20", "-O2", "-I", os.path.join(ROOT, "include"), "-I", "/usr/local/cuda/include",
+                    os.path.join(ROOT, "tests", "cpp", "test_shard_group.cpp"),
+                    "-L", os.path.join(ROOT, "paper_1209_0410_b200"), "-lhcg", "-L", os.path.join(ROOT, "oracle"),
+                    "-loracle", "-L", "/usr/local/cuda/lib64", "-lcudart",
+                    f"-Wl,-rpath,{os.path.join(ROOT, 'paper_1209_0410_b200')}:{os.path.join(ROOT, 'oracle')}",
+                    "-o", binp], check=True)
+    out = subprocess.run([binp], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
+    assert "shard group ok" in out.stdout
