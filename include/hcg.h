@@ -33,6 +33,10 @@
  *   hcg_write_vectors
  *   hcg_gen_rows /     the counter-based synthetic SIFT-like generator of
  *   hcg_gen_queries    SURVEY.md §8(d) (bench/test data; bit-identical to the oracle)
+ *   hcg_shard_group_*  hypershard module: partition / broadcast / IHLS / aggregate
+ *                       over G GPUs with NCCL
+ *   hcg_server_*       dtahe module: Alg. 3's buffer dispatch (
+ *                      SPEC.md:421-510) as a GPU batch-size controller
  *
  * Data model.  Descriptors are byte vectors (bvecs).  The reference sees each
  * byte b through a "view" v(b) (raw: float(b); lifted: 1 + b/256).  The
@@ -80,8 +84,9 @@ typedef enum hcg_curve_kind { HCG_ZORDER = 0, HCG_HILBERT = 1 } hcg_curve_kind;
  * scheme's view (cell_lut, dist_scale), distances exact integers.  HCG_F32:
  * the reference's float components as-is (fvecs): quantized on the device by
  * float_to_ordinal >> (32 - m) (curve.cpp:166-174), squared distances
- * accumulated in double (vecio.cpp:87-95; same terms, tree order: within
- * 1e-15 relative of the reference), searched with hcg_search_f32. */
+ * accumulated in double exactly as vecio.cpp:87-95 does (the same terms,
+ * summed sequentially in index order: the same double, bit for bit), searched
+ * with hcg_search_f32. */
 typedef enum hcg_dtype { HCG_U8 = 0, HCG_F32 = 1 } hcg_dtype;
 
 #define HCG_MAX_KEY_BITS 1024  /* HC_MAX_KEY_BITS, keys.hpp:15-23 */
@@ -281,6 +286,51 @@ uint32_t hcg_shard_group_shards(const hcg_shard_group* group);
 hcg_status hcg_shard_group_search(hcg_shard_group* group, const uint8_t* queries, uint32_t nq, uint32_t k,
                                   uint32_t shard_depth, uint64_t* out_ids, uint32_t* out_sqdist, uint32_t* out_len,
                                   void* stream);
+
+/* CUDA device of the group's first local shard (where results land) and the
+ * descriptor length. */
+int hcg_shard_group_device(const hcg_shard_group* group);
+uint32_t hcg_shard_group_dims(const hcg_shard_group* group);
+
+/* ---- GPU batch-size controller: DTAHE (Alg. 3, PAPER.md:1177-1191;
+ * SPEC.md:421-510) with the CPU branch removed (CC = 0) ----
+ * With a slot free (at most `slots` batches in flight: 2 = the double buffer,
+ * SPEC.md:436), the server launches min(waiting, max_batch) queries when the
+ * device is idle ("GPU idle"), when >= min_batch queries wait ("buffer
+ * full"), or when the oldest waiting query has waited max_wait_s; otherwise
+ * it keeps buffering.  FIFO, every query answered exactly once.
+ * A batch is H2D (host queries -> device) -> search (one index, or a shard
+ * group) -> D2H (results -> host), with uploads and downloads overlapping the
+ * neighbouring batches' searches; a query's response time runs from its
+ * arrival to its results being in host memory. */
+typedef struct hcg_server_policy {
+    uint32_t max_batch;  /* buffer capacity B                      */
+    uint32_t min_batch;  /* launch when this many queries wait      */
+    double max_wait_s;   /* launch when the oldest waited this long */
+    uint32_t slots;      /* batches in flight (1..8)                */
+} hcg_server_policy;
+typedef struct hcg_server hcg_server;
+
+/* Serve exactly one of `index` (u8) / `group` with fixed k and probe depth
+ * (per-shard depth for a group).  policy NULL: {8192, 1, 0, 2}. */
+hcg_status hcg_server_create(const hcg_index* index, hcg_shard_group* group, uint32_t k, uint32_t depth,
+                             const hcg_server_policy* policy, hcg_server** out);
+hcg_status hcg_server_free(hcg_server* server);
+/* Open-loop replay: query i (row i of `queries`, host memory) arrives
+ * arrival_s[i] seconds after the start (non-decreasing).  Results (host,
+ * nq x k, hcg_search's layout) and latency_s[i] = completion - arrival.
+ * batch_sizes (optional, capacity nq) / n_batches: the launched batches. */
+hcg_status hcg_server_replay(hcg_server* server, const uint8_t* queries, uint32_t nq, const double* arrival_s,
+                             uint64_t* out_ids, uint32_t* out_sqdist, uint32_t* out_len, double* latency_s,
+                             uint32_t* batch_sizes, uint32_t* n_batches);
+/* Online serving: start a dispatcher thread with a pinned ring of `capacity`
+ * queries; submit copies queries in and returns a ticket; wait blocks until
+ * the ticket's queries are answered and copies their results (and response
+ * times) out.  Thread-safe. */
+hcg_status hcg_server_start(hcg_server* server, uint64_t capacity);
+hcg_status hcg_server_submit(hcg_server* server, const uint8_t* queries, uint32_t nq, uint64_t* ticket);
+hcg_status hcg_server_wait(hcg_server* server, uint64_t ticket, uint64_t* out_ids, uint32_t* out_sqdist,
+                           uint32_t* out_len, double* latency_s);
 
 /* CUDA device of an index, and its id map (id of slot s = base + s * stride). */
 int hcg_index_device(const hcg_index* index);

@@ -19,7 +19,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
                      "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]
 CU = ["build.cu", "search.cu", "brute_tc.cu", "datagen.cu", "api.cu", "shard.cu"]
-CPP = ["planner.cpp", "io.cpp"]
+CPP = ["planner.cpp", "io.cpp", "serve.cpp"]
 HEADERS = ["hcg_internal.cuh", "hcg_host.hpp"]
 
 
@@ -57,6 +57,8 @@ def build(verbose: bool = False, ptxas_info: bool = False) -> str:
                 flags += ["-Xptxas", "-v"]
             if src.endswith(".cpp"):
                 flags = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include")]
+                if src == "serve.cpp":  # host code on the CUDA runtime
+                    flags += ["-x", "cu"] + ARCH
             jobs.append([_nvcc()] + flags + ["-c", s, "-o", o])
 
     def run(cmd):

@@ -40,6 +40,8 @@ EXPORTS = [
     "hcg_read_vectors", "hcg_write_vectors", "hcg_free_buffer",
     "hcg_nccl_unique_id", "hcg_shard_group_build", "hcg_shard_group_adopt", "hcg_shard_group_join",
     "hcg_shard_group_free", "hcg_shard_group_shards", "hcg_shard_group_search", "hcg_index_device", "hcg_index_ids",
+    "hcg_shard_group_device", "hcg_shard_group_dims", "hcg_server_create", "hcg_server_free", "hcg_server_replay",
+    "hcg_server_start", "hcg_server_submit", "hcg_server_wait",
 ]
 
 
@@ -60,6 +62,11 @@ class HcgScheme(C.Structure):
 
 class HcgNcclId(C.Structure):
     _fields_ = [("internal", C.c_uint8 * 128)]
+
+
+class HcgServerPolicy(C.Structure):
+    _fields_ = [("max_batch", C.c_uint32), ("min_batch", C.c_uint32), ("max_wait_s", C.c_double),
+                ("slots", C.c_uint32)]
 
 
 class HcgError(RuntimeError):
@@ -147,13 +154,24 @@ def lib() -> C.CDLL:
     L.hcg_index_device.restype = C.c_int
     L.hcg_index_device.argtypes = [vp]
     L.hcg_index_ids.argtypes = [vp, P(u64), P(u64)]
+    L.hcg_shard_group_device.restype = C.c_int
+    L.hcg_shard_group_device.argtypes = [vp]
+    L.hcg_shard_group_dims.restype = u32
+    L.hcg_shard_group_dims.argtypes = [vp]
+    L.hcg_server_create.argtypes = [vp, vp, u32, u32, P(HcgServerPolicy), P(vp)]
+    L.hcg_server_free.argtypes = [vp]
+    L.hcg_server_replay.argtypes = [vp, vp, u32, vp, vp, vp, vp, vp, vp, P(u32)]
+    L.hcg_server_start.argtypes = [vp, u64]
+    L.hcg_server_submit.argtypes = [vp, vp, u32, P(u64)]
+    L.hcg_server_wait.argtypes = [vp, u64, vp, vp, vp, vp]
     for name in ("hcg_make_lut", "hcg_default_assignment", "hcg_build", "hcg_free", "hcg_search",
                  "hcg_search_timed", "hcg_search_packed", "hcg_merge_packed", "hcg_keys", "hcg_sorted", "hcg_windows",
                  "hcg_candidates", "hcg_brute_force", "hcg_search_f32", "hcg_brute_force_f32", "hcg_sorted_range",
                  "hcg_describe", "hcg_gen_rows", "hcg_gen_queries", "hcg_insert",
                  "hcg_save", "hcg_load", "hcg_read_vectors", "hcg_write_vectors", "hcg_nccl_unique_id",
                  "hcg_shard_group_build", "hcg_shard_group_adopt", "hcg_shard_group_join", "hcg_shard_group_free",
-                 "hcg_shard_group_search", "hcg_index_ids"):
+                 "hcg_shard_group_search", "hcg_index_ids", "hcg_server_create", "hcg_server_free",
+                 "hcg_server_replay", "hcg_server_start", "hcg_server_submit", "hcg_server_wait"):
         getattr(L, name).restype = C.c_int
     del u8
     _lib = L

@@ -1,5 +1,10 @@
-"""GPU batch-size controller: the reference's DTAHE scheduler (Alg. 3,
-PAPER.md:1177-1191) re-targeted at a GPU-only search path.
+"""Simulation model of the GPU batch-size controller: the reference's DTAHE
+scheduler (Alg. 3) re-targeted at a
+GPU-only search path.  The product controller is C++ (libhcg hcg_server_*,
+csrc/serve.cpp, Python handle server.Server); this module states the same
+dispatch rule over an abstract backend so that its properties are tested on
+CPU against a simulated device (SPEC.md's `simulate` operation: virtual clock,
+deterministic), and provides the Poisson workload generator.
 
 DTAHE routes each arriving query either to a CPU core (lines 3-4) or into the
 current GPU buffer, and queues the buffer on the device when the device is
@@ -20,8 +25,7 @@ Batch size therefore follows the load: ~1 query per batch when lightly loaded
 contiguous range of the arrival sequence.
 
 The policy is independent of time and device: `run()` takes a `clock` and a
-`backend` (launch / poll), so the same code drives the B200 (CudaBackend:
-CUDA events, two streams) and the CPU tests (a simulated device).
+`backend` (launch / poll).
 """
 from __future__ import annotations
 
@@ -142,143 +146,3 @@ class _WallClock:
 
     def __call__(self):
         return time.perf_counter() - self.t0
-
-
-class CudaBackend:
-    """Dispatch batches of a device-resident query tensor to a search callable
-    on `slots` CUDA streams; completion times come from CUDA events relative to
-    a start event, on the same clock as the controller (seconds since start)."""
-
-    def __init__(self, search_fn, queries, k: int, slots: int = 2, max_batch: int = 8192):
-        import torch
-        self.torch = torch
-        self.search_fn = search_fn      # search_fn(queries_slice, out, stream)
-        self.queries = queries
-        dev = queries.device
-        # One stream for all slots: a slot bounds the batches outstanding, the
-        # batches themselves run back to back (measured: two streams whose
-        # kernels overlap lose ~10 % to interference).
-        stream = torch.cuda.Stream(device=dev)
-        self.streams = [stream] * slots
-        self.outs = [(torch.empty((max_batch, k), dtype=torch.uint64, device=dev),
-                      torch.empty((max_batch, k), dtype=torch.uint32, device=dev),
-                      torch.empty((max_batch,), dtype=torch.uint32, device=dev)) for _ in range(slots)]
-        self.clock = None
-        self.start = None
-
-    def begin(self):
-        """Synchronise and pin t=0 of both clocks; returns the host clock."""
-        torch = self.torch
-        torch.cuda.synchronize()
-        self.start = torch.cuda.Event(enable_timing=True)
-        self.start.record(self.streams[0])
-        self.start.synchronize()
-        self.clock = _WallClock()
-        return self.clock
-
-    def launch(self, first: int, count: int, slot: int):
-        torch = self.torch
-        st = self.streams[slot]
-        out = tuple(o[:count] for o in self.outs[slot])
-        with torch.cuda.stream(st):
-            self.search_fn(self.queries[first:first + count], out, st)
-            ev = torch.cuda.Event(enable_timing=True)
-            ev.record(st)
-        return ev
-
-    def poll(self, ev):
-        if not ev.query():
-            return None
-        return self.start.elapsed_time(ev) * 1e-3
-
-
-def spin_idle(clock):
-    def idle(t_next):
-        # short spin: batches finish in ~0.1-10 ms
-        if t_next == np.inf:
-            time.sleep(20e-6)
-            return
-        d = t_next - clock()
-        if d > 200e-6:
-            time.sleep(min(d, 1e-3) - 100e-6)
-    return idle
-
-
-class ShardedBackend:
-    """Multi-GPU serving (configs[4]): rank 0 runs the controller; every
-    dispatch sends (first, count) to the other ranks over a host-side (gloo)
-    group, and all ranks enqueue the sharded search of that batch, whose NCCL
-    all-gather keeps the GPUs in lockstep; rank 0 observes completion.  The
-    command channel never waits on a GPU, so with `slots` = 2 every rank
-    enqueues batch b+1 while batch b runs (double buffering, SPEC.md:436);
-    consecutive batches' collectives are issued in the same order on every
-    rank, which keeps them matched."""
-
-    STOP = -1
-
-    def __init__(self, search_fn, queries, k: int, max_batch: int = 8192, slots: int = 2, cmd_group=None):
-        import torch
-        import torch.distributed as dist
-        self.torch = torch
-        self.search_fn = search_fn  # search_fn(queries_slice, out)
-        self.queries = queries
-        dev = queries.device
-        self.group = cmd_group if cmd_group is not None else dist.new_group(backend="gloo")
-        self.cmd = torch.zeros(2, dtype=torch.int64)  # host tensor: gloo
-        self.outs = [(torch.empty((max_batch, k), dtype=torch.uint64, device=dev),
-                      torch.empty((max_batch, k), dtype=torch.uint32, device=dev),
-                      torch.empty((max_batch,), dtype=torch.uint32, device=dev)) for _ in range(slots)]
-        self.start = None
-        self.clock = None
-
-    def _run_batch(self, first: int, count: int, slot: int):
-        out = tuple(o[:count] for o in self.outs[slot])
-        self.search_fn(self.queries[first:first + count], out)
-
-    def begin(self):
-        torch = self.torch
-        torch.cuda.synchronize()
-        self.start = torch.cuda.Event(enable_timing=True)
-        self.start.record()
-        self.start.synchronize()
-        self.clock = _WallClock()
-        return self.clock
-
-    def _send(self, first: int, count: int, slot: int):
-        import torch.distributed as dist
-        self.cmd[0], self.cmd[1] = first, (count << 8) | slot
-        dist.broadcast(self.cmd, 0, group=self.group)
-
-    def launch(self, first: int, count: int, slot: int):
-        self._send(first, count, slot)
-        self._run_batch(first, count, slot)
-        ev = self.torch.cuda.Event(enable_timing=True)
-        ev.record()
-        return ev
-
-    def poll(self, ev):
-        if not ev.query():
-            return None
-        return self.start.elapsed_time(ev) * 1e-3
-
-    def stop(self):
-        self._send(self.STOP, 0, 0)
-
-    def follow(self):
-        """Non-zero ranks: run every broadcast batch until the stop command."""
-        import torch.distributed as dist
-        gc_on = gc.isenabled()
-        gc.disable()
-        try:
-            self._follow(dist)
-        finally:
-            if gc_on:
-                gc.enable()
-
-    def _follow(self, dist):
-        while True:
-            dist.broadcast(self.cmd, 0, group=self.group)
-            first, word = int(self.cmd[0]), int(self.cmd[1])
-            if first == self.STOP:
-                break
-            self._run_batch(first, word >> 8, word & 0xFF)

@@ -25,7 +25,7 @@ import paper_1209_0410_b200 as H  # noqa: E402
 from paper_1209_0410_b200.sharded import ShardedIndex  # noqa: E402
 
 p = argparse.ArgumentParser()
-p.add_argument("--n", type=int, default=20000)
+p.add_argument("--rows", type=int, default=20000)
 p.add_argument("--queries", type=int, default=64)
 p.add_argument("--view", choices=["lifted", "raw"], default="lifted")
 p.add_argument("--depths", default="")
@@ -35,7 +35,7 @@ a = p.parse_args()
 rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
 torch.cuda.set_device(local)
 dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-n, nq, k = a.n, a.queries, a.k
+n, nq, k = a.rows, a.queries, a.k
 view, m = (H.LIFTED, 16) if a.view == "lifted" else (H.RAW, 8)
 scheme = H.default_scheme(128, 8, m)
 t0 = time.time()
