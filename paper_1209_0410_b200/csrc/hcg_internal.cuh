@@ -338,10 +338,60 @@ struct WarpTopK {
         }
     }
 
+    // Drop values equal to their predecessor from the sorted list (after a
+    // merge, copies of one value are adjacent) and close the gaps: the kept
+    // values move down through the warp's shared scratch `wsm` (32 * R
+    // slots), kNone fills the tail.
+    __device__ __forceinline__ void dedup_sorted(int lane, uint64_t* wsm) {
+        const uint64_t prev_last = __shfl_up_sync(kFull, a[R - 1], 1);
+        uint32_t dmask = 0;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const uint64_t p = r == 0 ? prev_last : a[r - 1];
+            if (a[r] != kNone && (r > 0 || lane > 0) && a[r] == p) dmask |= 1u << r;
+        }
+        if (!__any_sync(kFull, dmask != 0)) return;
+        const uint32_t cnt = __popc(dmask);
+        uint32_t incl = cnt;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const uint32_t t = __shfl_up_sync(kFull, incl, off);
+            if (lane >= off) incl += t;
+        }
+        const uint32_t total = __shfl_sync(kFull, incl, 31);
+        uint32_t removed = incl - cnt;
+        constexpr uint32_t N = 32 * R;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const uint32_t idx = uint32_t(lane) * R + r;
+            if ((dmask >> r) & 1u) ++removed;
+            else wsm[idx - removed] = a[r];
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const uint32_t idx = uint32_t(lane) * R + r;
+            if (idx >= N - total) wsm[idx] = kNone;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int r = 0; r < R; ++r) a[r] = wsm[uint32_t(lane) * R + r];
+        __syncwarp();
+    }
+
     // offer() for candidate streams that may repeat a value (the same row
     // reached through two curves): a value already held is not inserted again.
-    __device__ __forceinline__ void offer_unique(uint64_t cand, int lane) {
+    // Many passing offers (R >= 2, wsm given) are sorted, merged and then
+    // deduplicated in one go; a merge can push out up to 32 values that later
+    // turn out to be repeats, so the list keeps >= 32 * (R - 1) distinct
+    // values: k <= 32 * (R - 1) stays exact (the caller picks R that way).
+    __device__ __forceinline__ void offer_unique(uint64_t cand, int lane, uint64_t* wsm = nullptr) {
         unsigned m = __ballot_sync(kFull, cand < thr);
+        if (R >= 2 && wsm && __popc(m) >= kTopkBatchMin) {
+            merge_sorted32<R>(a, warp_sort_asc(cand < thr ? cand : kNone, lane), lane);
+            dedup_sorted(lane, wsm);
+            update_thr();
+            return;
+        }
         while (m) {
             const int src = __ffs(m) - 1;
             const uint64_t x = __shfl_sync(kFull, cand, src);

@@ -487,7 +487,7 @@ __device__ __forceinline__ void gather_list(const RefineArgs& a, const uint32_t*
 // costs one dependent load (the slot) instead of three (pointer, begin, slot).
 template <int R, int CR, bool SMALLC>
 __device__ __forceinline__ void gather_windows(const RefineArgs& a, const uint32_t* begins_q, const uint4 (&qv)[CR],
-                                               int lane, WarpTopK<R>& tk) {
+                                               int lane, WarpTopK<R>& tk, uint64_t* wsm) {
     const int l8 = lane & 7, grp = lane >> 3;
     const uint32_t chunks = a.pitch >> 4;
     const uint32_t take = a.take, n = a.C * take, C = a.C;
@@ -565,7 +565,7 @@ __device__ __forceinline__ void gather_windows(const RefineArgs& a, const uint32
             const bool pre = me != kEmpty && S <= uint32_t(tk.thr >> 32);
             if (__any_sync(kFull, pre) && pre) sl = __ldg(a.idtab + me);
         }
-        tk.offer_unique(me != kEmpty ? ((uint64_t(S) << 32) | sl) : kNone, lane);
+        tk.offer_unique(me != kEmpty ? ((uint64_t(S) << 32) | sl) : kNone, lane, wsm);
     }
 }
 
@@ -603,7 +603,10 @@ __global__ void __launch_bounds__(kRefineThreads, MINB) k_gather(RefineArgs a, c
 // K3c without the union: one warp per query over the raw windows.
 template <int R, int CR, int MINB, bool SMALLC, int NT = kRefineThreads>
 __global__ void __launch_bounds__(NT, MINB) k_gather_nu(RefineArgs a) {
+    // per-warp scratch of the batched dedup (R >= 2 only)
+    __shared__ uint64_t dsm[R >= 2 ? NT / 32 : 1][R >= 2 ? 32 * R : 1];
     const int lane = threadIdx.x & 31;
+    uint64_t* wsm = R >= 2 ? dsm[threadIdx.x >> 5] : nullptr;
     const uint32_t qstep = gridDim.x * (NT / 32);
     for (uint32_t q = (blockIdx.x * NT + threadIdx.x) >> 5; q < a.nq; q += qstep) {
         const uint32_t qq = a.qorder ? __ldg(a.qorder + q) : q;
@@ -611,7 +614,7 @@ __global__ void __launch_bounds__(NT, MINB) k_gather_nu(RefineArgs a) {
         load_query<CR>(a, qq, lane, qv);
         WarpTopK<R> tk;
         tk.init(int(a.k));
-        gather_windows<R, CR, SMALLC>(a, a.begins + uint64_t(qq) * a.C, qv, lane, tk);
+        gather_windows<R, CR, SMALLC>(a, a.begins + uint64_t(qq) * a.C, qv, lane, tk, wsm);
         uint32_t valid = 0;
 #pragma unroll
         for (int r = 0; r < R; ++r)
@@ -1241,13 +1244,34 @@ constexpr size_t kListBudget = size_t(2) << 30;
 // is sized from it; 2^27 entries keeps every table index in 32 bits).
 constexpr uint64_t kMaxWalk = uint64_t(1) << 27;
 
-// The union-less K3c (k_gather_nu) serves k <= 32, u8 rows in curve-0
+// The union-less K3c (k_gather_nu) serves k <= 128, u8 rows in curve-0
 // order and batches of >= 16K queries; everything else runs the separate
 // union (K3b) + K3c.  One predicate for the scratch query and the launch.
 template <int R>
 bool unionless_path(const RefineArgs& a) {
     static const bool off = getenv("HCG_NO_UNIONLESS") != nullptr;  // A/B: separate union for every k
-    return R == 1 && !off && a.mode != kOutCandidates && a.dtype == HCG_U8 && a.nq >= 16384 && a.idtab != nullptr;
+    return R <= 4 && a.k <= 128 && !off && a.mode != kOutCandidates && a.dtype == HCG_U8 && a.nq >= 16384 &&
+           a.idtab != nullptr;
+}
+
+// The union-less walk's list width: k <= 32 inserts one offer at a time
+// (R = 1); larger k merge batches of offers and dedup after the merge, which
+// needs 32 spare slots: k <= 32 * (R - 1).
+template <int CR, bool SMALLC>
+hcg_status launch_gather_nu(const RefineArgs& a, int device, int sms, cudaStream_t st) {
+    auto nk = a.k <= 32 ? k_gather_nu<1, CR, 3, SMALLC> : a.k <= 96 ? k_gather_nu<4, CR, 2, SMALLC>
+                                                                     : k_gather_nu<8, CR, 2, SMALLC>;
+    const int kb = a.k <= 32 ? 0 : a.k <= 96 ? 1 : 2;
+    static int per_sm_cache[64][3] = {};
+    int& per_sm = per_sm_cache[device & 63][kb];
+    if (per_sm == 0) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nk, kRefineThreads, 0);
+        per_sm = std::max(per_sm, 1);
+    }
+    const uint32_t blocks = std::min<uint32_t>((a.nq + 7) / 8, uint32_t(sms * per_sm));
+    count_launches(1);
+    nk<<<blocks, kRefineThreads, 0, st>>>(a);
+    return check_launch("k_gather_nu");
 }
 
 template <int R, int CR>
@@ -1322,27 +1346,14 @@ hcg_status refine_dispatch(const RefineArgs& a_in, void* scratch, size_t* scratc
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_per_sm, gk, kRefineThreads, 0);
         g_per_sm = std::max(g_per_sm, 1);
     }
-    if constexpr (R == 1) {
-        // k <= 32 and large batches: skip the union, walk the windows directly.
-        // 3 CTAs/SM (72 registers): 2 leaves DRAM latency uncovered, 4 forces
-        // 64 registers and spills the top-k (profiles/r01_nu_occupancy_ab.txt).
-        if (nu) {
-            RefineArgs a = a_in;
-            a.qorder = qorder;
-            auto nk = a.C <= 32 ? k_gather_nu<R, CR, 3, true> : k_gather_nu<R, CR, 3, false>;
-            static int per_sm_cache[64][2] = {};
-            int& per_sm = per_sm_cache[device & 63][a.C <= 32 ? 1 : 0];
-            if (per_sm == 0) {
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nk, kRefineThreads, 0);
-                per_sm = std::max(per_sm, 1);
-            }
-            const uint32_t blocks = std::min<uint32_t>((a.nq + 7) / 8, uint32_t(sms * per_sm));
-            if (a.ev_mid) cudaEventRecord(a.ev_mid, st);  // timed split: (batch order) | fused gather
-            count_launches(1);
-            nk<<<blocks, kRefineThreads, 0, st>>>(a);
-            HCG_RET_IF(check_launch("k_gather_nu"));
-            return HCG_OK;
-        }
+    if (nu) {
+        // large batches: skip the union, walk the windows directly.  k <= 32
+        // at 3 CTAs/SM (72 registers): 2 leaves DRAM latency uncovered, 4
+        // forces 64 registers and spills the top-k (profiles/r01_nu_occupancy_ab.txt).
+        RefineArgs a = a_in;
+        a.qorder = qorder;
+        if (a.ev_mid) cudaEventRecord(a.ev_mid, st);  // timed split: (batch order) | fused gather
+        return a.C <= 32 ? launch_gather_nu<CR, true>(a, device, sms, st) : launch_gather_nu<CR, false>(a, device, sms, st);
     }
     for (uint32_t q0 = 0; q0 < a_in.nq; q0 += chunk) {
         RefineArgs a = a_in;

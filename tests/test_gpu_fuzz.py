@@ -91,10 +91,11 @@ def test_random_configurations_f32(seed):
         assert d[q, :L].tobytes() == odist[q, :L].tobytes()
 
 
-@pytest.mark.parametrize("seed", range(10))
+@pytest.mark.parametrize("seed", range(16))
 def test_random_configurations_large_batch(seed):
-    """>= 16K queries with k <= 32: the union-less gather (k_gather_nu walks the
-    C windows and drops repeated candidates in the top-k) over random schemes,
+    """>= 16K queries with k <= 128: the union-less gather (k_gather_nu walks the
+    C windows and drops repeated candidates in the top-k; k > 32 merges
+    batches of offers and dedups after the merge) over random schemes,
     row widths, depths (windows past both ends included) and views."""
     rng = np.random.default_rng(9000 + seed)
     d_full = int(rng.choice([16, 24, 64, 100, 128]))
@@ -108,7 +109,7 @@ def test_random_configurations_large_batch(seed):
     n = int(rng.integers(1, 12_000))
     nq = int(rng.choice([16_384, 17_001]))
     depth = int(rng.choice([1, 3, 50, 350, 2000]))
-    k = int(rng.choice([1, 10, 32]))
+    k = int(rng.choice([1, 10, 32, 33, 64, 96, 100, 128]))
     rows = rng.integers(0, 256, (n, d_full), dtype=np.uint8)
     if n > 50:
         rows[n // 2:n // 2 + 20] = rows[0]  # ties and repeats across curves
