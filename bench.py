@@ -63,8 +63,10 @@ def parse():
     p.add_argument("--recall-sample", type=int, default=1000)
     p.add_argument("--cpu-sample", type=int, default=100_000,
                    help="queries of step 0 in our arm's CPU baseline + parity sample (~10 s on 16 cores)")
-    p.add_argument("--ref-sample", type=int, default=20_000,
-                   help="queries per step timed by the reference arm (--impl reference)")
+    p.add_argument("--ref-sample", type=int, default=100_000,
+                   help="queries per step timed by the reference arm (--impl reference); default = a whole step")
+    p.add_argument("--cert-sample", type=int, default=200,
+                   help="queries of step 0 certified against the reference semantics (oracle/certify.py)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--latency-batches", default="1,16,256,4096,65536")
     p.add_argument("--latency-reps", type=int, default=20)
@@ -171,6 +173,20 @@ def cpu_reference_qps(rows_u8, queries_u8, curves, m, kind, view, k, depth, thre
         best = dt if best is None else min(best, dt)
     del ri
     return queries_u8.shape[0] / best, best, res
+
+
+def workload_name(n_total: int, Q: int, k: int, C: int, D: int, world: int) -> str:
+    base = f"{n_total / 1e6:g}M x 128-d, {Q} queries/step, k={k}, {C} curves, probe depth {D}"
+    if n_total >= 100_000_000:
+        tag = ("configs[2]: 100M sharded id mod N over N GPUs (hcg_shard_group: per-shard search, NCCL all-gather, "
+               "K4 merge)" if world > 1 else "configs[2] at N=1: 100M on one B200 (same-workload anchor)")
+    elif n_total == 10_000_000 and world == 1:
+        tag = "configs[1]"
+    elif n_total == 1_000_000:
+        tag = "configs[0]"
+    else:
+        tag = "custom" if world == 1 else "sharded id mod N"
+    return f"{tag}: {base}"
 
 
 # ------------------------------------------------------------------- ours ----
@@ -345,9 +361,43 @@ def run_ours(a):
         lat[str(bs)] = {"p50_ms": round(ts[len(ts) // 2], 4), "p99_ms": round(ts[min(len(ts) - 1, int(0.99 * len(ts)))], 4),
                         "qps_at_p50": round(bs / (ts[len(ts) // 2] * 1e-3), 1)}
 
+    # Certificate parity on a query sample (oracle/certify.py; every config,
+    # every N): each rank recomputes its shard's top-k from the reference's
+    # semantics -- oracle keys of the regenerated rows around every window,
+    # lower bound, window rule, exact distances, (distance, id) order -- and
+    # rank 0 merges the shards' lists and compares them with the GPU result.
+    cert = None
+    if a.cert_sample > 0:
+        from oracle import certify as CE
+        from oracle import pyoracle as P
+        cs = min(a.cert_sample, Q)
+        qc = batches[0][:cs].contiguous()
+        gi, gs, gl = (x.cpu().numpy() for x in sidx.search(qc, k, shard_depth))
+        part = CE.certify_shard(sidx.local, qc.cpu().numpy(), shard_depth, k, 1 if a.view == "lifted" else 0, m,
+                                kind)
+        parts = [part]
+        if world > 1:
+            parts = [None] * world if rank == 0 else None
+            dist.gather_object(part, parts, dst=0)
+        if rank == 0:
+            oi, od, ol = P.merge_shard_lists([p_[:3] for p_ in parts], k)
+            rooted = np.sqrt(gs.astype(np.float64)) * view.scale
+            mism = sum(int(not (gl[q] == ol[q] and np.array_equal(gi[q, :ol[q]], oi[q, :ol[q]])
+                               and rooted[q, :ol[q]].tobytes() == od[q, :ol[q]].tobytes())) for q in range(cs))
+            failed = {}
+            for p_ in parts:
+                for key_, v in p_[3]["failed_checks"].items():
+                    failed[key_] = failed.get(key_, 0) + v
+            cert = {"sample_queries": cs, "shards": world, "rows_per_shard": [p_[3]["rows"] for p_ in parts],
+                    "failed_checks": failed, "mismatched_queries": mism,
+                    "identical": bool(mism == 0 and sum(failed.values()) == 0),
+                    "method": "oracle/certify.py: oracle keys of the regenerated rows at every window's sorted "
+                              "positions (order, lower bound, window rule), exact distances of the candidate union, "
+                              "(distance, id) top-k per shard, merged"}
+
     cpu = None
     parity = None
-    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+    if rank == 0 and world == 1 and n_total <= 20_000_000 and not a.no_cpu_baseline:
         threads = os.cpu_count() or 1
         S = min(a.cpu_sample, Q)
         rows_h = H.gen_rows(0, n_total, device=local).cpu().numpy()
@@ -385,9 +435,7 @@ def run_ours(a):
             "dtype": "u8",
             "data": DATA,
             "config": {
-                "workload": ("configs[1]: 10M x 128-d, 100K queries/step, k=10, 8 curves, fixed probe depth"
-                             if world == 1 else
-                             "configs[2]: 100M x 128-d sharded id mod N, k=10, NCCL allgather top-k merge"),
+                "workload": workload_name(n_total, Q, k, C, D, world),
                 "n_db": n_total, "queries_per_step": Q, "k": k, "curves": C, "probe_depth": D,
                 "shard_probe_depth": shard_depth, "curve": a.kind, "view": a.view, "bits_per_dim": m,
                 "recall_at_k": round(rec, 4), "recall_sample": rs,
@@ -422,6 +470,7 @@ def run_ours(a):
             },
             "cpu_baseline": cpu,
             "parity_vs_reference": parity,
+            "parity_certificate": cert,
             "e2e": {"value": round(e2e_value, 1), "unit": "queries/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": int(launches[0]),
@@ -466,7 +515,9 @@ def run_reference(a):
     ri = P.RefIndex(rows, C, m, kind, view)
     build_s = time.perf_counter() - t0
     S = min(a.ref_sample, a.queries)
-    steps_q = [P.gen_queries(b * a.queries, S, n_total, threads) for b in range(a.warmup + a.steps)]
+    # warm-up steps on a 10K-query slice (caches and threads only), timed steps on the whole S
+    steps_q = [P.gen_queries(b * a.queries, S if b >= a.warmup else min(S, 10_000), n_total, threads)
+               for b in range(a.warmup + a.steps)]
     for b in range(a.warmup):
         ri.search(steps_q[b], k, depth, threads)
     t0 = time.perf_counter()
@@ -489,8 +540,8 @@ def run_reference(a):
         "vs_baseline": None,
         "dtype": "u8",
         "data": DATA,
-        "config": {"workload": "configs[1]" if world == 1 else "configs[2]", "n_db": n_total,
-                   "queries_per_step_sample": S, "k": k, "curves": C, "probe_depth": D,
+        "config": {"workload": workload_name(n_total, a.queries, k, C, D, world), "n_db": n_total,
+                   "queries_per_step_sample": S, "same_config_as_gpu_arm": S == a.queries, "k": k, "curves": C, "probe_depth": D,
                    "shard_probe_depth": depth, "view": a.view, "bits_per_dim": m, "curve": a.kind,
                    "build_s": round(build_s, 2)},
         "cpu_baseline": {"value": round(value, 1), "unit": "queries/s", "cores": threads, "kind": kind_s,

@@ -501,6 +501,31 @@ void orc_gen_rows_strided(uint64_t first, uint64_t stride, uint64_t count, uint8
     });
 }
 
+// Rows of arbitrary generator ids (the certificate checks of tools/certify.py
+// regenerate exactly the rows a window touches).
+void orc_gen_rows_ids(const uint64_t* ids, uint64_t count, uint8_t* out, int threads) {
+    const GenTables& g = gen_tables();
+    const uint64_t chunk = 1024;
+    parallel_for((count + chunk - 1) / chunk, threads, [&](uint64_t b) {
+        const uint64_t e = std::min(count, (b + 1) * chunk);
+        for (uint64_t i = b * chunk; i < e; ++i) gen_row(g, ids[i], out + i * kD);
+    });
+}
+
+// Full keys (W words, LS word first) of n arbitrary float rows on curve c of
+// an index's scheme (curve.cpp:162-164 over multicurves.hpp:40's projection).
+int orc_keys_batch(void* h, const float* rows, uint64_t n, uint32_t c, uint64_t* keys_out) {
+    const Index& ix = *static_cast<Index*>(h);
+    const uint32_t w = ix.W[c];
+    for (uint64_t i = 0; i < n; ++i) {
+        uint64_t key[kMaxWords] = {};
+        const int rc = project_key(ix, rows + i * ix.d_full, c, key);
+        if (rc != ORC_OK) return rc;
+        std::memcpy(keys_out + i * w, key, 8 * w);
+    }
+    return ORC_OK;
+}
+
 void orc_gen_rows(uint64_t i0, uint64_t count, uint8_t* out, int threads) {
     orc_gen_rows_strided(i0, 1, count, out, threads);
 }

@@ -87,6 +87,8 @@ def orc() -> C.CDLL:
         L.orc_gen_rows.argtypes = [C.c_uint64, C.c_uint64, _u8p, C.c_int]
         L.orc_gen_rows_strided.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, _u8p, C.c_int]
         L.orc_gen_queries.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, _u8p, C.c_int]
+        L.orc_gen_rows_ids.argtypes = [_u64p, C.c_uint64, _u8p, C.c_int]
+        L.orc_keys_batch.argtypes = [C.c_void_p, _f32p, C.c_uint64, C.c_uint32, _u64p]
         _orc = L
     return _orc
 
@@ -98,6 +100,15 @@ def nthreads() -> int:
 def gen_rows(i0: int, count: int, threads: int | None = None, stride: int = 1) -> np.ndarray:
     out = np.empty((count, 128), np.uint8)
     orc().orc_gen_rows_strided(i0, stride, count, out, threads or nthreads())
+    return out
+
+
+def gen_rows_ids(ids, threads: int | None = None) -> np.ndarray:
+    """Generator rows of arbitrary global ids (SURVEY.md §8(d) is counter-based)."""
+    idx = np.ascontiguousarray(ids, np.uint64)
+    out = np.zeros((idx.shape[0], 128), np.uint8)
+    if idx.shape[0]:
+        orc().orc_gen_rows_ids(idx, idx.shape[0], out, threads or nthreads())
     return out
 
 
@@ -196,6 +207,16 @@ class Oracle:
         if rc:
             raise ValueError(f"query_key rc={rc}")
         return key
+
+    def keys(self, rows_f32: np.ndarray, c: int) -> np.ndarray:
+        """Full keys [n, words] (LS word first) of arbitrary rows on curve c."""
+        rows = np.ascontiguousarray(rows_f32, np.float32)
+        out = np.zeros((rows.shape[0], self.words(c)), np.uint64)
+        if rows.shape[0]:
+            rc = orc().orc_keys_batch(self.h, rows, rows.shape[0], c, out)
+            if rc:
+                raise ValueError(f"keys rc={rc}")
+        return out
 
     def windows(self, qs_f32: np.ndarray, depth: int):
         qs = np.ascontiguousarray(qs_f32, np.float32)

@@ -1257,10 +1257,17 @@ bool unionless_path(const RefineArgs& a) {
 // The union-less walk's list width: k <= 32 inserts one offer at a time
 // (R = 1); larger k merge batches of offers and dedup after the merge, which
 // needs 32 spare slots: k <= 32 * (R - 1).
+#ifndef HCG_NU_MINB4
+#define HCG_NU_MINB4 2
+#endif
+#ifndef HCG_NU_MINB8
+#define HCG_NU_MINB8 2
+#endif
 template <int CR, bool SMALLC>
 hcg_status launch_gather_nu(const RefineArgs& a, int device, int sms, cudaStream_t st) {
-    auto nk = a.k <= 32 ? k_gather_nu<1, CR, 3, SMALLC> : a.k <= 96 ? k_gather_nu<4, CR, 2, SMALLC>
-                                                                     : k_gather_nu<8, CR, 2, SMALLC>;
+    auto nk = a.k <= 32 ? k_gather_nu<1, CR, 3, SMALLC>
+              : a.k <= 96 ? k_gather_nu<4, CR, HCG_NU_MINB4, SMALLC>
+                          : k_gather_nu<8, CR, HCG_NU_MINB8, SMALLC>;
     const int kb = a.k <= 32 ? 0 : a.k <= 96 ? 1 : 2;
     static int per_sm_cache[64][3] = {};
     int& per_sm = per_sm_cache[device & 63][kb];

@@ -365,6 +365,13 @@ class MulticurvesIndex:
                                 _stream(None, q)))
         return r, b, e
 
+    def sorted_ids(self, c: int, begin: int, count: int) -> np.ndarray:
+        """Ids at positions [begin, begin + count) of sorted subindex c (SubIndex::entries() slice)."""
+        out = np.zeros(max(count, 1), np.uint64)
+        if count:
+            check(lib().hcg_sorted_range(self._h, c, begin, count, _ptr(out), None))
+        return out[:count]
+
     def retrieve_candidates(self, query, c: int, depth: int) -> np.ndarray:
         """Ids of the window on curve c (multicurves.hpp:83-85), in key order."""
         _, b, e = self.windows(query, depth)
