@@ -308,7 +308,7 @@ def run_ours(a):
     # Which K3c runs (the library's dispatch, search.cu refine_dispatch): for
     # k <= 128 and batches >= 16K on a reordered index the union is skipped and
     # k_gather_nu walks the windows; otherwise k_union_reg + k_gather.
-    unionless = k <= 128 and Q >= 16384 and os.environ.get("HCG_NO_UNIONLESS") is None
+    unionless = sidx.local.unionless(Q, k, shard_depth)
     if unionless:
         # k_gather_nu reads the C windows of ids, each unique row once (repeats
         # reached through a second curve are re-reads, not algorithmic), the

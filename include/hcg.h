@@ -332,6 +332,12 @@ hcg_status hcg_server_submit(hcg_server* server, const uint8_t* queries, uint32_
 hcg_status hcg_server_wait(hcg_server* server, uint64_t ticket, uint64_t* out_ids, uint32_t* out_sqdist,
                            uint32_t* out_len, double* latency_s);
 
+/* 1 when a search of nq queries at (k, depth) runs the union-less refine
+ * kernel (k_gather_nu: window walk + gather + top-k with repeats dropped),
+ * 0 when it runs the separate candidate union + gather (instrumentation for
+ * the byte model of bench.py). */
+uint32_t hcg_refine_unionless(const hcg_index* index, uint32_t nq, uint32_t k, uint32_t depth);
+
 /* CUDA device of an index, and its id map (id of slot s = base + s * stride). */
 int hcg_index_device(const hcg_index* index);
 hcg_status hcg_index_ids(const hcg_index* index, uint64_t* id_base, uint64_t* id_stride);

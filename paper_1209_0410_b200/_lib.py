@@ -41,7 +41,7 @@ EXPORTS = [
     "hcg_nccl_unique_id", "hcg_shard_group_build", "hcg_shard_group_adopt", "hcg_shard_group_join",
     "hcg_shard_group_free", "hcg_shard_group_shards", "hcg_shard_group_search", "hcg_index_device", "hcg_index_ids",
     "hcg_shard_group_device", "hcg_shard_group_dims", "hcg_server_create", "hcg_server_free", "hcg_server_replay",
-    "hcg_server_start", "hcg_server_submit", "hcg_server_wait",
+    "hcg_server_start", "hcg_server_submit", "hcg_server_wait", "hcg_refine_unionless",
 ]
 
 
@@ -154,6 +154,8 @@ def lib() -> C.CDLL:
     L.hcg_index_device.restype = C.c_int
     L.hcg_index_device.argtypes = [vp]
     L.hcg_index_ids.argtypes = [vp, P(u64), P(u64)]
+    L.hcg_refine_unionless.restype = u32
+    L.hcg_refine_unionless.argtypes = [vp, u32, u32, u32]
     L.hcg_shard_group_device.restype = C.c_int
     L.hcg_shard_group_device.argtypes = [vp]
     L.hcg_shard_group_dims.restype = u32

@@ -506,7 +506,7 @@ hcg_status insert_curve_into(const hcg_index* ix, uint32_t c, const uint8_t* row
 // physical rows (their (key, id) order is unchanged), and the search reads
 // idtab only for candidates that can enter a top-k (tie order by id).
 hcg_status reorder_rows(hcg_index* ix, cudaStream_t st) {
-    static const bool off = getenv("HCG_NO_REORDER") != nullptr;
+    static const bool off = knob("HCG_NO_REORDER") != nullptr;
     const uint64_t n = ix->n;
     if (off || n < 2 || ix->idtab) return HCG_OK;
     uint8_t* nr = nullptr;
@@ -547,7 +547,7 @@ hcg_status publish_tables(hcg_index* ix, cudaStream_t st) {
         ix->sample_bytes[c] = 0;
         cv.samples = nullptr;
         cv.n_samples = 0;
-        static const uint32_t stride = getenv("HCG_SAMPLE_STRIDE") ? uint32_t(atoi(getenv("HCG_SAMPLE_STRIDE")))
+        static const uint32_t stride = knob("HCG_SAMPLE_STRIDE") ? uint32_t(atoi(knob("HCG_SAMPLE_STRIDE")))
                                                                    : kSampleStride;
         if (stride < 2 || ix->n < 4 * uint64_t(stride) || !ix->keys[c]) continue;
         const uint64_t ns = (ix->n + stride - 1) / stride;
@@ -661,8 +661,8 @@ hcg_status check_flag(const QueryFlag& f, cudaStream_t st) {
     return h ? set_error(HCG_ENONFINITE, "non-finite query component") : HCG_OK;
 }
 
-hcg_status locate(const hcg_index* ix, Scratch& sc, const uint8_t* dq, uint32_t nq, uint32_t depth,
-                  uint32_t* begins, uint64_t* ranks, const QueryFlag& flag) {
+LocateArgs locate_args(const hcg_index* ix, const uint8_t* dq, uint32_t nq, uint32_t depth, uint32_t* begins,
+                       uint64_t* ranks, const QueryFlag& flag) {
     LocateArgs a{};
     a.dtype = int(ix->dtype);
     a.bad = flag.dev;
@@ -679,7 +679,12 @@ hcg_status locate(const hcg_index* ix, Scratch& sc, const uint8_t* dq, uint32_t 
     a.depth = depth;
     a.out_begin = begins;
     a.out_rank = ranks;
-    return launch_locate(a, ix->dmax, ix->wsmax, sc.st);
+    return a;
+}
+
+hcg_status locate(const hcg_index* ix, Scratch& sc, const uint8_t* dq, uint32_t nq, uint32_t depth,
+                  uint32_t* begins, uint64_t* ranks, const QueryFlag& flag) {
+    return launch_locate(locate_args(ix, dq, nq, depth, begins, ranks, flag), ix->dmax, ix->wsmax, sc.st);
 }
 
 RefineArgs refine_args(const hcg_index* ix, const uint8_t* dq, uint32_t nq, uint32_t depth, uint32_t k,
@@ -700,7 +705,7 @@ RefineArgs refine_args(const hcg_index* ix, const uint8_t* dq, uint32_t nq, uint
     a.n_rows = ix->n;
     a.dtype = int(ix->dtype);
     a.idtab = ix->idtab;
-    static const bool no_list = getenv("HCG_NO_UNION_LIST") != nullptr;
+    static const bool no_list = knob("HCG_NO_UNION_LIST") != nullptr;
     a.union_list = !no_list;
     return a;
 }
@@ -835,6 +840,12 @@ uint64_t hcg_device_bytes(const hcg_index* ix) { return ix ? ix->bytes : 0; }
 uint64_t hcg_launch_count(void) { return hcg::g_launches.load(); }
 uint32_t hcg_index_dtype(const hcg_index* ix) { return ix ? ix->dtype : 0; }
 int hcg_index_device(const hcg_index* ix) { return ix ? ix->device : -1; }
+uint32_t hcg_refine_unionless(const hcg_index* ix, uint32_t nq, uint32_t k, uint32_t depth) {
+    if (!ix || k < 1 || k > HCG_MAX_K || depth < 1 || ix->n == 0) return 0;
+    RefineArgs a = refine_args(ix, nullptr, nq, depth, k, nullptr);
+    a.mode = kOutIds;
+    return refine_unionless(a) ? 1u : 0u;
+}
 hcg_status hcg_index_ids(const hcg_index* ix, uint64_t* id_base, uint64_t* id_stride) {
     HCG_TRY(check_index(ix));
     if (id_base) *id_base = ix->id_base;
@@ -1110,6 +1121,21 @@ static hcg_status search_impl(const hcg_index* ix, const uint8_t* queries, uint3
         const uint8_t* dq = nullptr;
         HCG_TRY(stage_rows(sc, queries, nq, ix->row_bytes, ix->pitch, &dq));
         HCG_TRY(make_flag(ix, sc, &flag));
+        // small batches: the whole search of a query in one CTA, one launch
+        {
+            RefineArgs a = refine_args(ix, dq, nq, depth, k, nullptr);
+            a.mode = packed ? kOutPacked : kOutIds;
+            a.out_packed = op.dev;
+            a.out_ids = oi.dev;
+            a.out_sqdist = os.dev;
+            a.out_len = ol.dev;
+            const LocateArgs la = locate_args(ix, dq, nq, depth, nullptr, nullptr, flag);
+            if (!ms_out && small_eligible(la, a, ix->dmax, ix->wsmax)) {
+                HCG_TRY(launch_search_small(la, a, ix->dmax, ix->wsmax, ix->device, st));
+                goto finish;
+            }
+        }
+        {
         uint32_t* begins = sc.alloc<uint32_t>(size_t(nq) * ix->C);
         if (!begins) return set_error(HCG_ENOMEM, "window buffer");
         cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -1147,7 +1173,9 @@ static hcg_status search_impl(const hcg_index* ix, const uint8_t* queries, uint3
             }
             for (auto& e : ev) cudaEventDestroy(e);
         }
+        }
     }
+finish:
     HCG_TRY(finish_out(sc, oi));
     HCG_TRY(finish_out(sc, os));
     HCG_TRY(finish_out(sc, o64));

@@ -423,7 +423,7 @@ hcg_status launch_tc(const BruteArgs& a, const TcPlan& p, const CUtensorMap& mq,
 }  // namespace
 
 bool brute_tc_eligible(const BruteArgs& a) {
-    static const bool off = getenv("HCG_BRUTE_CUDA_CORES") != nullptr;
+    static const bool off = knob("HCG_BRUTE_CUDA_CORES") != nullptr;
     return !off && a.dtype == HCG_U8 && a.pitch == uint32_t(kRowBytes) && a.k <= 32 && a.n > 0 && a.nq > 0 &&
            a.n < (uint64_t(1) << 31) &&
            encode_fn() != nullptr;

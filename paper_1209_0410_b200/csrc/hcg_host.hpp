@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
 #include <string>
 
 #include "../../include/hcg.h"
@@ -15,6 +16,19 @@
     } while (0)
 
 namespace hcg {
+
+// A/B switches of the measured alternatives (e.g.
+// HCG_NO_UNIONLESS).  Read only in a library built with -DHCG_TUNING_KNOBS
+// (tools/build_variant.py); the release library always runs the measured-best
+// paths and ignores the environment.
+inline const char* knob(const char* name) {
+#ifdef HCG_TUNING_KNOBS
+    return std::getenv(name);
+#else
+    (void)name;
+    return nullptr;
+#endif
+}
 
 struct CurveDev;
 
@@ -99,6 +113,12 @@ struct RefineArgs {
 // does not fit in shared memory); query with scratch == nullptr first.
 hcg_status launch_refine(const RefineArgs& a, void* scratch, size_t* scratch_bytes, int device,
                          cudaStream_t st);
+// Small batches: the whole search of a query in one CTA (k_search_small).
+bool small_eligible(const LocateArgs& la, const RefineArgs& a, int dmax, int wsmax);
+hcg_status launch_search_small(const LocateArgs& la, const RefineArgs& a, int dmax, int wsmax, int device,
+                               cudaStream_t st);
+// Whether a search of nq queries at k takes the union-less K3c (k_gather_nu).
+bool refine_unionless(const RefineArgs& a);
 
 hcg_status launch_merge(const uint64_t* packed, uint32_t parts, uint32_t nq, uint32_t k, uint64_t* out_ids,
                         uint32_t* out_sqdist, uint32_t* out_len, cudaStream_t st);

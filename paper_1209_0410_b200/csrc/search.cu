@@ -53,16 +53,14 @@ __device__ __forceinline__ int suffix_cmp(const uint64_t* e, const uint64_t (&qs
 // COOP: one WARP per (query, curve) and a 32-ary lower_bound (each round the
 // lanes probe 32 splitters and a ballot narrows the range 33x: ~5 dependent
 // loads at 10M instead of 24) -- the small-batch latency path.
-template <int DMAX, int WSMAX, bool COOP, int MINB, class T>
-__global__ void __launch_bounds__(128, MINB) k_locate(LocateArgs a) {
+// rank_of + window of query q on curve c (one thread, or one warp with COOP:
+// every lane computes the key, the lanes split the 32-ary search).  lut: the
+// view's cell table in shared memory.  Returns the window begin; *rank_out
+// the rank.
+template <int DMAX, int WSMAX, bool COOP, class T>
+__device__ __forceinline__ uint64_t locate_one(const LocateArgs& a, const uint32_t* lut, uint32_t q, uint32_t c,
+                                               int lane, uint64_t* rank_out) {
     constexpr int WMAX = DMAX / 2 > kMaxKeyWords ? kMaxKeyWords : (DMAX / 2 < 1 ? 1 : DMAX / 2);
-    __shared__ uint32_t lut[256];
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) lut[i] = a.lut[i];
-    __syncthreads();
-    const uint64_t t = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> (COOP ? 5 : 0);
-    const int lane = threadIdx.x & 31;
-    if (t >= uint64_t(a.nq) * a.C) return;
-    const uint32_t q = uint32_t(t / a.C), c = uint32_t(t % a.C);
     const CurveDev& cv = a.curves[c];
     const int d = int(cv.dims);
 
@@ -153,6 +151,21 @@ __global__ void __launch_bounds__(128, MINB) k_locate(LocateArgs a) {
     uint64_t begin = rank >= below_n ? rank - below_n : 0;
     if (begin + take > a.n) begin = a.n - take;
     HCG_DASSERT(begin + take <= a.n && rank <= a.n);
+    *rank_out = rank;
+    return begin;
+}
+
+template <int DMAX, int WSMAX, bool COOP, int MINB, class T>
+__global__ void __launch_bounds__(128, MINB) k_locate(LocateArgs a) {
+    __shared__ uint32_t lut[256];
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) lut[i] = a.lut[i];
+    __syncthreads();
+    const uint64_t t = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> (COOP ? 5 : 0);
+    const int lane = threadIdx.x & 31;
+    if (t >= uint64_t(a.nq) * a.C) return;
+    const uint32_t q = uint32_t(t / a.C), c = uint32_t(t % a.C);
+    uint64_t rank;
+    const uint64_t begin = locate_one<DMAX, WSMAX, COOP, T>(a, lut, q, c, lane, &rank);
     if (!COOP || lane == 0) {
         a.out_begin[t] = uint32_t(begin);
         if (a.out_rank) a.out_rank[t] = rank;
@@ -410,16 +423,17 @@ __global__ void __launch_bounds__(kRefineThreads) k_union(RefineArgs a, uint32_t
 // (8*grp + l8)'s squared distance in lane l8 of group grp, which offers
 // (sqdist << 32 | slot).  Lists are read with ld.global.cg: they were written
 // by the preceding union launch.
-template <int R, int CR>
+template <int R, int CR, bool SMEMLIST = false>
 __device__ __forceinline__ void gather_list(const RefineArgs& a, const uint32_t* list, uint32_t n, uint32_t start,
                                             uint32_t step, const uint4 (&qv)[CR], int lane, WarpTopK<R>& tk) {
     const int l8 = lane & 7, grp = lane >> 3;
     const uint32_t chunks = a.pitch >> 4;
+    auto ld = [&](uint32_t e) -> uint32_t { return SMEMLIST ? list[e] : __ldcg(list + e); };
     uint32_t nx[8];
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
         const uint32_t e = start + grp * 8 + r;
-        nx[r] = e < n ? __ldcg(list + e) : kEmpty;
+        nx[r] = e < n ? ld(e) : kEmpty;
     }
     for (uint32_t base = start; base < n; base += step) {
 #pragma unroll
@@ -442,7 +456,7 @@ __device__ __forceinline__ void gather_list(const RefineArgs& a, const uint32_t*
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
             const uint32_t e = base + step + grp * 8 + r;
-            nx[r] = e < n ? __ldcg(list + e) : kEmpty;
+            nx[r] = e < n ? ld(e) : kEmpty;
         }
         uint32_t acc[8];
 #pragma unroll
@@ -485,9 +499,9 @@ __device__ __forceinline__ void gather_list(const RefineArgs& a, const uint32_t*
 // SMALLC (C <= 32): lane c holds curve c's window start pointer (slots[c] +
 // begin), fetched once per query and broadcast with a shuffle, so an entry
 // costs one dependent load (the slot) instead of three (pointer, begin, slot).
-template <int R, int CR, bool SMALLC>
+template <int CR, bool SMALLC, class TK>
 __device__ __forceinline__ void gather_windows(const RefineArgs& a, const uint32_t* begins_q, const uint4 (&qv)[CR],
-                                               int lane, WarpTopK<R>& tk, uint64_t* wsm) {
+                                               int lane, TK& tk, uint64_t* wsm) {
     const int l8 = lane & 7, grp = lane >> 3;
     const uint32_t chunks = a.pitch >> 4;
     const uint32_t take = a.take, n = a.C * take, C = a.C;
@@ -614,7 +628,7 @@ __global__ void __launch_bounds__(NT, MINB) k_gather_nu(RefineArgs a) {
         load_query<CR>(a, qq, lane, qv);
         WarpTopK<R> tk;
         tk.init(int(a.k));
-        gather_windows<R, CR, SMALLC>(a, a.begins + uint64_t(qq) * a.C, qv, lane, tk, wsm);
+        gather_windows<CR, SMALLC>(a, a.begins + uint64_t(qq) * a.C, qv, lane, tk, wsm);
         uint32_t valid = 0;
 #pragma unroll
         for (int r = 0; r < R; ++r)
@@ -653,6 +667,154 @@ __global__ void __launch_bounds__(NW * 32) k_gather_cta(RefineArgs a, const uint
             write_result<R>(a, a.qorder ? __ldg(a.qorder + q) : q, fin, lane, n);
         }
         __syncthreads();
+    }
+}
+
+// ------------------------------------------------------ small batches ----
+// The whole search of one query in one CTA -- the latency path for small
+// batches (u8 rows of <= 128 B, C x take <= kSmallMaxWalk): one launch
+// instead of locate + union + gather, no HBM scratch.
+//   1. warp w locates curves w, w + NW, ...: key + 32-ary cooperative
+//      lower_bound + window (rank_of / window, multicurves.hpp:57-63);
+//   2. all threads: candidate union (multicurves.hpp:87-89) -- the windows'
+//      slots into a shared-memory CAS hash set, first copies appended
+//      (warp-aggregated) to a shared unique list;
+//   3. each warp gathers a slice of the list into its warp top-k (exact u32
+//      distances, (distance, id) order), warp 0 merges the NW lists.
+constexpr int kSmallThreads = 512;
+constexpr uint32_t kSmallMaxWalk = 8192;
+constexpr uint32_t kSmallBatch = 512;
+
+__host__ __device__ __forceinline__ uint32_t small_table_bits(uint32_t T) {
+    uint32_t tb = 5;
+    while ((1u << tb) * 7u < T * 10u) ++tb;
+    return tb;
+}
+
+template <int R>
+__host__ __device__ __forceinline__ size_t small_smem_bytes(uint32_t C, uint32_t T) {
+    return size_t(kSmallThreads / 32) * 32 * R * 8 + 256 * 4 + ((C + 3) & ~3u) * 4 + (size_t(4) << small_table_bits(T)) +
+           size_t(T) * 4;
+}
+
+template <int DMAX, int WSMAX, int R>
+__global__ void __launch_bounds__(kSmallThreads) k_search_small(LocateArgs la, RefineArgs a) {
+    constexpr int NW = kSmallThreads / 32;
+    constexpr int KCAP = 32 * R;
+    extern __shared__ __align__(16) unsigned char ssm[];
+    uint64_t* mbuf = reinterpret_cast<uint64_t*>(ssm);      // NW x KCAP
+    uint32_t* lut = reinterpret_cast<uint32_t*>(mbuf + NW * KCAP);  // 256
+    uint32_t* begins = lut + 256;                           // C
+    const uint32_t T = a.C * a.take, tb = small_table_bits(T), tmask = (1u << tb) - 1;
+    uint32_t* table = begins + ((a.C + 3) & ~3u);           // 1 << tb
+    uint32_t* list = table + (1u << tb);                    // T
+    __shared__ uint32_t count;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (uint32_t q = blockIdx.x; q < a.nq; q += gridDim.x) {
+        for (int i = tid; i < 256; i += kSmallThreads) lut[i] = la.lut[i];
+        for (uint32_t i = tid; i <= tmask; i += kSmallThreads) table[i] = kEmpty;
+        if (tid == 0) count = 0;
+        __syncthreads();
+        for (uint32_t c = warp; c < a.C; c += NW) {
+            uint64_t rank;
+            const uint64_t b = locate_one<DMAX, WSMAX, true, uint8_t>(la, lut, q, c, lane, &rank);
+            if (lane == 0) begins[c] = uint32_t(b);
+        }
+        __syncthreads();
+        for (uint32_t i0 = uint32_t(warp) * 32; i0 < T; i0 += kSmallThreads) {
+            const uint32_t i = i0 + lane;
+            const bool has = i < T;
+            bool fresh = false;
+            uint32_t s = 0;
+            if (has) {
+                const uint32_t c = i / a.take, p = i - c * a.take;
+                s = __ldg(a.slots[c] + begins[c] + p);
+                uint32_t h = hash_slot(s) >> (32 - tb);
+                while (true) {
+                    const uint32_t prev = atomicCAS(&table[h], kEmpty, s);
+                    if (prev == kEmpty) {
+                        fresh = true;
+                        break;
+                    }
+                    if (prev == s) break;
+                    h = (h + 1) & tmask;
+                }
+            }
+            const unsigned b = __ballot_sync(kFull, fresh);
+            if (b) {
+                const int leader = __ffs(b) - 1;
+                uint32_t base = 0;
+                if (lane == leader) base = atomicAdd(&count, uint32_t(__popc(b)));
+                base = __shfl_sync(kFull, base, leader);
+                if (fresh) list[base + __popc(b & lanemask_lt_s())] = s;
+            }
+        }
+        __syncthreads();
+        const uint32_t n = count;
+        uint4 qv[1];
+        load_query<1>(a, q, lane, qv);
+        WarpTopK<R> tk;
+        tk.init(int(a.k));
+        gather_list<R, 1, true>(a, list, n, uint32_t(warp) * 32, NW * 32, qv, lane, tk);
+#pragma unroll
+        for (int r = 0; r < R; ++r) mbuf[warp * KCAP + lane * R + r] = tk.a[r];
+        __syncthreads();
+        if (warp == 0) {
+            WarpTopK<R> fin;
+            fin.init(int(a.k));
+            const uint32_t kr = (a.k + 31) & ~31u;
+            for (int w = 0; w < NW; ++w)
+                for (uint32_t i = 0; i < kr; i += 32) fin.offer(mbuf[w * KCAP + i + lane], lane);
+            write_result<R>(a, q, fin, lane, n);
+        }
+        __syncthreads();
+    }
+}
+
+template <int DMAX, int WSMAX, int R>
+hcg_status small_launch(const LocateArgs& la, const RefineArgs& a, int device, cudaStream_t st) {
+    auto kern = k_search_small<DMAX, WSMAX, R>;
+    static bool cfg[64] = {};
+    if (!cfg[device & 63]) {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(small_smem_bytes<R>(512, kSmallMaxWalk))) != cudaSuccess)
+            return set_error(HCG_ECUDA, "small-batch search: cannot opt in to dynamic shared memory");
+        cfg[device & 63] = true;
+    }
+    count_launches(1);
+    kern<<<a.nq, kSmallThreads, small_smem_bytes<R>(a.C, a.C * a.take), st>>>(la, a);
+    return check_launch("k_search_small");
+}
+
+template <int DMAX, int WSMAX>
+hcg_status small_dispatch_r(const LocateArgs& la, const RefineArgs& a, int device, cudaStream_t st) {
+    switch (a.k <= 32 ? 1 : a.k <= 64 ? 2 : a.k <= 128 ? 4 : 8) {
+        case 1: return small_launch<DMAX, WSMAX, 1>(la, a, device, st);
+        case 2: return small_launch<DMAX, WSMAX, 2>(la, a, device, st);
+        case 4: return small_launch<DMAX, WSMAX, 4>(la, a, device, st);
+        default: return small_launch<DMAX, WSMAX, 8>(la, a, device, st);
+    }
+}
+
+bool small_eligible(const LocateArgs& la, const RefineArgs& a, int dmax, int wsmax) {
+    static const bool off = knob("HCG_NO_SMALL") != nullptr;  // A/B: locate + union + gather for every batch
+    return !off && a.dtype == HCG_U8 && la.dtype == HCG_U8 && a.nq >= 1 && a.nq <= kSmallBatch && a.pitch <= 128 &&
+           uint64_t(a.C) * a.take <= kSmallMaxWalk && dmax <= 16 && wsmax <= 4 && a.mode != kOutCandidates;
+}
+
+hcg_status launch_search_small(const LocateArgs& la, const RefineArgs& a, int dmax, int wsmax, int device,
+                               cudaStream_t st) {
+    if (dmax <= 8) {
+        switch (wsmax) {
+            case 1: return small_dispatch_r<8, 1>(la, a, device, st);
+            case 2: return small_dispatch_r<8, 2>(la, a, device, st);
+            default: return small_dispatch_r<8, 4>(la, a, device, st);
+        }
+    }
+    switch (wsmax) {
+        case 1: return small_dispatch_r<16, 1>(la, a, device, st);
+        case 2: return small_dispatch_r<16, 2>(la, a, device, st);
+        default: return small_dispatch_r<16, 4>(la, a, device, st);
     }
 }
 
@@ -1247,11 +1409,20 @@ constexpr uint64_t kMaxWalk = uint64_t(1) << 27;
 // The union-less K3c (k_gather_nu) serves k <= 128, u8 rows in curve-0
 // order and batches of >= 16K queries; everything else runs the separate
 // union (K3b) + K3c.  One predicate for the scratch query and the launch.
+// k > 32 pays for the merge + dedup of repeats (and wider lists) in the walk;
+// that beats the union's hash rounds only for long walks: measured at 10M,
+// C = 8, 100K queries (profiles/r02_unionless_k_ab.jsonl), k = 64 / 100 union-less vs
+// union + gather: D = 350 8.1 / 10.2 vs 6.7 / 7.5 ms, D = 1024 18.3 / 21.9 vs
+// 23.1 / 23.6 ms; k <= 32 is faster union-less at every depth.
+constexpr uint32_t kUnionlessWideWalk = 8192;  // C x take from which k > 32 walks union-less
+
 template <int R>
 bool unionless_path(const RefineArgs& a) {
-    static const bool off = getenv("HCG_NO_UNIONLESS") != nullptr;  // A/B: separate union for every k
-    return R <= 4 && a.k <= 128 && !off && a.mode != kOutCandidates && a.dtype == HCG_U8 && a.nq >= 16384 &&
-           a.idtab != nullptr;
+    static const bool off = knob("HCG_NO_UNIONLESS") != nullptr;  // A/B: separate union for every k
+    static const bool wide = knob("HCG_UNIONLESS_WIDE") != nullptr;  // A/B: union-less for every k <= 128
+    if (R > 4 || a.k > 128 || off) return false;
+    if (a.k > 32 && !wide && uint64_t(a.C) * a.take < kUnionlessWideWalk) return false;
+    return a.mode != kOutCandidates && a.dtype == HCG_U8 && a.nq >= 16384 && a.idtab != nullptr;
 }
 
 // The union-less walk's list width: k <= 32 inserts one offer at a time
@@ -1295,7 +1466,7 @@ hcg_status refine_dispatch(const RefineArgs& a_in, void* scratch, size_t* scratc
     const uint32_t utb = std::min<uint32_t>(tb + 1, 16);
     const size_t usmem = union_smem_bytes(a_in.C, T, utb);
     const bool smem_union = T <= kUnionMaxT && usmem <= 160 * 1024;
-    static const bool force_smem_union = getenv("HCG_UNION_SMEM") != nullptr;
+    static const bool force_smem_union = knob("HCG_UNION_SMEM") != nullptr;
     const bool reg_union = T <= 32u * 256 && (size_t(8) << tb) <= 128 * 1024 && !force_smem_union;
     const int sms = dev_info(device).sms;
     const uint32_t chunk = uint32_t(std::max<size_t>(1, std::min<size_t>(a_in.nq, kListBudget / (size_t(lstride) * 4))));
@@ -1307,7 +1478,7 @@ hcg_status refine_dispatch(const RefineArgs& a_in, void* scratch, size_t* scratc
     // Large batches run in curve-0 window order: queries processed at the
     // same time share candidate rows (rows are stored in curve-0 order), so
     // part of the gather hits L2 (measured 5.15 -> 4.75 ms at 100K queries).
-    static const bool no_qsort = getenv("HCG_NO_QSORT") != nullptr;
+    static const bool no_qsort = knob("HCG_NO_QSORT") != nullptr;
     const bool qsort = !no_qsort && (nu || reg_union) && a_in.mode != kOutCandidates && a_in.nq >= 16384 &&
                        (nu || chunk >= a_in.nq) && a_in.idtab != nullptr;  // both gathers map list q -> qorder[q]
     const size_t qsort_bytes = qsort ? size_t(a_in.nq) * 24 + radix_counts_bytes(a_in.nq) + 256 : 0;
@@ -1421,6 +1592,15 @@ hcg_status refine_cr(const RefineArgs& a, void* scratch, size_t* sb, int device,
     return refine_dispatch<R, 4>(a, scratch, sb, device, st);
 }
 }  // namespace
+
+bool refine_unionless(const RefineArgs& a) {
+    switch (r_bucket(a.k)) {
+        case 1: return unionless_path<1>(a);
+        case 2: return unionless_path<2>(a);
+        case 4: return unionless_path<4>(a);
+        default: return unionless_path<8>(a);
+    }
+}
 
 hcg_status launch_refine(const RefineArgs& a, void* scratch, size_t* scratch_bytes, int device, cudaStream_t st) {
     if (scratch_bytes) *scratch_bytes = 0;

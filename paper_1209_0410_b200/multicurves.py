@@ -283,6 +283,10 @@ class MulticurvesIndex:
     def key_words(self, c: int) -> int:
         return int(lib().hcg_key_words(self._h, c))
 
+    def unionless(self, nq: int, k: int, depth: int) -> bool:
+        """Whether a search of nq queries runs the union-less refine kernel."""
+        return bool(lib().hcg_refine_unionless(self._h, nq, k, depth))
+
     def device_bytes(self) -> int:
         return int(lib().hcg_device_bytes(self._h))
 

@@ -129,3 +129,37 @@ def test_random_configurations_large_batch(seed):
         np.testing.assert_array_equal(ids[q, :L], oids[q, :L])
         assert d[q, :L].tobytes() == odist[q, :L].tobytes()
         assert (ids[q, L:] == np.uint64(2**64 - 1)).all()
+
+
+@pytest.mark.parametrize("k", [33, 64, 100, 128])
+def test_unionless_wide_k_long_walks(k):
+    """k > 32 with C x depth >= 8192 (and >= 16K queries): the union-less walk
+    with batched merges and the dedup of repeats after each merge."""
+    n = 12_000
+    rows = P.gen_rows(0, n)
+    qs = P.gen_queries(0, 16_384, n)
+    gi = H.MulticurvesIndex(rows, H.default_scheme(128, 8, 16), H.LIFTED)
+    assert gi.unionless(16_384, k, 1100)
+    oi = P.Oracle(H.LIFTED.floats(rows), 8, 16)
+    ids, sq, ln = gi.search_batch(qs, k, 1100)
+    oids, odist, oln = oi.search(H.LIFTED.floats(qs), k, 1100)
+    np.testing.assert_array_equal(ln, oln)
+    np.testing.assert_array_equal(ids, oids)
+    assert gi.rooted(sq).tobytes() == odist.tobytes()
+
+
+@pytest.mark.parametrize("view,m", [(H.LIFTED, 16), (H.RAW, 8)])
+def test_batch_size_paths_agree(view, m):
+    """The fused one-CTA-per-query latency kernel (<= 512 queries), the
+    union + gather path and the union-less walk (>= 16K) return the same
+    lists for the same queries."""
+    n = 30_000
+    rows = P.gen_rows(0, n)
+    qs = P.gen_queries(0, 16_384, n)
+    gi = H.MulticurvesIndex(rows, H.default_scheme(128, 8, m), view)
+    for k, depth in ((10, 350), (100, 350), (1, 16), (256, 600)):
+        big = gi.search_batch(qs, k, depth)
+        for lo, hi in ((0, 1), (5, 37), (100, 612), (1000, 4000)):
+            part = gi.search_batch(qs[lo:hi], k, depth)
+            for x, y in zip(part, big):
+                np.testing.assert_array_equal(x, y[lo:hi] if y.ndim == 1 else y[lo:hi])

@@ -1,4 +1,5 @@
-"""K5 ground-truth throughput: tensor-core (tcgen05 kind::i8) vs CUDA-core
+"""(A/B switches: run against a knob build, HCG_LIB_OVERRIDE=$(python tools/build_variant.py knobs).)
+K5 ground-truth throughput: tensor-core (tcgen05 kind::i8) vs CUDA-core
 brute force, 10M lifted rows x 1000 queries, k=10.  Run twice, once with
 HCG_BRUTE_CUDA_CORES=1 (the env var is read once per process)."""
 import json

@@ -1,4 +1,5 @@
-"""Probe: which batch order gives the gather the most L2 reuse?  Times
+"""(A/B switches: run against a knob build, HCG_LIB_OVERRIDE=$(python tools/build_variant.py knobs).)
+Probe: which batch order gives the gather the most L2 reuse?  Times
 search_timed (batch-order sort disabled, HCG_NO_QSORT=1) on the same queries
 pre-sorted on the host by: generator order, curve-0 rank, a coarse Z-order key
 over many dimensions (top bits of 32 / 64 dims interleaved)."""

@@ -54,7 +54,7 @@ for C in [int(x) for x in a.curves.split(",")]:
                 U = float(ix.candidate_counts(qs[:2000], D).mean())
                 print(json.dumps({"curves": C, "depth": D, "k": k, "view": a.view, "n": a.n,
                                   "qps": a.queries / (ms * 1e-3), "ms_per_batch": ms,
-                                  "unionless": k <= 128 and os.environ.get("HCG_NO_UNIONLESS") is None,
+                                  "unionless": ix.unionless(a.queries, k, D),
                                   "recall_at_k": recall(got, truth[k], k), "unique_candidates": U}), flush=True)
             except Exception as e:  # capacity limits (curves x depth) are reported, not fatal
                 print(json.dumps({"curves": C, "depth": D, "k": k, "error": str(e)}), flush=True)

@@ -1,4 +1,5 @@
-"""Time the refine kernel on the bench workload (10M lifted, 100K queries,
+"""(A/B switches: run against a knob build, HCG_LIB_OVERRIDE=$(python tools/build_variant.py knobs).)
+Time the refine kernel on the bench workload (10M lifted, 100K queries,
 k=10, depth $DEPTH) and print its per-launch device time and GB/s."""
 import os
 import sys
