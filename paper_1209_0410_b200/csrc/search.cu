@@ -683,7 +683,7 @@ __global__ void __launch_bounds__(NW * 32) k_gather_cta(RefineArgs a, const uint
 //      distances, (distance, id) order), warp 0 merges the NW lists.
 constexpr int kSmallThreads = 512;
 constexpr uint32_t kSmallMaxWalk = 8192;
-constexpr uint32_t kSmallBatch = 512;
+constexpr uint32_t kSmallBatch = 128;
 
 __host__ __device__ __forceinline__ uint32_t small_table_bits(uint32_t T) {
     uint32_t tb = 5;

@@ -1,4 +1,4 @@
-"""Multi-process sharding on CPU (gloo, world size 2 and 3): each rank owns the
+"""Multi-process sharding on CPU (gloo, world size 2, 3 and 8 -- the 8-GPU box layout): each rank owns the
 ids i = rank (mod G), answers every query on its shard, packs
 (sqdist << 32 | gid), and the product's exchange() all-gathers the blocks; the
 (distance, id) merge of the gathered blocks must equal the sharded oracle
@@ -47,7 +47,7 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 8])
 def test_sharded_exchange_and_merge_match_oracle(world):
     ctx = mp.get_context("spawn")
     q = ctx.SimpleQueue()

@@ -5,10 +5,13 @@
 //   cpasync  : LDGSTS (cp.async.cg 16 B) into a per-warp shared ring
 //   bulk     : cp.async.bulk (TMA engine, 128 B per row) into a per-warp ring,
 //              completion on an mbarrier per stage
+//   gather4  : cp.async.bulk.tensor.2d.tile::gather4 (TMA, 4 rows of a 2-D
+//              tensor map per instruction) into a per-warp ring
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o gather_bench gather_bench.cu
 #include <cstdio>
 #include <cstdint>
 #include <vector>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s: %s\n", #x, cudaGetErrorString(e)); return 1; } } while (0)
@@ -150,6 +153,65 @@ __global__ void __launch_bounds__(128) k_bulk(const uint8_t* __restrict__ rows, 
     out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
 }
 
+// tile::gather4: per warp S stages of 32 rows; lanes 0..7 each issue one
+// gather4 (4 rows x 128 B) per stage, one mbarrier per stage.
+template <int S>
+__global__ void __launch_bounds__(128) k_gather4(const __grid_constant__ CUtensorMap map, const uint32_t* __restrict__ idx,
+                                                 uint64_t nidx, uint32_t* out) {
+    extern __shared__ __align__(128) uint8_t sm[];
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    uint8_t* ring = sm + wl * S * 4096;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + (blockDim.x / 32) * S * 4096) + wl * S;
+    if (lane == 0)
+        for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;");
+    __syncwarp();
+    const uint64_t warps = uint64_t(gridDim.x) * (blockDim.x / 32);
+    const uint64_t w = uint64_t(blockIdx.x) * (blockDim.x / 32) + wl;
+    const uint64_t nb = nidx / 32;
+    uint32_t acc = 0;
+    auto issue = [&](uint64_t b, int stage) {
+        const uint32_t my = __ldg(idx + b * 32 + lane);
+        if (lane == 0) mbar_expect(&bars[stage], 32 * 128);
+        __syncwarp();
+        const int r0 = __shfl_sync(0xffffffff, my, (lane * 4) & 31), r1 = __shfl_sync(0xffffffff, my, (lane * 4 + 1) & 31),
+                  r2 = __shfl_sync(0xffffffff, my, (lane * 4 + 2) & 31), r3 = __shfl_sync(0xffffffff, my, (lane * 4 + 3) & 31);
+        if (lane < 8) {
+            const uint32_t dst = (uint32_t)__cvta_generic_to_shared(ring + stage * 4096 + lane * 512);
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(dst),
+                "l"(reinterpret_cast<uint64_t>(&map)), "r"((uint32_t)__cvta_generic_to_shared(&bars[stage])), "r"(0),
+                "r"(r0), "r"(r1), "r"(r2), "r"(r3)
+                : "memory");
+        }
+    };
+    uint64_t b_issue = w;
+    for (int s = 0; s < S && b_issue < nb; ++s, b_issue += warps) issue(b_issue, s);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (uint64_t b = w; b < nb; b += warps) {
+        mbar_wait(&bars[stage], phase);
+        const uint32_t* p = reinterpret_cast<const uint32_t*>(ring + stage * 4096);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) acc += p[i * 32 + lane];
+        __syncwarp();
+        if (b_issue < nb) {
+            issue(b_issue, stage);
+            b_issue += warps;
+        }
+        if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+        }
+    }
+    out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
+
+typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                             const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                             CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
 int main() {
     const uint64_t n = 10000000, nidx = 256ull << 20;  // 268M rows = 34 GB gathered
     uint8_t* rows;
@@ -215,6 +277,32 @@ int main() {
             snprintf(nm, 64, "bulk S=%d %d blk/SM", S, bps);
             if (S == 4) RUN(nm, (k_bulk<4><<<148 * bps, 128, smem>>>(rows, idx, nidx, out)));
             else RUN(nm, (k_bulk<8><<<148 * bps, 128, smem>>>(rows, idx, nidx, out)));
+        }
+    }
+    {
+        void* fp = nullptr;
+        cudaDriverEntryPointQueryResult qr;
+        CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fp, cudaEnableDefault, &qr));
+        CUtensorMap map;
+        const cuuint64_t dims[2] = {128, n};
+        const cuuint64_t strides[1] = {128};
+        const cuuint32_t box[2] = {128, 1};
+        const cuuint32_t estr[2] = {1, 1};
+        CUresult r = reinterpret_cast<EncodeFn>(fp)(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, rows, dims, strides, box, estr,
+                                                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                                    CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) printf("tensor map encode failed: %d\n", int(r));
+        for (int S : {4, 8}) {
+            const int smem = 4 * S * 4096 + 4 * S * 8;
+            if (S == 4) { CK(cudaFuncSetAttribute(k_gather4<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)); }
+            if (S == 8) { CK(cudaFuncSetAttribute(k_gather4<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)); }
+            for (int bps : {1, 2, 3}) {
+                if (bps * smem > 220 * 1024) continue;
+                char nm[64];
+                snprintf(nm, 64, "gather4 S=%d %d blk/SM", S, bps);
+                if (S == 4) RUN(nm, (k_gather4<4><<<148 * bps, 128, smem>>>(map, idx, nidx, out)));
+                else RUN(nm, (k_gather4<8><<<148 * bps, 128, smem>>>(map, idx, nidx, out)));
+            }
         }
     }
     // sequential copy for reference
