@@ -38,6 +38,7 @@ struct hcg_index {
     uint32_t** d_slot_ptrs = nullptr;
     uint64_t bytes = 0;
     bool broken = false;  // a failed table upload after an insert: every call is refused
+    bool dims16 = false;  // every curve has exactly 16 dims (the default scheme at d = 128, C = 8)
 };
 
 namespace hcg {
@@ -595,6 +596,8 @@ hcg_status new_index(const hcg_scheme* s, uint64_t n, uint64_t id_base, uint64_t
     uint32_t maxd = 1;
     for (uint32_t c = 0; c < ix->C; ++c) maxd = std::max(maxd, ix->off[c + 1] - ix->off[c]);
     ix->dmax = pow2_bucket(maxd, 8, 128);
+    ix->dims16 = true;
+    for (uint32_t c = 0; c < ix->C; ++c) ix->dims16 = ix->dims16 && ix->off[c + 1] - ix->off[c] == 16;
     ix->curves.resize(ix->C);
     for (uint32_t c = 0; c < ix->C; ++c) {
         CurveDev& cv = ix->curves[c];
@@ -1130,8 +1133,8 @@ static hcg_status search_impl(const hcg_index* ix, const uint8_t* queries, uint3
             a.out_sqdist = os.dev;
             a.out_len = ol.dev;
             const LocateArgs la = locate_args(ix, dq, nq, depth, nullptr, nullptr, flag);
-            if (!ms_out && small_eligible(la, a, ix->dmax, ix->wsmax)) {
-                HCG_TRY(launch_search_small(la, a, ix->dmax, ix->wsmax, ix->device, st));
+            if (!ms_out && small_eligible(la, a, ix->dims16, ix->wsmax)) {
+                HCG_TRY(launch_search_small(la, a, ix->wsmax, ix->device, st));
                 goto finish;
             }
         }

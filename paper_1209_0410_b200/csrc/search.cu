@@ -57,7 +57,10 @@ __device__ __forceinline__ int suffix_cmp(const uint64_t* e, const uint64_t (&qs
 // every lane computes the key, the lanes split the 32-ary search).  lut: the
 // view's cell table in shared memory.  Returns the window begin; *rank_out
 // the rank.
-template <int DMAX, int WSMAX, bool COOP, class T>
+// MFIX (8 or 16): every curve has exactly 16 dims and m = MFIX -- the key is
+// built by the compile-time d16 transform alone (a fraction of the generic
+// code: the latency kernel runs it from a cold instruction cache).
+template <int DMAX, int WSMAX, bool COOP, class T, int MFIX = 0>
 __device__ __forceinline__ uint64_t locate_one(const LocateArgs& a, const uint32_t* lut, uint32_t q, uint32_t c,
                                                int lane, uint64_t* rank_out) {
     constexpr int WMAX = DMAX / 2 > kMaxKeyWords ? kMaxKeyWords : (DMAX / 2 < 1 ? 1 : DMAX / 2);
@@ -70,7 +73,10 @@ __device__ __forceinline__ uint64_t locate_one(const LocateArgs& a, const uint32
 #pragma unroll
     for (int s = 0; s < DMAX; ++s) x[s] = s < d ? cell_of(__ldg(row + __ldg(asg + s)), lut, a.m, a.bad) : 0u;
     uint64_t key[WMAX];
-    make_key<DMAX, WMAX>(x, d, a.m, a.kind, key);
+    if constexpr (MFIX != 0 && DMAX == 16 && WMAX >= 4)
+        make_key_d16<MFIX, WMAX>(x, a.kind, key);
+    else
+        make_key<DMAX, WMAX>(x, d, a.m, a.kind, key);
 
     // Compare the query against the common prefix (bits above hv).
     const int hw = int(cv.hv >> 6), hb = int(cv.hv & 63);
@@ -693,21 +699,22 @@ __host__ __device__ __forceinline__ uint32_t small_table_bits(uint32_t T) {
 
 template <int R>
 __host__ __device__ __forceinline__ size_t small_smem_bytes(uint32_t C, uint32_t T) {
-    return size_t(kSmallThreads / 32) * 32 * R * 8 + 256 * 4 + ((C + 3) & ~3u) * 4 + (size_t(4) << small_table_bits(T)) +
+    return size_t(kSmallThreads / 32) * 32 * R * 8 + size_t(C) * 8 + 256 * 4 + (size_t(4) << small_table_bits(T)) +
            size_t(T) * 4;
 }
 
-template <int DMAX, int WSMAX, int R>
+template <int M, int WSMAX, int R>
 __global__ void __launch_bounds__(kSmallThreads) k_search_small(LocateArgs la, RefineArgs a) {
     constexpr int NW = kSmallThreads / 32;
     constexpr int KCAP = 32 * R;
+    constexpr int JN = kSmallMaxWalk / kSmallThreads;  // window entries per thread
     extern __shared__ __align__(16) unsigned char ssm[];
-    uint64_t* mbuf = reinterpret_cast<uint64_t*>(ssm);      // NW x KCAP
-    uint32_t* lut = reinterpret_cast<uint32_t*>(mbuf + NW * KCAP);  // 256
-    uint32_t* begins = lut + 256;                           // C
+    uint64_t* mbuf = reinterpret_cast<uint64_t*>(ssm);              // NW x KCAP
+    const uint32_t** wptr = reinterpret_cast<const uint32_t**>(mbuf + NW * KCAP);  // C: slots[c] + begin
+    uint32_t* lut = reinterpret_cast<uint32_t*>(wptr + a.C);        // 256
     const uint32_t T = a.C * a.take, tb = small_table_bits(T), tmask = (1u << tb) - 1;
-    uint32_t* table = begins + ((a.C + 3) & ~3u);           // 1 << tb
-    uint32_t* list = table + (1u << tb);                    // T
+    uint32_t* table = lut + 256;                                    // 1 << tb
+    uint32_t* list = table + (1u << tb);                            // T
     __shared__ uint32_t count;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (uint32_t q = blockIdx.x; q < a.nq; q += gridDim.x) {
@@ -715,20 +722,31 @@ __global__ void __launch_bounds__(kSmallThreads) k_search_small(LocateArgs la, R
         for (uint32_t i = tid; i <= tmask; i += kSmallThreads) table[i] = kEmpty;
         if (tid == 0) count = 0;
         __syncthreads();
+        // 1. locate: a warp per curve
         for (uint32_t c = warp; c < a.C; c += NW) {
             uint64_t rank;
-            const uint64_t b = locate_one<DMAX, WSMAX, true, uint8_t>(la, lut, q, c, lane, &rank);
-            if (lane == 0) begins[c] = uint32_t(b);
+            const uint64_t b = locate_one<16, WSMAX, true, uint8_t, M>(la, lut, q, c, lane, &rank);
+            if (lane == 0) wptr[c] = a.slots[c] + b;
         }
         __syncthreads();
-        for (uint32_t i0 = uint32_t(warp) * 32; i0 < T; i0 += kSmallThreads) {
-            const uint32_t i = i0 + lane;
-            const bool has = i < T;
+        // 2. union: every thread loads its window entries first (independent
+        // loads in flight together), then inserts them into the hash set
+        uint32_t sl[JN];
+#pragma unroll
+        for (int j = 0; j < JN; ++j) {
+            const uint32_t i = uint32_t(tid) + uint32_t(j) * kSmallThreads;
+            sl[j] = kEmpty;
+            if (i < T) {
+                const uint32_t c = i / a.take;
+                sl[j] = __ldg(wptr[c] + (i - c * a.take));
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < JN; ++j) {
+            if (uint32_t(j) * kSmallThreads >= T) break;  // block-uniform
+            const uint32_t s = sl[j];
             bool fresh = false;
-            uint32_t s = 0;
-            if (has) {
-                const uint32_t c = i / a.take, p = i - c * a.take;
-                s = __ldg(a.slots[c] + begins[c] + p);
+            if (s != kEmpty) {
                 uint32_t h = hash_slot(s) >> (32 - tb);
                 while (true) {
                     const uint32_t prev = atomicCAS(&table[h], kEmpty, s);
@@ -740,16 +758,17 @@ __global__ void __launch_bounds__(kSmallThreads) k_search_small(LocateArgs la, R
                     h = (h + 1) & tmask;
                 }
             }
-            const unsigned b = __ballot_sync(kFull, fresh);
-            if (b) {
-                const int leader = __ffs(b) - 1;
+            const unsigned bal = __ballot_sync(kFull, fresh);
+            if (bal) {
+                const int leader = __ffs(bal) - 1;
                 uint32_t base = 0;
-                if (lane == leader) base = atomicAdd(&count, uint32_t(__popc(b)));
+                if (lane == leader) base = atomicAdd(&count, uint32_t(__popc(bal)));
                 base = __shfl_sync(kFull, base, leader);
-                if (fresh) list[base + __popc(b & lanemask_lt_s())] = s;
+                if (fresh) list[base + __popc(bal & lanemask_lt_s())] = s;
             }
         }
         __syncthreads();
+        // 3. gather + exact L2 + warp top-k over slices of the list; warp 0 merges
         const uint32_t n = count;
         uint4 qv[1];
         load_query<1>(a, q, lane, qv);
@@ -771,9 +790,9 @@ __global__ void __launch_bounds__(kSmallThreads) k_search_small(LocateArgs la, R
     }
 }
 
-template <int DMAX, int WSMAX, int R>
+template <int M, int WSMAX, int R>
 hcg_status small_launch(const LocateArgs& la, const RefineArgs& a, int device, cudaStream_t st) {
-    auto kern = k_search_small<DMAX, WSMAX, R>;
+    auto kern = k_search_small<M, WSMAX, R>;
     static bool cfg[64] = {};
     if (!cfg[device & 63]) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -786,25 +805,26 @@ hcg_status small_launch(const LocateArgs& la, const RefineArgs& a, int device, c
     return check_launch("k_search_small");
 }
 
-template <int DMAX, int WSMAX>
+template <int M, int WSMAX>
 hcg_status small_dispatch_r(const LocateArgs& la, const RefineArgs& a, int device, cudaStream_t st) {
     switch (a.k <= 32 ? 1 : a.k <= 64 ? 2 : a.k <= 128 ? 4 : 8) {
-        case 1: return small_launch<DMAX, WSMAX, 1>(la, a, device, st);
-        case 2: return small_launch<DMAX, WSMAX, 2>(la, a, device, st);
-        case 4: return small_launch<DMAX, WSMAX, 4>(la, a, device, st);
-        default: return small_launch<DMAX, WSMAX, 8>(la, a, device, st);
+        case 1: return small_launch<M, WSMAX, 1>(la, a, device, st);
+        case 2: return small_launch<M, WSMAX, 2>(la, a, device, st);
+        case 4: return small_launch<M, WSMAX, 4>(la, a, device, st);
+        default: return small_launch<M, WSMAX, 8>(la, a, device, st);
     }
 }
 
-bool small_eligible(const LocateArgs& la, const RefineArgs& a, int dmax, int wsmax) {
+// The default scheme's shapes (16 dims per curve, m = 8 raw / 16 lifted).
+bool small_eligible(const LocateArgs& la, const RefineArgs& a, bool dims16, int wsmax) {
     static const bool off = knob("HCG_NO_SMALL") != nullptr;  // A/B: locate + union + gather for every batch
-    return !off && a.dtype == HCG_U8 && la.dtype == HCG_U8 && a.nq >= 1 && a.nq <= kSmallBatch && a.pitch <= 128 &&
-           uint64_t(a.C) * a.take <= kSmallMaxWalk && dmax <= 16 && wsmax <= 4 && a.mode != kOutCandidates;
+    return !off && dims16 && (la.m == 8 || la.m == 16) && a.dtype == HCG_U8 && la.dtype == HCG_U8 && a.nq >= 1 &&
+           a.nq <= kSmallBatch && a.pitch <= 128 && uint64_t(a.C) * a.take <= kSmallMaxWalk && wsmax <= 4 &&
+           a.mode != kOutCandidates;
 }
 
-hcg_status launch_search_small(const LocateArgs& la, const RefineArgs& a, int dmax, int wsmax, int device,
-                               cudaStream_t st) {
-    if (dmax <= 8) {
+hcg_status launch_search_small(const LocateArgs& la, const RefineArgs& a, int wsmax, int device, cudaStream_t st) {
+    if (la.m == 8) {
         switch (wsmax) {
             case 1: return small_dispatch_r<8, 1>(la, a, device, st);
             case 2: return small_dispatch_r<8, 2>(la, a, device, st);

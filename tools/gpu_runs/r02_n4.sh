@@ -9,3 +9,5 @@ timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node=4 --mast
 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node=4 --master-addr 127.0.0.1 --master-port 29553 bench.py --gpus 4 --steps 10 --warmup 3 --n 50000000 --shard-depth 80 > gpurun_out/b_n4_proxy8.json 2> gpurun_out/b_n4_proxy8.err
 timeout 900 python tools/online_sweep.py --gpus 4 > gpurun_out/online_n4.jsonl 2> gpurun_out/online_n4.err
 tail -3 gpurun_out/t_n4.log; grep '^{' gpurun_out/sc10m_n4.log | cut -c1-300
+python tools/latency_probe.py > gpurun_out/latency_probe_v2.jsonl 2> gpurun_out/latency_probe_v2.err
+cat gpurun_out/latency_probe_v2.jsonl
