@@ -51,7 +51,8 @@ def parse():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--n", type=int, default=0, help="database rows (default 10M at N=1, 100M at N>1)")
+    p.add_argument("--rows", "--n", dest="n", type=int, default=0,
+                   help="database rows (default 10M at N=1, 100M at N>1); spell it --rows under torchrun")
     p.add_argument("--queries", type=int, default=100_000, help="queries per step")
     p.add_argument("--k", type=int, default=10)
     p.add_argument("--depth", type=int, default=350)

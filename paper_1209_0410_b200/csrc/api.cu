@@ -1134,7 +1134,19 @@ static hcg_status search_impl(const hcg_index* ix, const uint8_t* queries, uint3
             a.out_len = ol.dev;
             const LocateArgs la = locate_args(ix, dq, nq, depth, nullptr, nullptr, flag);
             if (!ms_out && small_eligible(la, a, ix->dims16, ix->wsmax)) {
+                static unsigned long long* prof = nullptr;  // phase stamps (tuning builds: HCG_SMALL_PROF)
+                if (knob("HCG_SMALL_PROF")) {
+                    if (!prof) cudaMalloc(&prof, 8 * 8);
+                    a.prof = prof;
+                }
                 HCG_TRY(launch_search_small(la, a, ix->wsmax, ix->device, st));
+                if (a.prof) {
+                    unsigned long long h[5];
+                    cudaMemcpyAsync(h, prof, 40, cudaMemcpyDeviceToHost, st);
+                    cudaStreamSynchronize(st);
+                    fprintf(stderr, "small-batch phases (ns): locate %llu union %llu gather %llu merge %llu\n",
+                            h[1] - h[0], h[2] - h[1], h[3] - h[2], h[4] - h[3]);
+                }
                 goto finish;
             }
         }

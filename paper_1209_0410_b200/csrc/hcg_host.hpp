@@ -100,7 +100,7 @@ struct RefineArgs {
     uint32_t* out_len;     // kOutIds: len; kOutCandidates: count
     uint64_t* out_packed;  // kOutPacked
     uint32_t cap;          // kOutCandidates
-    unsigned long long* prof;  // unused (kept zero)
+    unsigned long long* prof;  // k_search_small phase timestamps (tuning builds, HCG_SMALL_PROF); null otherwise
     cudaEvent_t ev_mid;        // optional: recorded between the union and gather launches
     uint64_t n_rows;           // rows in the index (bounds checks)
     int dtype;                 // hcg_dtype of rows and queries

@@ -717,7 +717,16 @@ __global__ void __launch_bounds__(kSmallThreads) k_search_small(LocateArgs la, R
     uint32_t* list = table + (1u << tb);                            // T
     __shared__ uint32_t count;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // phase timestamps of the first query (a.prof: tuning builds only)
+    auto stamp = [&](int i) {
+        if (a.prof && blockIdx.x == 0 && tid == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            a.prof[i] = t;
+        }
+    };
     for (uint32_t q = blockIdx.x; q < a.nq; q += gridDim.x) {
+        stamp(0);
         for (int i = tid; i < 256; i += kSmallThreads) lut[i] = la.lut[i];
         for (uint32_t i = tid; i <= tmask; i += kSmallThreads) table[i] = kEmpty;
         if (tid == 0) count = 0;
@@ -729,6 +738,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_search_small(LocateArgs la, R
             if (lane == 0) wptr[c] = a.slots[c] + b;
         }
         __syncthreads();
+        stamp(1);
         // 2. union: every thread loads its window entries first (independent
         // loads in flight together), then inserts them into the hash set
         uint32_t sl[JN];
@@ -768,6 +778,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_search_small(LocateArgs la, R
             }
         }
         __syncthreads();
+        stamp(2);
         // 3. gather + exact L2 + warp top-k over slices of the list; warp 0 merges
         const uint32_t n = count;
         uint4 qv[1];
@@ -778,6 +789,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_search_small(LocateArgs la, R
 #pragma unroll
         for (int r = 0; r < R; ++r) mbuf[warp * KCAP + lane * R + r] = tk.a[r];
         __syncthreads();
+        stamp(3);
         if (warp == 0) {
             WarpTopK<R> fin;
             fin.init(int(a.k));
@@ -786,6 +798,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_search_small(LocateArgs la, R
                 for (uint32_t i = 0; i < kr; i += 32) fin.offer(mbuf[w * KCAP + i + lane], lane);
             write_result<R>(a, q, fin, lane, n);
         }
+        stamp(4);
         __syncthreads();
     }
 }
