@@ -453,6 +453,10 @@ def run_ours(a):
                            "k_gather (gather of the unique candidate rows + exact L2 + top-k)"),
                 "algorithmic_bytes_per_launch": bytes_gather,
                 "launch_ms": round(gather_ms, 4),
+                # device time of the step's kernels (locate + batch order / union + refine), CUDA
+                # events on the launching stream; ms_per_step minus this is launch gaps + (N>1) the
+                # all-gather and merge
+                "kernel_ms_sum": round(statistics.median(tl) + union_ms + gather_ms, 4),
                 "other_kernels_ms": ({"k_locate": round(statistics.median(tl), 4),
                                       "batch_order_sort": round(union_ms, 4)} if unionless else
                                      {"k_locate": round(statistics.median(tl), 4), "k_union": round(union_ms, 4)}),
