@@ -321,10 +321,13 @@ struct WarpTopK {
     }
 
     // Offer one candidate per lane (kNone = no candidate).  Many passing
-    // offers (the fill phase of a large k) are sorted and merged in one go.
+    // offers (the fill phase of a large k) are sorted and merged in one go;
+    // BATCH1 extends that to R = 1 (the latency kernel: its warps each fill
+    // a fresh list from few passes).
+    template <bool BATCH1 = false>
     __device__ __forceinline__ void offer(uint64_t cand, int lane) {
         unsigned m = __ballot_sync(kFull, cand < thr);
-        if (R >= 2 && __popc(m) >= kTopkBatchMin) {
+        if ((R >= 2 || BATCH1) && __popc(m) >= kTopkBatchMin) {
             merge_sorted32<R>(a, warp_sort_asc(cand < thr ? cand : kNone, lane), lane);
             update_thr();
             return;

@@ -60,7 +60,9 @@ __device__ __forceinline__ int suffix_cmp(const uint64_t* e, const uint64_t (&qs
 // MFIX (8 or 16): every curve has exactly 16 dims and m = MFIX -- the key is
 // built by the compile-time d16 transform alone (a fraction of the generic
 // code: the latency kernel runs it from a cold instruction cache).
-template <int DMAX, int WSMAX, bool COOP, class T, int MFIX = 0>
+// SMEMIN: the query row and the assignment table sit in shared memory (plain
+// loads; __ldg is global-only).
+template <int DMAX, int WSMAX, bool COOP, class T, int MFIX = 0, bool SMEMIN = false>
 __device__ __forceinline__ uint64_t locate_one(const LocateArgs& a, const uint32_t* lut, uint32_t q, uint32_t c,
                                                int lane, uint64_t* rank_out) {
     constexpr int WMAX = DMAX / 2 > kMaxKeyWords ? kMaxKeyWords : (DMAX / 2 < 1 ? 1 : DMAX / 2);
@@ -71,7 +73,12 @@ __device__ __forceinline__ uint64_t locate_one(const LocateArgs& a, const uint32
     const T* row = reinterpret_cast<const T*>(a.queries + uint64_t(q) * a.pitch);
     const uint16_t* asg = a.assign + cv.off;
 #pragma unroll
-    for (int s = 0; s < DMAX; ++s) x[s] = s < d ? cell_of(__ldg(row + __ldg(asg + s)), lut, a.m, a.bad) : 0u;
+    for (int s = 0; s < DMAX; ++s) {
+        if constexpr (SMEMIN)
+            x[s] = s < d ? cell_of(row[asg[s]], lut, a.m, a.bad) : 0u;
+        else
+            x[s] = s < d ? cell_of(__ldg(row + __ldg(asg + s)), lut, a.m, a.bad) : 0u;
+    }
     uint64_t key[WMAX];
     if constexpr (MFIX != 0 && DMAX == 16 && WMAX >= 4)
         make_key_d16<MFIX, WMAX>(x, a.kind, key);
@@ -105,19 +112,32 @@ __device__ __forceinline__ uint64_t locate_one(const LocateArgs& a, const uint32
         const uint32_t wsu = uint32_t(ws);
         uint64_t lo = 0;
         if (COOP) {
-            uint64_t hi = a.n;  // the answer lies in [lo, hi]
-            while (hi - lo > 32) {
-                const uint64_t len = hi - lo;
-                const uint64_t sp = lo + ((uint64_t(lane) + 1) * len) / 33;  // strictly increasing, < hi
-                const unsigned b = __ballot_sync(kFull, suffix_cmp<WSMAX>(keys + sp * wsu, qs, ws) < 0);
-                const int cnt = __popc(b);
-                const uint64_t s_lo = __shfl_sync(kFull, sp, cnt > 0 ? cnt - 1 : 0);
-                const uint64_t s_hi = __shfl_sync(kFull, sp, cnt < 32 ? cnt : 31);
-                if (cnt > 0) lo = s_lo + 1;
-                if (cnt < 32) hi = s_hi;
+            // 32-ary lower bound of qs in arr[lo, hi)
+            auto coop = [&](const uint64_t* arr, uint64_t lo_, uint64_t hi) -> uint64_t {
+                while (hi - lo_ > 32) {
+                    const uint64_t len = hi - lo_;
+                    const uint64_t sp = lo_ + ((uint64_t(lane) + 1) * len) / 33;  // strictly increasing, < hi
+                    const unsigned b = __ballot_sync(kFull, suffix_cmp<WSMAX>(arr + sp * wsu, qs, ws) < 0);
+                    const int cnt = __popc(b);
+                    const uint64_t s_lo = __shfl_sync(kFull, sp, cnt > 0 ? cnt - 1 : 0);
+                    const uint64_t s_hi = __shfl_sync(kFull, sp, cnt < 32 ? cnt : 31);
+                    if (cnt > 0) lo_ = s_lo + 1;
+                    if (cnt < 32) hi = s_hi;
+                }
+                const bool less = lo_ + lane < hi && suffix_cmp<WSMAX>(arr + (lo_ + lane) * wsu, qs, ws) < 0;
+                return lo_ + __popc(__ballot_sync(kFull, less));
+            };
+            uint64_t hi = a.n;
+            if (cv.samples) {
+                // the sampled keys first (every S-th key; L2-resident under load),
+                // then the <= S keys between two samples: one dependent DRAM round
+                const uint64_t j = coop(cv.samples, 0, cv.n_samples);
+                const uint64_t S = cv.sample_stride;
+                lo = j == 0 ? 0 : (j - 1) * S + 1;
+                hi = j * S < a.n ? j * S : a.n;
+                if (hi < lo) hi = lo;
             }
-            const bool less = lo + lane < hi && suffix_cmp<WSMAX>(keys + (lo + lane) * wsu, qs, ws) < 0;
-            lo += __popc(__ballot_sync(kFull, less));
+            lo = coop(keys, lo, hi);
         } else {
             uint64_t len = a.n;
             if (cv.samples) {
@@ -459,6 +479,10 @@ __device__ __forceinline__ void gather_list(const RefineArgs& a, const uint32_t*
 #pragma unroll
         for (int r = 1; r < 8; ++r)
             if (r == l8) me = nx[r];
+        // latency path (shared-memory list, few passes): the id slot of every
+        // row is fetched with the rows instead of after the distance
+        uint32_t idpre = me;
+        if (SMEMLIST && a.idtab && me != kEmpty) idpre = __ldg(a.idtab + me);
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
             const uint32_t e = base + step + grp * 8 + r;
@@ -488,11 +512,13 @@ __device__ __forceinline__ void gather_list(const RefineArgs& a, const uint32_t*
         }
         const uint32_t S = (b0 ? s2[1] : s2[0]) + __shfl_xor_sync(kFull, b0 ? s2[0] : s2[1], 1);
         uint32_t sl = me;
-        if (a.idtab) {  // physical row -> id slot, read only for rows that can enter the top-k
+        if (SMEMLIST) {
+            sl = idpre;
+        } else if (a.idtab) {  // physical row -> id slot, read only for rows that can enter the top-k
             const bool pre = me != kEmpty && S <= uint32_t(tk.thr >> 32);
             if (__any_sync(kFull, pre) && pre) sl = __ldg(a.idtab + me);
         }
-        tk.offer(me != kEmpty ? ((uint64_t(S) << 32) | sl) : kNone, lane);
+        tk.template offer<SMEMLIST>(me != kEmpty ? ((uint64_t(S) << 32) | sl) : kNone, lane);
     }
 }
 
@@ -687,9 +713,11 @@ __global__ void __launch_bounds__(NW * 32) k_gather_cta(RefineArgs a, const uint
 //      (warp-aggregated) to a shared unique list;
 //   3. each warp gathers a slice of the list into its warp top-k (exact u32
 //      distances, (distance, id) order), warp 0 merges the NW lists.
-constexpr int kSmallThreads = 512;
+constexpr int kSmallThreads = 1024;
 constexpr uint32_t kSmallMaxWalk = 8192;
 constexpr uint32_t kSmallBatch = 128;
+constexpr uint32_t kSmallMaxCurves = 32;
+constexpr uint32_t kSmallMaxAssign = 512;
 
 __host__ __device__ __forceinline__ uint32_t small_table_bits(uint32_t T) {
     uint32_t tb = 5;
@@ -697,24 +725,29 @@ __host__ __device__ __forceinline__ uint32_t small_table_bits(uint32_t T) {
     return tb;
 }
 
+// mbuf (half the warps' lists) | CurveDev[C] | wptr[C] | assignment (u16) | query row | lut | table | list
 template <int R>
-__host__ __device__ __forceinline__ size_t small_smem_bytes(uint32_t C, uint32_t T) {
-    return size_t(kSmallThreads / 32) * 32 * R * 8 + size_t(C) * 8 + 256 * 4 + (size_t(4) << small_table_bits(T)) +
-           size_t(T) * 4;
+__host__ __device__ __forceinline__ size_t small_smem_bytes(uint32_t C, uint32_t T, uint32_t n_assign, uint32_t pitch) {
+    return size_t(kSmallThreads / 64) * 32 * R * 8 + size_t(C) * sizeof(CurveDev) + size_t(C) * 8 +
+           ((size_t(n_assign) * 2 + 15) & ~size_t(15)) + ((size_t(pitch) + 15) & ~size_t(15)) + 256 * 4 +
+           (size_t(4) << small_table_bits(T)) + size_t(T) * 4;
 }
 
 template <int M, int WSMAX, int R>
-__global__ void __launch_bounds__(kSmallThreads) k_search_small(LocateArgs la, RefineArgs a) {
+__global__ void __launch_bounds__(kSmallThreads) k_search_small(LocateArgs la, RefineArgs a, uint32_t n_assign) {
     constexpr int NW = kSmallThreads / 32;
     constexpr int KCAP = 32 * R;
     constexpr int JN = kSmallMaxWalk / kSmallThreads;  // window entries per thread
     extern __shared__ __align__(16) unsigned char ssm[];
-    uint64_t* mbuf = reinterpret_cast<uint64_t*>(ssm);              // NW x KCAP
-    const uint32_t** wptr = reinterpret_cast<const uint32_t**>(mbuf + NW * KCAP);  // C: slots[c] + begin
-    uint32_t* lut = reinterpret_cast<uint32_t*>(wptr + a.C);        // 256
+    uint64_t* mbuf = reinterpret_cast<uint64_t*>(ssm);                       // NW/2 x KCAP
+    CurveDev* scv = reinterpret_cast<CurveDev*>(mbuf + (NW / 2) * KCAP);      // C
+    const uint32_t** wptr = reinterpret_cast<const uint32_t**>(scv + a.C);   // C: slots[c] + begin
+    uint16_t* sasg = reinterpret_cast<uint16_t*>(wptr + a.C);                 // n_assign
+    uint8_t* sq = reinterpret_cast<uint8_t*>(sasg) + ((size_t(n_assign) * 2 + 15) & ~size_t(15));  // pitch
+    uint32_t* lut = reinterpret_cast<uint32_t*>(sq + ((a.pitch + 15) & ~15u));  // 256
     const uint32_t T = a.C * a.take, tb = small_table_bits(T), tmask = (1u << tb) - 1;
-    uint32_t* table = lut + 256;                                    // 1 << tb
-    uint32_t* list = table + (1u << tb);                            // T
+    uint32_t* table = lut + 256;                                            // 1 << tb
+    uint32_t* list = table + (1u << tb);                                    // T
     __shared__ uint32_t count;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     // phase timestamps of the first query (a.prof: tuning builds only)
@@ -725,16 +758,29 @@ __global__ void __launch_bounds__(kSmallThreads) k_search_small(LocateArgs la, R
             a.prof[i] = t;
         }
     };
+    // what the locate reads per curve, staged once: one round trip instead of a chain
+    {
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(la.curves);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(scv);
+        for (uint32_t i = tid; i < a.C * (sizeof(CurveDev) / 4); i += kSmallThreads) dst[i] = __ldg(src + i);
+        for (uint32_t i = tid; i < n_assign; i += kSmallThreads) sasg[i] = __ldg(la.assign + i);
+        for (int i = tid; i < 256; i += kSmallThreads) lut[i] = __ldg(la.lut + i);
+    }
+    LocateArgs ls = la;
+    ls.curves = scv;
+    ls.assign = sasg;
+    ls.queries = sq;
     for (uint32_t q = blockIdx.x; q < a.nq; q += gridDim.x) {
         stamp(0);
-        for (int i = tid; i < 256; i += kSmallThreads) lut[i] = la.lut[i];
+        for (uint32_t i = tid; i < (a.pitch >> 2); i += kSmallThreads)
+            reinterpret_cast<uint32_t*>(sq)[i] = __ldg(reinterpret_cast<const uint32_t*>(la.queries + uint64_t(q) * la.pitch) + i);
         for (uint32_t i = tid; i <= tmask; i += kSmallThreads) table[i] = kEmpty;
         if (tid == 0) count = 0;
         __syncthreads();
         // 1. locate: a warp per curve
         for (uint32_t c = warp; c < a.C; c += NW) {
             uint64_t rank;
-            const uint64_t b = locate_one<16, WSMAX, true, uint8_t, M>(la, lut, q, c, lane, &rank);
+            const uint64_t b = locate_one<16, WSMAX, true, uint8_t, M, true>(ls, lut, 0, c, lane, &rank);
             if (lane == 0) wptr[c] = a.slots[c] + b;
         }
         __syncthreads();
@@ -779,52 +825,64 @@ __global__ void __launch_bounds__(kSmallThreads) k_search_small(LocateArgs la, R
         }
         __syncthreads();
         stamp(2);
-        // 3. gather + exact L2 + warp top-k over slices of the list; warp 0 merges
+        // 3. gather + exact L2 + warp top-k over slices of the list
         const uint32_t n = count;
         uint4 qv[1];
-        load_query<1>(a, q, lane, qv);
+        {
+            const uint32_t ch = uint32_t(lane & 7);
+            qv[0] = ch < (a.pitch >> 4) ? reinterpret_cast<const uint4*>(sq)[ch] : make_uint4(0, 0, 0, 0);
+        }
         WarpTopK<R> tk;
         tk.init(int(a.k));
         gather_list<R, 1, true>(a, list, n, uint32_t(warp) * 32, NW * 32, qv, lane, tk);
-#pragma unroll
-        for (int r = 0; r < R; ++r) mbuf[warp * KCAP + lane * R + r] = tk.a[r];
-        __syncthreads();
         stamp(3);
-        if (warp == 0) {
-            WarpTopK<R> fin;
-            fin.init(int(a.k));
-            const uint32_t kr = (a.k + 31) & ~31u;
-            for (int w = 0; w < NW; ++w)
-                for (uint32_t i = 0; i < kr; i += 32) fin.offer(mbuf[w * KCAP + i + lane], lane);
-            write_result<R>(a, q, fin, lane, n);
+        // 4. tree merge of the warps' sorted lists: the upper half hands its
+        // lists to the lower half (shared memory), which merges them slice by
+        // slice (merge_sorted32 keeps the 32R smallest); log2(NW) rounds
+#pragma unroll 1
+        for (int half = NW / 2; half >= 1; half >>= 1) {
+            __syncthreads();
+            if (warp >= half && warp < 2 * half) {
+#pragma unroll
+                for (int r = 0; r < R; ++r) mbuf[(warp - half) * KCAP + lane * R + r] = tk.a[r];
+            }
+            __syncthreads();
+            if (warp < half) {
+#pragma unroll
+                for (int r = 0; r < R; ++r)  // slice r of the partner's list, ascending over the lanes
+                    merge_sorted32<R>(tk.a, mbuf[warp * KCAP + lane * R + r], lane);
+            }
         }
+        if (warp == 0) write_result<R>(a, q, tk, lane, n);
         stamp(4);
         __syncthreads();
     }
 }
 
 template <int M, int WSMAX, int R>
-hcg_status small_launch(const LocateArgs& la, const RefineArgs& a, int device, cudaStream_t st) {
+hcg_status small_launch(const LocateArgs& la, const RefineArgs& a, uint32_t n_assign, int device, cudaStream_t st) {
     auto kern = k_search_small<M, WSMAX, R>;
     static bool cfg[64] = {};
     if (!cfg[device & 63]) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(small_smem_bytes<R>(512, kSmallMaxWalk))) != cudaSuccess)
+                                 int(small_smem_bytes<R>(kSmallMaxCurves, kSmallMaxWalk, kSmallMaxAssign, 128))) !=
+            cudaSuccess)
             return set_error(HCG_ECUDA, "small-batch search: cannot opt in to dynamic shared memory");
         cfg[device & 63] = true;
     }
     count_launches(1);
-    kern<<<a.nq, kSmallThreads, small_smem_bytes<R>(a.C, a.C * a.take), st>>>(la, a);
+    kern<<<a.nq, kSmallThreads, small_smem_bytes<R>(a.C, a.C * a.take, n_assign, a.pitch), st>>>(la, a, n_assign);
     return check_launch("k_search_small");
 }
 
 template <int M, int WSMAX>
-hcg_status small_dispatch_r(const LocateArgs& la, const RefineArgs& a, int device, cudaStream_t st) {
+hcg_status small_dispatch_r(const LocateArgs& la, const RefineArgs& a, uint32_t n_assign, int device,
+                            cudaStream_t st) {
     switch (a.k <= 32 ? 1 : a.k <= 64 ? 2 : a.k <= 128 ? 4 : 8) {
-        case 1: return small_launch<M, WSMAX, 1>(la, a, device, st);
-        case 2: return small_launch<M, WSMAX, 2>(la, a, device, st);
-        case 4: return small_launch<M, WSMAX, 4>(la, a, device, st);
-        default: return small_launch<M, WSMAX, 8>(la, a, device, st);
+        case 1: return small_launch<M, WSMAX, 1>(la, a, n_assign, device, st);
+        case 2: return small_launch<M, WSMAX, 2>(la, a, n_assign, device, st);
+        case 4: return small_launch<M, WSMAX, 4>(la, a, n_assign, device, st);
+        default: return small_launch<M, WSMAX, 8>(la, a, n_assign, device, st);
     }
 }
 
@@ -833,21 +891,22 @@ bool small_eligible(const LocateArgs& la, const RefineArgs& a, bool dims16, int 
     static const bool off = knob("HCG_NO_SMALL") != nullptr;  // A/B: locate + union + gather for every batch
     return !off && dims16 && (la.m == 8 || la.m == 16) && a.dtype == HCG_U8 && la.dtype == HCG_U8 && a.nq >= 1 &&
            a.nq <= kSmallBatch && a.pitch <= 128 && uint64_t(a.C) * a.take <= kSmallMaxWalk && wsmax <= 4 &&
-           a.mode != kOutCandidates;
+           a.C <= kSmallMaxCurves && a.C * 16 <= kSmallMaxAssign && a.mode != kOutCandidates;
 }
 
 hcg_status launch_search_small(const LocateArgs& la, const RefineArgs& a, int wsmax, int device, cudaStream_t st) {
+    const uint32_t n_assign = a.C * 16;  // every curve has 16 dims here
     if (la.m == 8) {
         switch (wsmax) {
-            case 1: return small_dispatch_r<8, 1>(la, a, device, st);
-            case 2: return small_dispatch_r<8, 2>(la, a, device, st);
-            default: return small_dispatch_r<8, 4>(la, a, device, st);
+            case 1: return small_dispatch_r<8, 1>(la, a, n_assign, device, st);
+            case 2: return small_dispatch_r<8, 2>(la, a, n_assign, device, st);
+            default: return small_dispatch_r<8, 4>(la, a, n_assign, device, st);
         }
     }
     switch (wsmax) {
-        case 1: return small_dispatch_r<16, 1>(la, a, device, st);
-        case 2: return small_dispatch_r<16, 2>(la, a, device, st);
-        default: return small_dispatch_r<16, 4>(la, a, device, st);
+        case 1: return small_dispatch_r<16, 1>(la, a, n_assign, device, st);
+        case 2: return small_dispatch_r<16, 2>(la, a, n_assign, device, st);
+        default: return small_dispatch_r<16, 4>(la, a, n_assign, device, st);
     }
 }
 
