@@ -715,7 +715,7 @@ __global__ void __launch_bounds__(NW * 32) k_gather_cta(RefineArgs a, const uint
 //      distances, (distance, id) order), warp 0 merges the NW lists.
 constexpr int kSmallThreads = 1024;
 constexpr uint32_t kSmallMaxWalk = 8192;
-constexpr uint32_t kSmallBatch = 128;
+constexpr uint32_t kSmallBatch = 512;
 constexpr uint32_t kSmallMaxCurves = 32;
 constexpr uint32_t kSmallMaxAssign = 512;
 
