@@ -367,8 +367,12 @@ struct WarpTopK {
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const uint32_t idx = uint32_t(lane) * R + r;
-            if ((dmask >> r) & 1u) ++removed;
-            else wsm[idx - removed] = a[r];
+            if ((dmask >> r) & 1u) {
+                ++removed;
+            } else {
+                HCG_DASSERT(idx >= removed && idx - removed < N);
+                wsm[idx - removed] = a[r];
+            }
         }
 #pragma unroll
         for (int r = 0; r < R; ++r) {

@@ -781,6 +781,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_search_small(LocateArgs la, R
         for (uint32_t c = warp; c < a.C; c += NW) {
             uint64_t rank;
             const uint64_t b = locate_one<16, WSMAX, true, uint8_t, M, true>(ls, lut, 0, c, lane, &rank);
+            HCG_DASSERT(b + a.take <= a.n_rows);
             if (lane == 0) wptr[c] = a.slots[c] + b;
         }
         __syncthreads();
@@ -820,6 +821,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_search_small(LocateArgs la, R
                 uint32_t base = 0;
                 if (lane == leader) base = atomicAdd(&count, uint32_t(__popc(bal)));
                 base = __shfl_sync(kFull, base, leader);
+                HCG_DASSERT(!fresh || (base + __popc(bal & lanemask_lt_s()) < T && s < a.n_rows));
                 if (fresh) list[base + __popc(bal & lanemask_lt_s())] = s;
             }
         }

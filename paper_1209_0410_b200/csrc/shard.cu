@@ -8,8 +8,11 @@
 // truncated to k.
 //
 // Two ways to drive it:
-//   * one process, G GPUs (hcg_shard_group_build / _adopt): ncclCommInitAll,
-//     one stream per GPU, the merged result on the first GPU;
+//   * one process, G GPUs (hcg_shard_group_build / _adopt): one stream per
+//     GPU, the merged result on the first GPU; with NVLink peer access the
+//     exchange is fused into the search: every shard's kernel stores its
+//     packed top-k straight into the first GPU's gathered buffer (no
+//     collective, no copy); otherwise ncclCommInitAll + ncclAllGather;
 //   * one process per GPU (hcg_shard_group_join): ncclCommInitRank from an id
 //     the caller distributed (hcg_nccl_unique_id); every rank gets the result.
 //
@@ -147,6 +150,8 @@ struct hcg_shard_group {
     std::vector<cudaEvent_t> done;
     std::vector<DevBuf> dq, packed, gathered;
     cudaEvent_t ev_in = nullptr;  // on dev[0]: the caller's stream reached the search
+    cudaEvent_t merged = nullptr; // on dev[0]: the last merge has read the gathered lists
+    bool p2p = false;             // one process, every GPU writes into dev[0]'s memory over NVLink
     std::mutex mu;
 };
 
@@ -164,6 +169,7 @@ void destroy(hcg_shard_group* g) {
         if (r < g->done.size() && g->done[r]) cudaEventDestroy(g->done[r]);
         if (r < g->st.size() && g->st[r]) cudaStreamDestroy(g->st[r]);
         if (r == 0 && g->ev_in) cudaEventDestroy(g->ev_in);
+        if (r == 0 && g->merged) cudaEventDestroy(g->merged);
         if (g->own && r < g->ix.size() && g->ix[r]) hcg_free(g->ix[r]);
     }
     delete g;
@@ -182,6 +188,7 @@ hcg_status init_local(hcg_shard_group* g) {
         SG_CUDA(cudaStreamCreateWithFlags(&g->st[r], cudaStreamNonBlocking));
         SG_CUDA(cudaEventCreateWithFlags(&g->done[r], cudaEventDisableTiming));
         if (r == 0) SG_CUDA(cudaEventCreateWithFlags(&g->ev_in, cudaEventDisableTiming));
+        if (r == 0) SG_CUDA(cudaEventCreateWithFlags(&g->merged, cudaEventDisableTiming));
     }
     return HCG_OK;
 }
@@ -251,6 +258,24 @@ hcg_status hcg_shard_group_adopt(uint32_t G, hcg_index* const* shards, hcg_shard
     if (rc == HCG_OK) {
         g->comm.assign(G, nullptr);
         rc = nccl_check(nccl().CommInitAll(g->comm.data(), int(G), g->dev.data()), "ncclCommInitAll");
+    }
+    // Fused exchange: when every GPU can write the first GPU's memory (NVLink
+    // peers), each shard's search kernel stores its packed top-k straight
+    // into the first GPU's gathered buffer -- the transfer happens in the
+    // producing kernel's epilogue, no collective and no copy.
+    if (rc == HCG_OK && G > 1 && !knob("HCG_SHARD_NCCL")) {
+        bool ok = true;
+        for (uint32_t r = 1; r < G && ok; ++r) {
+            int can = 0;
+            ok = cudaDeviceCanAccessPeer(&can, g->dev[r], g->dev[0]) == cudaSuccess && can;
+            if (ok) {
+                SetDev sd(g->dev[r]);
+                const cudaError_t e = cudaDeviceEnablePeerAccess(g->dev[0], 0);
+                ok = e == cudaSuccess || e == cudaErrorPeerAccessAlreadyEnabled;
+            }
+            cudaGetLastError();
+        }
+        g->p2p = ok;
     }
     if (rc != HCG_OK) {
         g->own = false;  // the caller keeps its shards on failure
@@ -356,6 +381,10 @@ hcg_status hcg_shard_group_search(hcg_shard_group* g, const uint8_t* queries, ui
         SetDev sd(g->dev[0]);
         SG_CUDA(cudaEventRecord(g->ev_in, caller));
     }
+    if (g->p2p) {
+        SetDev sd(g->dev[0]);
+        HCG_RET_IF(g->gathered[0].reserve(pbytes * g->G));
+    }
     // every shard answers the whole batch at the per-shard depth (IHLS)
     for (size_t r = 0; r < L; ++r) {
         SetDev sd(g->dev[r]);
@@ -366,25 +395,43 @@ hcg_status hcg_shard_group_search(hcg_shard_group* g, const uint8_t* queries, ui
             SG_CUDA(cudaMemcpyAsync(g->dq[r].p, queries, qbytes, cudaMemcpyDefault, g->st[r]));
             qr = static_cast<const uint8_t*>(g->dq[r].p);
         }
-        HCG_RET_IF(g->packed[r].reserve(pbytes));
-        HCG_RET_IF(g->gathered[r].reserve(pbytes * g->G));
-        HCG_RET_IF(hcg_search_packed(g->ix[r], qr, nq, k, shard_depth, static_cast<uint64_t*>(g->packed[r].p),
-                                     g->st[r]));
+        uint64_t* out = nullptr;
+        if (g->p2p) {
+            // straight into slice r of the first GPU's gathered lists (NVLink
+            // stores from the search kernel), after the last merge read them
+            SG_CUDA(cudaStreamWaitEvent(g->st[r], g->merged, 0));
+            out = static_cast<uint64_t*>(g->gathered[0].p) + r * size_t(nq) * k;
+        } else {
+            HCG_RET_IF(g->packed[r].reserve(pbytes));
+            HCG_RET_IF(g->gathered[r].reserve(pbytes * g->G));
+            out = static_cast<uint64_t*>(g->packed[r].p);
+        }
+        HCG_RET_IF(hcg_search_packed(g->ix[r], qr, nq, k, shard_depth, out, g->st[r]));
     }
-    // aggregate: all-gather the packed top-k lists (B x k x 8 bytes per shard)
-    HCG_RET_IF(nccl_check(nccl().GroupStart(), "ncclGroupStart"));
-    ncclResult_t nr = ncclSuccess;
-    for (size_t r = 0; r < L && nr == ncclSuccess; ++r) {
-        SetDev sd(g->dev[r]);
-        nr = nccl().AllGather(g->packed[r].p, g->gathered[r].p, size_t(nq) * k, ncclUint64, g->comm[r], g->st[r]);
+    if (g->p2p) {
+        for (size_t r = 1; r < L; ++r) {
+            SetDev sd(g->dev[r]);
+            SG_CUDA(cudaEventRecord(g->done[r], g->st[r]));
+        }
+        SetDev sd(g->dev[0]);
+        for (size_t r = 1; r < L; ++r) SG_CUDA(cudaStreamWaitEvent(g->st[0], g->done[r], 0));
+    } else {
+        // aggregate: all-gather the packed top-k lists (B x k x 8 bytes per shard)
+        HCG_RET_IF(nccl_check(nccl().GroupStart(), "ncclGroupStart"));
+        ncclResult_t nr = ncclSuccess;
+        for (size_t r = 0; r < L && nr == ncclSuccess; ++r) {
+            SetDev sd(g->dev[r]);
+            nr = nccl().AllGather(g->packed[r].p, g->gathered[r].p, size_t(nq) * k, ncclUint64, g->comm[r], g->st[r]);
+        }
+        const ncclResult_t ne = nccl().GroupEnd();
+        HCG_RET_IF(nccl_check(nr, "ncclAllGather"));
+        HCG_RET_IF(nccl_check(ne, "ncclGroupEnd"));
     }
-    const ncclResult_t ne = nccl().GroupEnd();
-    HCG_RET_IF(nccl_check(nr, "ncclAllGather"));
-    HCG_RET_IF(nccl_check(ne, "ncclGroupEnd"));
     // K4 on the first local GPU (every rank, in per-process mode)
     SetDev sd(g->dev[0]);
     HCG_RET_IF(hcg_merge_packed(static_cast<const uint64_t*>(g->gathered[0].p), g->G, nq, k, out_ids, out_sqdist,
                                 out_len, g->dev[0], g->st[0]));
+    SG_CUDA(cudaEventRecord(g->merged, g->st[0]));
     for (size_t r = 0; r < L; ++r) {
         SetDev sd2(g->dev[r]);
         SG_CUDA(cudaEventRecord(g->done[r], g->st[r]));
