@@ -198,13 +198,16 @@ __global__ void __launch_bounds__(128, MINB) k_locate(LocateArgs a) {
     }
 }
 
+#ifndef HCG_LOCATE_MINB
+#define HCG_LOCATE_MINB 8
+#endif
 template <int DMAX, int WSMAX, class T>
 static void locate_launch_t(const LocateArgs& a, cudaStream_t st) {
     const uint64_t total = uint64_t(a.nq) * a.C;
     if (total <= 1024)  // small batches: a warp per (query, curve), ~5 dependent loads
         k_locate<DMAX, WSMAX, true, 1, T><<<unsigned((total * 32 + 127) / 128), 128, 0, st>>>(a);
     else  // 8 CTAs/SM: measured 3 % faster than the 88-register default
-        k_locate<DMAX, WSMAX, false, (DMAX <= 16 ? 8 : 1), T><<<unsigned((total + 127) / 128), 128, 0, st>>>(a);
+        k_locate<DMAX, WSMAX, false, (DMAX <= 16 ? HCG_LOCATE_MINB : 1), T><<<unsigned((total + 127) / 128), 128, 0, st>>>(a);
 }
 
 template <int DMAX, int WSMAX>

@@ -19,7 +19,7 @@
 //
 // A batch is H2D (pinned / registered host queries -> the slot's device
 // buffer, copy stream) -> search (compute stream; one index, or a shard group:
-// per-GPU search + NCCL all-gather + merge) -> D2H (results -> host, copy
+// per-GPU search + exchange + merge) -> D2H (results -> host, copy
 // stream); events order slot reuse, so batch b+1's upload and batch b-1's
 // download overlap batch b's search.  A query's response time runs from its
 // arrival to the moment its results are in host memory (the CUDA event after
@@ -237,7 +237,6 @@ struct HostPin {
 void worker_loop(hcg_server* s) {
     cudaSetDevice(s->device);
     uint64_t head = 0;  // first query not yet dispatched
-    std::vector<double> next_wait;
     while (true) {
         // retire finished batches
         for (uint32_t si = 0; si < s->slots.size(); ++si) {

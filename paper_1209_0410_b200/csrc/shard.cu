@@ -396,17 +396,22 @@ hcg_status hcg_shard_group_search(hcg_shard_group* g, const uint8_t* queries, ui
             qr = static_cast<const uint8_t*>(g->dq[r].p);
         }
         uint64_t* out = nullptr;
+        uint64_t* slice = nullptr;
         if (g->p2p) {
             // straight into slice r of the first GPU's gathered lists (NVLink
             // stores from the search kernel), after the last merge read them
             SG_CUDA(cudaStreamWaitEvent(g->st[r], g->merged, 0));
-            out = static_cast<uint64_t*>(g->gathered[0].p) + r * size_t(nq) * k;
-        } else {
+            slice = static_cast<uint64_t*>(g->gathered[0].p) + r * size_t(nq) * k;
+            out = slice;
+        }
+        if (!out || hcg_size(g->ix[r]) == 0) {  // NCCL path, or an empty shard (padding written locally)
             HCG_RET_IF(g->packed[r].reserve(pbytes));
-            HCG_RET_IF(g->gathered[r].reserve(pbytes * g->G));
+            if (!g->p2p) HCG_RET_IF(g->gathered[r].reserve(pbytes * g->G));
             out = static_cast<uint64_t*>(g->packed[r].p);
         }
         HCG_RET_IF(hcg_search_packed(g->ix[r], qr, nq, k, shard_depth, out, g->st[r]));
+        if (slice && out != slice)
+            SG_CUDA(cudaMemcpyPeerAsync(slice, g->dev[0], out, g->dev[r], pbytes, g->st[r]));
     }
     if (g->p2p) {
         for (size_t r = 1; r < L; ++r) {
