@@ -921,27 +921,23 @@ hcg_status launch_search_small(const LocateArgs& la, const RefineArgs& a, int ws
 // acc += (double(a_i) - double(b_i))^2, each subtract, multiply and add
 // rounded on its own (no FMA contraction) -- the same double, bit for bit,
 // so ids and (distance, id) tie order match the reference by construction.
-// A sequential sum needs one lane per row: a warp stages 32 rows (lane =
-// 16-B chunk, coalesced cp.async) into its shared-memory tile, chunk c of row
-// r at chunk position c ^ (r & 7) so that the 8 lanes of an LDS.128 phase hit
-// distinct banks, then lane r sums row r in index order and offers
-// (double bits, slot) to the pair top-k.  Padding components are zero on both
-// sides and add exact zeros.
+// A sequential sum needs one lane per row: each pass a warp takes 32 rows,
+// lane r streams row r through registers (16 floats at a time, loads issued
+// ahead of their terms) against the query held as doubles in shared memory,
+// and offers (double bits, slot) to the pair top-k.  Padding components are
+// zero on both sides and add exact zeros.  The sums are FP64-latency chains:
+// occupancy (no tile in shared memory) is what hides them -- a 32-row
+// shared-memory tile per warp ran 39 ms per 100K queries at 12 warps / SM,
+// double-buffered (6 warps / SM) 70 ms.
 constexpr uint32_t kF32Rows = 32;  // rows per warp pass (one per lane)
 
-__device__ __forceinline__ uint32_t f32_tile_stride(uint32_t pitch) { return (pitch + 127u) & ~127u; }
-// Shared bytes per warp: the 32-row tile + the query row.
-__host__ __device__ __forceinline__ uint32_t f32_warp_smem(uint32_t pitch) {
-    return kF32Rows * ((pitch + 127u) & ~127u) + pitch;
-}
+constexpr int kF32Threads = 256;  // k_gather_f32
+constexpr int kF32CtaWarps = 8;   // k_gather_cta_f32 / k_brute_f32
+// Shared bytes per warp: the query row as doubles (converted once per query).
+__host__ __device__ __forceinline__ uint32_t f32_warp_smem(uint32_t pitch) { return 2 * pitch; }
 
-__device__ __forceinline__ void cp_async16(void* smem_dst, const void* src) {
-    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst));
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
-}
-
-__device__ __forceinline__ double sq_term(float a, float b) {
-    const double d = __dsub_rn(double(a), double(b));
+__device__ __forceinline__ double sq_term(float a, double b) {
+    const double d = __dsub_rn(double(a), b);
     return __dmul_rn(d, d);
 }
 
@@ -951,12 +947,14 @@ __device__ __forceinline__ uint32_t f32_entry(const uint32_t* list, uint32_t e, 
     return e < n ? __ldcg(list + e) : kEmpty;
 }
 
-// Query row q -> the warp's query buffer (qs, pitch bytes).
+// Query row q -> the warp's query buffer (qs: pitch / 4 doubles, converted
+// once per query instead of once per candidate row).
 __device__ __forceinline__ void stage_query_f32(const uint8_t* queries, uint32_t pitch, uint32_t q, uint8_t* qs,
                                                 int lane) {
     __syncwarp();  // the previous query's reads are done
-    for (uint32_t c = lane; c < (pitch >> 4); c += 32)
-        *reinterpret_cast<uint4*>(qs + c * 16) = *reinterpret_cast<const uint4*>(queries + uint64_t(q) * pitch + c * 16);
+    const float* src = reinterpret_cast<const float*>(queries + uint64_t(q) * pitch);
+    double* dst = reinterpret_cast<double*>(qs);
+    for (uint32_t i = lane; i < (pitch >> 2); i += 32) dst[i] = double(src[i]);
     __syncwarp();
 }
 
@@ -964,35 +962,35 @@ __device__ __forceinline__ void stage_query_f32(const uint8_t* queries, uint32_t
 // the entries are the row slots themselves, i.e. rows [start, n)).
 template <int R, bool DIRECT>
 __device__ __forceinline__ void gather_list_f32(const uint8_t* rows, uint32_t pitch, const uint32_t* list, uint32_t n,
-                                                uint32_t start, uint32_t step, const uint8_t* qs, uint8_t* tile,
+                                                uint32_t start, uint32_t step, const uint8_t* qs, uint8_t*,
                                                 int lane, WarpTopK2<R>& tk, const uint32_t* idtab) {
-    const uint32_t chunks = pitch >> 4, rstride = f32_tile_stride(pitch);
-    const uint8_t* mine_row = tile + uint32_t(lane) * rstride;
-    const uint32_t swz = uint32_t(lane) & 7;
+    const uint32_t chunks = pitch >> 4;
+    const double2* qd = reinterpret_cast<const double2*>(qs);
     for (uint32_t base = start; base < n; base += step) {
         const uint32_t me = f32_entry<DIRECT>(list, base + lane, n);
-#pragma unroll 4
-        for (int r = 0; r < int(kF32Rows); ++r) {
-            const uint32_t row = __shfl_sync(kFull, me, r);
-            if (row != kEmpty)
-                for (uint32_t c = lane; c < chunks; c += 32)
-                    cp_async16(tile + r * rstride + ((c ^ (r & 7)) << 4), rows + uint64_t(row) * pitch + c * 16);
-        }
-        cp_async_commit();
-        cp_async_wait_all();
-        __syncwarp();
         double acc = 0.0;
         if (me != kEmpty) {
-            for (uint32_t c = 0; c < chunks; ++c) {
-                const float4 v = *reinterpret_cast<const float4*>(mine_row + ((c ^ swz) << 4));
-                const float4 q = *reinterpret_cast<const float4*>(qs + (c << 4));
-                acc = __dadd_rn(acc, sq_term(v.x, q.x));
-                acc = __dadd_rn(acc, sq_term(v.y, q.y));
-                acc = __dadd_rn(acc, sq_term(v.z, q.z));
-                acc = __dadd_rn(acc, sq_term(v.w, q.w));
+            // lane = row: the row streams through registers 4 chunks (16
+            // floats) at a time, the loads of a group issued before its terms
+            const float4* src = reinterpret_cast<const float4*>(rows + uint64_t(me) * pitch);
+            for (uint32_t c0 = 0; c0 < chunks; c0 += 4) {
+                float4 v[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    v[u] = c0 + u < chunks ? __ldg(src + c0 + u) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const uint32_t c = c0 + u;
+                    if (c < chunks) {
+                        const double2 q01 = qd[2 * c], q23 = qd[2 * c + 1];
+                        acc = __dadd_rn(acc, sq_term(v[u].x, q01.x));
+                        acc = __dadd_rn(acc, sq_term(v[u].y, q01.y));
+                        acc = __dadd_rn(acc, sq_term(v[u].z, q23.x));
+                        acc = __dadd_rn(acc, sq_term(v[u].w, q23.y));
+                    }
+                }
             }
         }
-        __syncwarp();  // tile reads done before the next pass overwrites it
         const uint64_t sb = uint64_t(__double_as_longlong(acc));
         uint32_t sl = me;
         if (idtab) {  // physical row -> id slot for rows that can enter the top-k
@@ -1020,16 +1018,15 @@ __device__ __forceinline__ void write_result_f32(const RefineArgs& a, uint32_t q
 }
 
 template <int R>
-__global__ void __launch_bounds__(kRefineThreads) k_gather_f32(RefineArgs a, const uint32_t* __restrict__ lists,
-                                                               const uint32_t* __restrict__ counts,
-                                                               uint32_t lstride) {
+__global__ void __launch_bounds__(kF32Threads) k_gather_f32(RefineArgs a, const uint32_t* __restrict__ lists,
+                                                            const uint32_t* __restrict__ counts,
+                                                            uint32_t lstride) {
     extern __shared__ __align__(128) uint8_t f32_smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t rstride = f32_tile_stride(a.pitch);
-    uint8_t* tile = f32_smem + warp * f32_warp_smem(a.pitch);
-    uint8_t* qs = tile + kF32Rows * rstride;
-    const uint32_t qstep = gridDim.x * (kRefineThreads / 32);
-    for (uint32_t q = (blockIdx.x * kRefineThreads + threadIdx.x) >> 5; q < a.nq; q += qstep) {
+    uint8_t* tile = nullptr;
+    uint8_t* qs = f32_smem + warp * f32_warp_smem(a.pitch);
+    const uint32_t qstep = gridDim.x * (kF32Threads / 32);
+    for (uint32_t q = (blockIdx.x * kF32Threads + threadIdx.x) >> 5; q < a.nq; q += qstep) {
         const uint32_t n = __ldcg(counts + q);
         const uint32_t qq = a.qorder ? __ldg(a.qorder + q) : q;  // list q holds query qq
         stage_query_f32(a.queries, a.pitch, qq, qs, lane);
@@ -1067,9 +1064,8 @@ __global__ void __launch_bounds__(NW * 32) k_gather_cta_f32(RefineArgs a, const 
     __shared__ uint64_t ma[NW * 32 * R];
     __shared__ uint32_t mb[NW * 32 * R];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t rstride = f32_tile_stride(a.pitch);
-    uint8_t* tile = f32_smem + warp * f32_warp_smem(a.pitch);
-    uint8_t* qs = tile + kF32Rows * rstride;
+    uint8_t* tile = nullptr;
+    uint8_t* qs = f32_smem + warp * f32_warp_smem(a.pitch);
     for (uint32_t q = blockIdx.x; q < a.nq; q += gridDim.x) {
         const uint32_t n = __ldcg(counts + q);
         const uint32_t qq = a.qorder ? __ldg(a.qorder + q) : q;
@@ -1096,17 +1092,18 @@ hcg_status gather_f32_launch(const RefineArgs& a, const uint32_t* lists, const u
                              int sms, cudaStream_t st) {
     const size_t wsm = f32_warp_smem(a.pitch);
     if (a.nq * 2 < uint32_t(sms) * 16 * 8) {
-        auto kern = k_gather_cta_f32<R, 8>;
-        HCG_RET_IF(f32_smem_opt_in(kern, 8 * wsm));
-        kern<<<a.nq, 256, 8 * wsm, st>>>(a, lists, counts, lstride);
+        auto kern = k_gather_cta_f32<R, kF32CtaWarps>;
+        HCG_RET_IF(f32_smem_opt_in(kern, kF32CtaWarps * wsm));
+        kern<<<a.nq, kF32CtaWarps * 32, kF32CtaWarps * wsm, st>>>(a, lists, counts, lstride);
         return check_launch("k_gather_cta_f32");
     }
+    constexpr int W = kF32Threads / 32;
     auto kern = k_gather_f32<R>;
-    HCG_RET_IF(f32_smem_opt_in(kern, 8 * wsm));
+    HCG_RET_IF(f32_smem_opt_in(kern, W * wsm));
     int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRefineThreads, 8 * wsm);
-    const uint32_t blocks = std::min<uint32_t>((a.nq + 7) / 8, uint32_t(sms) * uint32_t(std::max(per_sm, 1)));
-    kern<<<blocks, kRefineThreads, 8 * wsm, st>>>(a, lists, counts, lstride);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kF32Threads, W * wsm);
+    const uint32_t blocks = std::min<uint32_t>((a.nq + W - 1) / W, uint32_t(sms) * uint32_t(std::max(per_sm, 1)));
+    kern<<<blocks, kF32Threads, W * wsm, st>>>(a, lists, counts, lstride);
     return check_launch("k_gather_f32");
 }
 
@@ -1843,14 +1840,14 @@ static hcg_status brute_launch(const BruteArgs& a, uint64_t* scratch, cudaStream
 // f32 rows: warp per (query, chunk of rows) through the exact gather path,
 // then a pair merge over the chunks.  Scratch: chunks x nq x k (u64 key, u32 slot).
 template <int R>
-__global__ void __launch_bounds__(256) k_brute_f32(BruteArgs a, uint64_t* __restrict__ part_a,
-                                                   uint32_t* __restrict__ part_b) {
+__global__ void __launch_bounds__(kF32CtaWarps * 32) k_brute_f32(BruteArgs a, uint64_t* __restrict__ part_a,
+                                                                 uint32_t* __restrict__ part_b) {
     extern __shared__ __align__(128) uint8_t f32_smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t chunk = blockIdx.x, q = blockIdx.y * 8 + warp;
+    const uint32_t chunk = blockIdx.x, q = blockIdx.y * kF32CtaWarps + warp;
     if (q >= a.nq) return;
-    uint8_t* tile = f32_smem + warp * f32_warp_smem(a.pitch);
-    uint8_t* qs = tile + kF32Rows * f32_tile_stride(a.pitch);
+    uint8_t* tile = nullptr;
+    uint8_t* qs = f32_smem + warp * f32_warp_smem(a.pitch);
     const uint64_t r0 = uint64_t(chunk) * kBruteChunk;
     const uint32_t r1 = uint32_t(min(a.n, r0 + kBruteChunk));
     stage_query_f32(a.queries, a.pitch, q, qs, lane);
@@ -1907,9 +1904,9 @@ static hcg_status brute_f32_launch(const BruteArgs& a, uint64_t* scratch, uint64
     const uint32_t chunks = uint32_t((a.n + kBruteChunk - 1) / kBruteChunk);
     uint64_t* pa = scratch;
     uint32_t* pb = reinterpret_cast<uint32_t*>(scratch + uint64_t(chunks) * a.nq * a.k);
-    const size_t smem = 8 * size_t(f32_warp_smem(a.pitch));
+    const size_t smem = kF32CtaWarps * size_t(f32_warp_smem(a.pitch));
     HCG_RET_IF(f32_smem_opt_in(k_brute_f32<R>, smem));
-    k_brute_f32<R><<<dim3(chunks, (a.nq + 7) / 8), 256, smem, st>>>(a, pa, pb);
+    k_brute_f32<R><<<dim3(chunks, (a.nq + kF32CtaWarps - 1) / kF32CtaWarps), kF32CtaWarps * 32, smem, st>>>(a, pa, pb);
     HCG_RET_IF(check_launch("k_brute_f32"));
     k_merge_f32<R><<<unsigned((uint64_t(a.nq) * 32 + 255) / 256), 256, 0, st>>>(pa, pb, chunks, a, out_ids, out_sq,
                                                                                  out_len);
