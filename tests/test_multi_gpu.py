@@ -54,3 +54,29 @@ def test_cpp_shard_group_single_process():
     out = subprocess.run([binp], capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
     assert "shard group ok" in out.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not gpu_available() or _ngpus() < 2, reason="needs >= 2 GPUs")
+def test_one_process_group_with_empty_shards():
+    """Fewer rows than GPUs: the empty shards' padding still reaches GPU 0 (the
+    fused exchange writes it locally and copies it over), and the merge equals
+    the sharded oracle."""
+    import numpy as np
+    import paper_1209_0410_b200 as H
+    from oracle import pyoracle as P
+    from paper_1209_0410_b200.sharded import ShardGroup
+    G = min(_ngpus(), 4)
+    for n in (1, G - 1, G + 1):
+        rows = P.gen_rows(0, n)
+        qs = P.gen_queries(0, 7, max(n, 1))
+        grp = ShardGroup.build(rows, H.default_scheme(128, 8, 16), H.LIFTED, list(range(G)))
+        for nq in (7, 3):  # the small-batch kernel and a resized exchange buffer
+            ids, sq, ln = grp.search(qs[:nq], 5, 64)
+            oids, odist, oln = P.sharded_search(H.LIFTED.floats(rows), H.LIFTED.floats(qs[:nq]), G, 8, 16, 5, 64)
+            np.testing.assert_array_equal(ln, oln)
+            for q in range(nq):
+                L = int(oln[q])
+                np.testing.assert_array_equal(ids[q, :L], oids[q, :L])
+                assert (np.sqrt(sq[q, :L].astype(np.float64)) / 256.0).tobytes() == odist[q, :L].tobytes()
+        grp.close()
