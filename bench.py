@@ -240,8 +240,21 @@ def run_ours(a):
            torch.empty((Q, k), dtype=torch.uint32, device=dev),
            torch.empty((Q,), dtype=torch.uint32, device=dev))
 
+    # N>1: the aggregate is routed (route_to_aggregator):
+    # each rank merges the partials of its own 1/N block of the batch, so the
+    # box's ranks together hold every query's global top-k
+    routed = world > 1
+    block = [0, Q]
+
+    def search_step(q, out_):
+        if routed:
+            _, block[0], block[1] = sidx.shard_group.search_routed(q, k, shard_depth, out=out_)
+            return block[0], block[0] + block[1]
+        sidx.search(q, k, shard_depth, out=out_)
+        return 0, int(q.shape[0])
+
     def step(b):
-        sidx.search(batches[b], k, shard_depth, out=out)
+        search_step(batches[b], out)
 
     launches = [0]  # our kernels launched inside the timed region (libhcg's counter)
 
@@ -279,7 +292,7 @@ def run_ours(a):
     host_outs = [(torch.empty((Q, k), dtype=torch.uint64).pin_memory(),
                   torch.empty((Q, k), dtype=torch.uint32).pin_memory(),
                   torch.empty((Q,), dtype=torch.uint32).pin_memory()) for _ in range(2)]
-    pipe = HostPipeline(lambda q, out: sidx.search(q, k, shard_depth, out=out), k, Q, device=local)
+    pipe = HostPipeline(search_step, k, Q, device=local)
     pipe.run(host_batches[:a.warmup], [host_outs[b % 2] for b in range(a.warmup)])
     if world > 1:
         dist.barrier()
@@ -294,7 +307,8 @@ def run_ours(a):
         ms_e2e = float(t.item())
     clocks.stop()
     h2d = Q * 128
-    d2h = Q * k * 8 + Q * k * 4 + Q * 4
+    rows_back = block[1] if routed else Q  # each rank reads back the rows it aggregated
+    d2h = rows_back * (k * 8 + k * 4 + 4)
 
     # dominant-kernel roofline (outside the timed region): per-launch device
     # times of locate / candidate union / gather+score, CUDA events on `stream`.

@@ -287,6 +287,18 @@ hcg_status hcg_shard_group_search(hcg_shard_group* group, const uint8_t* queries
                                   uint32_t shard_depth, uint64_t* out_ids, uint32_t* out_sqdist, uint32_t* out_len,
                                   void* stream);
 
+/* The aggregate routed to one aggregator per query (route_to_aggregator,
+ * SPEC.md:375-383): in per-process mode rank p receives every shard's
+ * partials of the query block [nq*p/G, nq*(p+1)/G) only (NCCL send / recv:
+ * 1/G of an all-gather's bytes and of the merge) and writes those rows of the
+ * outputs (nq-row buffers); *block_first / *block_count name the block.  In
+ * one process (all shards local) it is hcg_shard_group_search (block = all).
+ * Collective. */
+hcg_status hcg_shard_group_search_routed(hcg_shard_group* group, const uint8_t* queries, uint32_t nq, uint32_t k,
+                                         uint32_t shard_depth, uint64_t* out_ids, uint32_t* out_sqdist,
+                                         uint32_t* out_len, void* stream, uint32_t* block_first,
+                                         uint32_t* block_count);
+
 /* CUDA device of the group's first local shard (where results land) and the
  * descriptor length. */
 int hcg_shard_group_device(const hcg_shard_group* group);

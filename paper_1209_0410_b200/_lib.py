@@ -42,6 +42,7 @@ EXPORTS = [
     "hcg_shard_group_free", "hcg_shard_group_shards", "hcg_shard_group_search", "hcg_index_device", "hcg_index_ids",
     "hcg_shard_group_device", "hcg_shard_group_dims", "hcg_server_create", "hcg_server_free", "hcg_server_replay",
     "hcg_server_start", "hcg_server_submit", "hcg_server_wait", "hcg_refine_unionless",
+    "hcg_shard_group_search_routed",
 ]
 
 
@@ -151,6 +152,7 @@ def lib() -> C.CDLL:
     L.hcg_shard_group_shards.restype = u32
     L.hcg_shard_group_shards.argtypes = [vp]
     L.hcg_shard_group_search.argtypes = [vp, vp, u32, u32, u32, vp, vp, vp, vp]
+    L.hcg_shard_group_search_routed.argtypes = [vp, vp, u32, u32, u32, vp, vp, vp, vp, P(u32), P(u32)]
     L.hcg_index_device.restype = C.c_int
     L.hcg_index_device.argtypes = [vp]
     L.hcg_index_ids.argtypes = [vp, P(u64), P(u64)]
@@ -172,7 +174,7 @@ def lib() -> C.CDLL:
                  "hcg_describe", "hcg_gen_rows", "hcg_gen_queries", "hcg_insert",
                  "hcg_save", "hcg_load", "hcg_read_vectors", "hcg_write_vectors", "hcg_nccl_unique_id",
                  "hcg_shard_group_build", "hcg_shard_group_adopt", "hcg_shard_group_join", "hcg_shard_group_free",
-                 "hcg_shard_group_search", "hcg_index_ids", "hcg_server_create", "hcg_server_free",
+                 "hcg_shard_group_search", "hcg_shard_group_search_routed", "hcg_index_ids", "hcg_server_create", "hcg_server_free",
                  "hcg_server_replay", "hcg_server_start", "hcg_server_submit", "hcg_server_wait"):
         getattr(L, name).restype = C.c_int
     del u8

@@ -41,6 +41,8 @@ struct NcclApi {
     ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
     ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*GroupStart)() = nullptr;
     ncclResult_t (*GroupEnd)() = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
@@ -70,6 +72,8 @@ NcclApi& nccl() {
         sym(api.CommInitRank, "ncclCommInitRank");
         sym(api.CommDestroy, "ncclCommDestroy");
         sym(api.AllGather, "ncclAllGather");
+        sym(api.Send, "ncclSend");
+        sym(api.Recv, "ncclRecv");
         sym(api.GroupStart, "ncclGroupStart");
         sym(api.GroupEnd, "ncclGroupEnd");
         sym(api.GetErrorString, "ncclGetErrorString");
@@ -443,6 +447,60 @@ hcg_status hcg_shard_group_search(hcg_shard_group* g, const uint8_t* queries, ui
     }
     SetDev sd3(g->dev[0]);
     for (size_t r = 0; r < L; ++r) SG_CUDA(cudaStreamWaitEvent(caller, g->done[r], 0));
+    return HCG_OK;
+}
+
+hcg_status hcg_shard_group_search_routed(hcg_shard_group* g, const uint8_t* queries, uint32_t nq, uint32_t k,
+                                         uint32_t shard_depth, uint64_t* out_ids, uint32_t* out_sqdist,
+                                         uint32_t* out_len, void* stream, uint32_t* block_first,
+                                         uint32_t* block_count) {
+    if (!g || !block_first || !block_count) return set_error(HCG_EINVAL, "null argument");
+    if (g->ix.size() != 1 || g->G == 1) {  // one process holds every shard: it aggregates every query
+        *block_first = 0;
+        *block_count = nq;
+        return hcg_shard_group_search(g, queries, nq, k, shard_depth, out_ids, out_sqdist, out_len, stream);
+    }
+    if (k < 1) return set_error(HCG_EINVAL, "k must be >= 1");
+    if (k > HCG_MAX_K) return set_error(HCG_ECAPACITY, "k exceeds HCG_MAX_K");
+    if (shard_depth < 1) return set_error(HCG_EINVAL, "probe_depth must be >= 1");
+    const uint32_t G = g->G, me = g->first;
+    auto lo = [&](uint32_t p) { return uint32_t(uint64_t(nq) * p / G); };
+    *block_first = lo(me);
+    *block_count = lo(me + 1) - lo(me);
+    if (nq == 0) return HCG_OK;
+    if (!queries || !out_ids || !out_sqdist || !out_len) return set_error(HCG_EINVAL, "null buffer");
+    std::lock_guard<std::mutex> lock(g->mu);
+    const size_t pbytes = size_t(nq) * k * 8;
+    const uint32_t mine = *block_count;
+    cudaStream_t caller = static_cast<cudaStream_t>(stream);
+    SetDev sd(g->dev[0]);
+    SG_CUDA(cudaEventRecord(g->ev_in, caller));
+    SG_CUDA(cudaStreamWaitEvent(g->st[0], g->ev_in, 0));
+    HCG_RET_IF(g->packed[0].reserve(pbytes));
+    HCG_RET_IF(g->gathered[0].reserve(size_t(std::max<uint32_t>(mine, 1)) * k * 8 * G));
+    uint64_t* packed = static_cast<uint64_t*>(g->packed[0].p);
+    uint64_t* gathered = static_cast<uint64_t*>(g->gathered[0].p);
+    HCG_RET_IF(hcg_search_packed(g->ix[0], queries, nq, k, shard_depth, packed, g->st[0]));
+    // route: the partials of queries [lo(p), lo(p+1)) go to rank p, which
+    // receives every shard's partials of its own block (1/G of an all-gather)
+    HCG_RET_IF(nccl_check(nccl().GroupStart(), "ncclGroupStart"));
+    ncclResult_t nr = ncclSuccess;
+    for (uint32_t p = 0; p < G && nr == ncclSuccess; ++p) {
+        const size_t cnt_p = size_t(lo(p + 1) - lo(p)) * k;
+        if (cnt_p) nr = nccl().Send(packed + size_t(lo(p)) * k, cnt_p, ncclUint64, int(p), g->comm[0], g->st[0]);
+        if (nr == ncclSuccess && mine)
+            nr = nccl().Recv(gathered + size_t(p) * mine * k, size_t(mine) * k, ncclUint64, int(p), g->comm[0],
+                             g->st[0]);
+    }
+    const ncclResult_t ne = nccl().GroupEnd();
+    HCG_RET_IF(nccl_check(nr, "ncclSend/ncclRecv"));
+    HCG_RET_IF(nccl_check(ne, "ncclGroupEnd"));
+    if (mine)
+        HCG_RET_IF(hcg_merge_packed(gathered, G, mine, k, out_ids + size_t(*block_first) * k,
+                                    out_sqdist + size_t(*block_first) * k, out_len + *block_first, g->dev[0],
+                                    g->st[0]));
+    SG_CUDA(cudaEventRecord(g->done[0], g->st[0]));
+    SG_CUDA(cudaStreamWaitEvent(caller, g->done[0], 0));
     return HCG_OK;
 }
 

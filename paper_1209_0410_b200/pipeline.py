@@ -13,7 +13,8 @@ from __future__ import annotations
 
 class HostPipeline:
     def __init__(self, search_fn, k: int, max_batch: int, d_full: int = 128, device: int = 0, slots: int = 2):
-        """search_fn(queries_cuda, out=(ids, sqdist, len)) runs on the current stream."""
+        """search_fn(queries_cuda, (ids, sqdist, len)) runs on the current stream; it may return
+        the (lo, hi) rows it produced (a routed sharded aggregate), only those are read back."""
         import torch
         self.torch = torch
         self.search_fn = search_fn
@@ -52,14 +53,16 @@ class HostPipeline:
                 if ev_copied[s] is not None:
                     self.comp.wait_event(ev_copied[s])
                 outs = tuple(o[:n] for o in self.out[s])
-                self.search_fn(self.dq[s][:n], out=outs)
+                rows = self.search_fn(self.dq[s][:n], outs)
+                routed = isinstance(rows, tuple) and len(rows) == 2 and all(isinstance(x, int) for x in rows)
+                lo, hi = rows if routed else (0, n)
                 done = torch.cuda.Event()
                 done.record(self.comp)
                 ev_read[s] = done
             with torch.cuda.stream(self.d2h):
                 self.d2h.wait_event(done)
                 for h, d in zip(host_outs[b], outs):
-                    h.copy_(d, non_blocking=True)
+                    h[lo:hi].copy_(d[lo:hi], non_blocking=True)
                 copied = torch.cuda.Event()
                 copied.record(self.d2h)
                 ev_copied[s] = copied

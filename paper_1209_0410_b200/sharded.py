@@ -129,6 +129,21 @@ class ShardGroup:
                                            _stream(stream, q)))
         return ids, sq, ln
 
+    def search_routed(self, queries, k: int, shard_depth: int, out=None, stream=None):
+        """The aggregate routed to one aggregator per query:
+        this rank merges only its query block [first, first + count) of the
+        batch and fills those rows of `out`.  Returns (out, first, count)."""
+        q = _u8_2d(queries, self.d_full)
+        nq = q.shape[0]
+        if out is None:
+            out = (_empty_like_kind(q, (nq, k), np.uint64), _empty_like_kind(q, (nq, k), np.uint32),
+                   _empty_like_kind(q, (nq,), np.uint32))
+        ids, sq, ln = out
+        first, count = C.c_uint32(), C.c_uint32()
+        check(lib().hcg_shard_group_search_routed(self._h, _ptr(q), nq, k, shard_depth, _ptr(ids), _ptr(sq), _ptr(ln),
+                                                  _stream(stream, q), C.byref(first), C.byref(count)))
+        return out, first.value, count.value
+
     def close(self) -> None:
         if self._h:
             lib().hcg_shard_group_free(self._h)

@@ -61,6 +61,13 @@ for depth in depths:
     torch.cuda.synchronize()
     same_torch = torch.equal(ids, tids) and torch.equal(sq, tsq) and torch.equal(ln, tln)
     bad += int(not same_torch)
+    # the routed aggregate: this rank's block of the batch equals the full result's rows
+    (rids, rsq, rln), first, cnt = sidx.shard_group.search_routed(qs, k, depth)
+    torch.cuda.synchronize()
+    blk = slice(first, first + cnt)
+    same_routed = (torch.equal(rids[blk], ids[blk]) and torch.equal(rsq[blk], sq[blk]) and torch.equal(rln[blk], ln[blk])
+                   and cnt == (nq * (rank + 1)) // world - (nq * rank) // world)
+    bad += int(not same_routed)
     # every rank holds the same merged result
     t = ids.view(torch.int64).sum().reshape(1)
     tt = [torch.zeros_like(t) for _ in range(world)]
@@ -85,7 +92,8 @@ for depth in depths:
                     mism += 1
             bad += mism
             report["checks"].append({"depth": depth, "against": name, "mismatched_queries": mism,
-                                     "torch_aggregate_identical": bool(same_torch)})
+                                     "torch_aggregate_identical": bool(same_torch),
+                                     "routed_block_identical_rank0": bool(same_routed)})
 dist.barrier()
 # exact brute force across shards
 ex_ids, _, _ = sidx.brute_force(qs[:16], k)
