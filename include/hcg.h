@@ -302,6 +302,8 @@ hcg_status hcg_shard_group_search_routed(hcg_shard_group* group, const uint8_t* 
 /* CUDA device of the group's first local shard (where results land) and the
  * descriptor length. */
 int hcg_shard_group_device(const hcg_shard_group* group);
+/* Shards driven by this process: G for one process over G GPUs, 1 per rank. */
+uint32_t hcg_shard_group_local_shards(const hcg_shard_group* group);
 uint32_t hcg_shard_group_dims(const hcg_shard_group* group);
 
 /* ---- GPU batch-size controller: DTAHE (Alg. 3, PAPER.md:1177-1191;
@@ -323,8 +325,9 @@ typedef struct hcg_server_policy {
 } hcg_server_policy;
 typedef struct hcg_server hcg_server;
 
-/* Serve exactly one of `index` (u8) / `group` with fixed k and probe depth
- * (per-shard depth for a group).  policy NULL: {8192, 1, 0, 2}. */
+/* Serve exactly one of `index` (u8) / `group` (one process over all its GPUs;
+ * a per-rank group is rejected: its searches are collective) with fixed k and
+ * probe depth (per-shard depth for a group).  policy NULL: {8192, 1, 0, 2}. */
 hcg_status hcg_server_create(const hcg_index* index, hcg_shard_group* group, uint32_t k, uint32_t depth,
                              const hcg_server_policy* policy, hcg_server** out);
 hcg_status hcg_server_free(hcg_server* server);

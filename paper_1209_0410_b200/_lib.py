@@ -42,7 +42,7 @@ EXPORTS = [
     "hcg_shard_group_free", "hcg_shard_group_shards", "hcg_shard_group_search", "hcg_index_device", "hcg_index_ids",
     "hcg_shard_group_device", "hcg_shard_group_dims", "hcg_server_create", "hcg_server_free", "hcg_server_replay",
     "hcg_server_start", "hcg_server_submit", "hcg_server_wait", "hcg_refine_unionless",
-    "hcg_shard_group_search_routed",
+    "hcg_shard_group_search_routed", "hcg_shard_group_local_shards",
 ]
 
 
@@ -160,6 +160,8 @@ def lib() -> C.CDLL:
     L.hcg_refine_unionless.argtypes = [vp, u32, u32, u32]
     L.hcg_shard_group_device.restype = C.c_int
     L.hcg_shard_group_device.argtypes = [vp]
+    L.hcg_shard_group_local_shards.restype = u32
+    L.hcg_shard_group_local_shards.argtypes = [vp]
     L.hcg_shard_group_dims.restype = u32
     L.hcg_shard_group_dims.argtypes = [vp]
     L.hcg_server_create.argtypes = [vp, vp, u32, u32, P(HcgServerPolicy), P(vp)]

@@ -300,6 +300,8 @@ hcg_status hcg_server_create(const hcg_index* index, hcg_shard_group* group, uin
     if (!out) return set_error(HCG_EINVAL, "null output handle");
     *out = nullptr;
     if ((index == nullptr) == (group == nullptr)) return set_error(HCG_EINVAL, "serve exactly one index or shard group");
+    if (group && hcg_shard_group_local_shards(group) != hcg_shard_group_shards(group))
+        return set_error(HCG_EINVAL, "the server drives a one-process shard group (a per-rank group's searches are collective)");
     if (k < 1 || depth < 1) return set_error(HCG_EINVAL, "k and probe_depth must be >= 1");
     if (k > HCG_MAX_K) return set_error(HCG_ECAPACITY, "k exceeds HCG_MAX_K");
     hcg_server_policy p{8192, 1, 0.0, 2};

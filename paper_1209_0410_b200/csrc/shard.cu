@@ -365,6 +365,7 @@ hcg_status hcg_shard_group_free(hcg_shard_group* g) {
 
 uint32_t hcg_shard_group_shards(const hcg_shard_group* g) { return g ? g->G : 0; }
 int hcg_shard_group_device(const hcg_shard_group* g) { return g ? g->dev[0] : -1; }
+uint32_t hcg_shard_group_local_shards(const hcg_shard_group* g) { return g ? uint32_t(g->ix.size()) : 0; }
 uint32_t hcg_shard_group_dims(const hcg_shard_group* g) { return g ? g->d_full : 0; }
 
 hcg_status hcg_shard_group_search(hcg_shard_group* g, const uint8_t* queries, uint32_t nq, uint32_t k,
