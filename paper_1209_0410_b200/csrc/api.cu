@@ -807,10 +807,6 @@ hcg_status hcg_build(const hcg_scheme* s, const uint8_t* rows, uint64_t n, uint6
     HCG_TRY(check_device(device));
     DeviceGuard g(device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (const char* gran = knob("HCG_L2_FETCH")) {  // A/B: L2 fetch granularity hint (tuning builds)
-        cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, size_t(atoi(gran)));
-        cudaGetLastError();
-    }
 
     hcg_index* ix = nullptr;
     HCG_TRY(new_index(s, n, id_base, id_stride, device, st, &ix));

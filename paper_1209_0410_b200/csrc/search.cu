@@ -618,135 +618,6 @@ __device__ __forceinline__ void gather_windows(const RefineArgs& a, const uint32
     }
 }
 
-// The union-less walk in two stages for rows of <= 128 bytes (the bench
-// shape).  Every term of the squared distance is >= 0, so the first 64 bytes
-// of a row give a lower bound of its distance: a row whose bound already
-// exceeds the top-k threshold's distance cannot enter the top-k (a tie needs
-// the full read: only bound > threshold is dropped), and its second 64 bytes
-// are never read.  Results are exact; at 10M rows, D = 350, k = 10 about 56 %
-// of the walked rows stop after the first half (`tools/partial_bound_probe.py`).
-// Per pass a warp takes 64 entries: the 4 groups of 8 lanes own 16 rows each,
-// lane (h, c) = (l8 >> 2, l8 & 3) reads chunk c (stage A) and chunk 4 + c
-// (stage B, live rows only) of rows h + 2j, j < 8; a reduce-scatter over the 4
-// chunk lanes leaves rows 4 b1 + 2 b0 + t (t = 0, 1) with lane (b1, b0); a
-// ballot tells every lane which of its rows are live.
-template <bool SMALLC>
-__device__ __forceinline__ void gather_windows_split(const RefineArgs& a, const uint32_t* begins_q, const uint8_t* qrow,
-                                                     int lane, WarpTopK<1>& tk, uint64_t* wsm) {
-    const int l8 = lane & 7, grp = lane >> 3, h = l8 >> 2, cl = l8 & 3;
-    const bool b1 = l8 & 2, b0 = l8 & 1;
-    const uint32_t chunks = a.pitch >> 4;
-    const uint32_t take = a.take, n = a.C * take, C = a.C;
-    const uint4 qa = uint32_t(cl) < chunks ? *reinterpret_cast<const uint4*>(qrow + cl * 16) : make_uint4(0, 0, 0, 0);
-    const uint4 qb =
-        uint32_t(4 + cl) < chunks ? *reinterpret_cast<const uint4*>(qrow + (4 + cl) * 16) : make_uint4(0, 0, 0, 0);
-    // (curve, position) of this lane's 8 entries (walk positions grp*16 + h + 2j), advanced by 64 per pass
-    uint32_t cc[8], pp[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        const uint32_t e = uint32_t(grp * 16 + h + 2 * j);
-        cc[j] = e / take;
-        pp[j] = e - cc[j] * take;
-    }
-    unsigned long long wstart = 0;
-    if (SMALLC && uint32_t(lane) < C)
-        wstart = reinterpret_cast<unsigned long long>(a.slots[lane] + __ldg(begins_q + lane));
-    auto entry = [&](int j) -> uint32_t {
-        if constexpr (SMALLC) {
-            const uint32_t* w = reinterpret_cast<const uint32_t*>(__shfl_sync(kFull, wstart, int(cc[j] & 31)));
-            return cc[j] < C ? __ldg(w + pp[j]) : kEmpty;
-        } else {
-            return cc[j] < C ? __ldg(a.slots[cc[j]] + __ldg(begins_q + cc[j]) + pp[j]) : kEmpty;
-        }
-    };
-    uint32_t nx[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) nx[j] = entry(j);
-    // lane of the half-group that holds row j after the reduce-scatter
-    const int hbase = grp * 8 + h * 4;
-    for (uint32_t base = 0; base < n; base += 64) {
-        // stage A: the first halves
-        uint32_t acc[8];
-        uint32_t cur[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            cur[j] = nx[j];
-            const uint4 v = (cur[j] != kEmpty && uint32_t(cl) < chunks)
-                                ? ldg_stream(a.rows + uint64_t(cur[j]) * a.pitch + cl * 16)
-                                : make_uint4(0, 0, 0, 0);
-            acc[j] = sad2_16(v, qa, 0u);
-        }
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            pp[j] += 64;
-            while (pp[j] >= take && cc[j] < C) {
-                pp[j] -= take;
-                ++cc[j];
-            }
-            nx[j] = entry(j);
-        }
-        uint32_t s4[4], s2[2];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const uint32_t send = b1 ? acc[i] : acc[i + 4];
-            const uint32_t keep = b1 ? acc[i + 4] : acc[i];
-            s4[i] = keep + __shfl_xor_sync(kFull, send, 2);
-        }
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-            const uint32_t send = b0 ? s4[i] : s4[i + 2];
-            const uint32_t keep = b0 ? s4[i + 2] : s4[i];
-            s2[i] = keep + __shfl_xor_sync(kFull, send, 1);
-        }
-        // this lane's two rows: j = 4 b1 + 2 b0 + t
-        const int jb = (b1 ? 4 : 0) + (b0 ? 2 : 0);
-        uint32_t row[2] = {cur[0], cur[1]};
-#pragma unroll
-        for (int j = 2; j < 8; j += 2)
-            if (j == jb) {
-                row[0] = cur[j];
-                row[1] = cur[j + 1];
-            }
-        const uint32_t thr_s = uint32_t(tk.thr >> 32);
-        bool live[2];
-#pragma unroll
-        for (int t = 0; t < 2; ++t) live[t] = row[t] != kEmpty && s2[t] <= thr_s;
-        const unsigned L0 = __ballot_sync(kFull, live[0]), L1 = __ballot_sync(kFull, live[1]);
-        // stage B: the second halves of the live rows
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const int owner = hbase + ((j >> 2) & 1) * 2 + ((j >> 1) & 1);
-            const bool lj = (((j & 1) ? L1 : L0) >> owner) & 1u;
-            const uint4 v = (lj && uint32_t(4 + cl) < chunks)
-                                ? ldg_stream(a.rows + uint64_t(cur[j]) * a.pitch + (4 + cl) * 16)
-                                : make_uint4(0, 0, 0, 0);
-            acc[j] = sad2_16(v, qb, 0u);
-        }
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const uint32_t send = b1 ? acc[i] : acc[i + 4];
-            const uint32_t keep = b1 ? acc[i + 4] : acc[i];
-            s4[i] = keep + __shfl_xor_sync(kFull, send, 2);
-        }
-        uint32_t S[2];
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-            const uint32_t send = b0 ? s4[i] : s4[i + 2];
-            const uint32_t keep = b0 ? s4[i + 2] : s4[i];
-            S[i] = s2[i] + keep + __shfl_xor_sync(kFull, send, 1);
-        }
-#pragma unroll
-        for (int t = 0; t < 2; ++t) {
-            uint32_t sl = row[t];
-            if (a.idtab) {
-                const bool pre = live[t] && S[t] <= uint32_t(tk.thr >> 32);
-                if (__any_sync(kFull, pre) && pre) sl = __ldg(a.idtab + row[t]);
-            }
-            tk.offer_unique(live[t] ? ((uint64_t(S[t]) << 32) | sl) : kNone, lane, wsm);
-        }
-    }
-}
-
 template <int CR>
 __device__ __forceinline__ void load_query(const RefineArgs& a, uint32_t q, int lane, uint4 (&qv)[CR]) {
     const uint32_t chunks = a.pitch >> 4;
@@ -779,9 +650,6 @@ __global__ void __launch_bounds__(kRefineThreads, MINB) k_gather(RefineArgs a, c
 }
 
 // K3c without the union: one warp per query over the raw windows.
-#ifndef HCG_SPLIT_ROWS
-#define HCG_SPLIT_ROWS 1  // two-stage rows (first-half bound) in the union-less walk
-#endif
 template <int R, int CR, int MINB, bool SMALLC, int NT = kRefineThreads>
 __global__ void __launch_bounds__(NT, MINB) k_gather_nu(RefineArgs a) {
     // per-warp scratch of the batched dedup (R >= 2 only)
@@ -795,11 +663,7 @@ __global__ void __launch_bounds__(NT, MINB) k_gather_nu(RefineArgs a) {
         load_query<CR>(a, qq, lane, qv);
         WarpTopK<R> tk;
         tk.init(int(a.k));
-        if constexpr (CR == 1 && R == 1 && HCG_SPLIT_ROWS)
-            gather_windows_split<SMALLC>(a, a.begins + uint64_t(qq) * a.C, a.queries + uint64_t(qq) * a.pitch, lane,
-                                         tk, wsm);
-        else
-            gather_windows<CR, SMALLC>(a, a.begins + uint64_t(qq) * a.C, qv, lane, tk, wsm);
+        gather_windows<CR, SMALLC>(a, a.begins + uint64_t(qq) * a.C, qv, lane, tk, wsm);
         uint32_t valid = 0;
 #pragma unroll
         for (int r = 0; r < R; ++r)
