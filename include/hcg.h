@@ -339,9 +339,11 @@ hcg_status hcg_server_replay(hcg_server* server, const uint8_t* queries, uint32_
                              uint64_t* out_ids, uint32_t* out_sqdist, uint32_t* out_len, double* latency_s,
                              uint32_t* batch_sizes, uint32_t* n_batches);
 /* Online serving: start a dispatcher thread with a pinned ring of `capacity`
- * queries; submit copies queries in and returns a ticket; wait blocks until
- * the ticket's queries are answered and copies their results (and response
- * times) out.  Thread-safe. */
+ * queries; submit copies queries in and returns a ticket (it blocks while
+ * `capacity` submitted queries await collection); wait blocks until the
+ * ticket's queries are answered and copies their results (and response times)
+ * out, freeing their ring space.  Thread-safe; a replay and an online session
+ * do not run at the same time on one server. */
 hcg_status hcg_server_start(hcg_server* server, uint64_t capacity);
 hcg_status hcg_server_submit(hcg_server* server, const uint8_t* queries, uint32_t nq, uint64_t* ticket);
 hcg_status hcg_server_wait(hcg_server* server, uint64_t ticket, uint64_t* out_ids, uint32_t* out_sqdist,
