@@ -99,6 +99,9 @@ __device__ __forceinline__ uint64_t locate_one(const LocateArgs& a, const uint32
         }
     }
     uint64_t rank;
+#ifdef HCG_PROBE_NOSEARCH  // timing probe (tuning builds): key + prefix only, no lower_bound
+    if (SMEMIN) cmp = -1;
+#endif
     if (cmp < 0) {
         rank = 0;
     } else if (cmp > 0) {
