@@ -1133,7 +1133,7 @@ static hcg_status search_impl(const hcg_index* ix, const uint8_t* queries, uint3
             a.out_sqdist = os.dev;
             a.out_len = ol.dev;
             const LocateArgs la = locate_args(ix, dq, nq, depth, nullptr, nullptr, flag);
-            if (!ms_out && small_eligible(la, a, ix->dims16, ix->wsmax)) {
+            if (!ms_out && small_eligible(la, a, ix->dims16, ix->wsmax, ix->device)) {
                 static unsigned long long* prof = nullptr;  // phase stamps (tuning builds: HCG_SMALL_PROF)
                 if (knob("HCG_SMALL_PROF")) {
                     if (!prof) cudaMalloc(&prof, 8 * 8);

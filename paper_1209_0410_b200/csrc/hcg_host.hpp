@@ -114,7 +114,7 @@ struct RefineArgs {
 hcg_status launch_refine(const RefineArgs& a, void* scratch, size_t* scratch_bytes, int device,
                          cudaStream_t st);
 // Small batches: the whole search of a query in one CTA (k_search_small).
-bool small_eligible(const LocateArgs& la, const RefineArgs& a, bool dims16, int wsmax);
+bool small_eligible(const LocateArgs& la, const RefineArgs& a, bool dims16, int wsmax, int device);
 hcg_status launch_search_small(const LocateArgs& la, const RefineArgs& a, int wsmax, int device, cudaStream_t st);
 // Whether a search of nq queries at k takes the union-less K3c (k_gather_nu).
 bool refine_unionless(const RefineArgs& a);

@@ -114,10 +114,12 @@ __device__ __forceinline__ void key_shl(uint64_t (&k)[WMAX], int s) {
 // bit-plane interleave as a 16 x 16 bit-matrix transpose (4 block-swap
 // stages) -- T[b] bit i = bit b of x[i]; plane b = brev16(T[b]) sits at key
 // bits [16 b, 16 b + 16), the same key as the generic loop below.
-template <int M, int WMAX>
+// COMPACT: the bit-plane loop stays rolled (a tenth of the code; the
+// latency kernel runs it once per query, from cold instruction caches).
+template <int M, int WMAX, bool COMPACT = false>
 __device__ __forceinline__ void make_key_d16(uint32_t (&x)[16], int kind, uint64_t (&key)[WMAX]) {
     if (kind == HCG_HILBERT) {
-#pragma unroll
+#pragma unroll(COMPACT ? 1 : M)
         for (uint32_t q = 1u << (M - 1); q > 1; q >>= 1) {
             const uint32_t low = q - 1;
 #pragma unroll

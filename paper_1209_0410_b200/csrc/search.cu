@@ -28,6 +28,21 @@
 
 namespace hcg {
 
+// Device attributes of the refine launches, queried once per device.
+struct DevInfo {
+    int sms = 0;
+};
+inline const DevInfo& dev_info(int device) {
+    static DevInfo info[64];
+    DevInfo& d = info[device & 63];
+    if (d.sms == 0) {
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+        d.sms = sms;
+    }
+    return d;
+}
+
 __device__ __forceinline__ unsigned lanemask_lt_s() {
     unsigned m;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
@@ -57,6 +72,9 @@ __device__ __forceinline__ int suffix_cmp(const uint64_t* e, const uint64_t (&qs
 // every lane computes the key, the lanes split the 32-ary search).  lut: the
 // view's cell table in shared memory.  Returns the window begin; *rank_out
 // the rank.
+#ifndef HCG_SMALL_COMPACT_KEY
+#define HCG_SMALL_COMPACT_KEY true
+#endif
 // MFIX (8 or 16): every curve has exactly 16 dims and m = MFIX -- the key is
 // built by the compile-time d16 transform alone (a fraction of the generic
 // code: the latency kernel runs it from a cold instruction cache).
@@ -81,7 +99,7 @@ __device__ __forceinline__ uint64_t locate_one(const LocateArgs& a, const uint32
     }
     uint64_t key[WMAX];
     if constexpr (MFIX != 0 && DMAX == 16 && WMAX >= 4)
-        make_key_d16<MFIX, WMAX>(x, a.kind, key);
+        make_key_d16<MFIX, WMAX, HCG_SMALL_COMPACT_KEY>(x, a.kind, key);
     else
         make_key<DMAX, WMAX>(x, d, a.m, a.kind, key);
 
@@ -895,11 +913,15 @@ hcg_status small_dispatch_r(const LocateArgs& la, const RefineArgs& a, uint32_t 
 }
 
 // The default scheme's shapes (16 dims per curve, m = 8 raw / 16 lifted).
-bool small_eligible(const LocateArgs& la, const RefineArgs& a, bool dims16, int wsmax) {
+// One wave of CTAs at most: 2 per SM (1024 threads each) while the shared
+// memory allows (k <= 64), else 1.  Measured at 10M, D = 350: batch 256 69 µs
+// fused vs 91 µs on the three-kernel path, batch 512 (two waves) 129 vs 96 µs.
+bool small_eligible(const LocateArgs& la, const RefineArgs& a, bool dims16, int wsmax, int device) {
     static const bool off = knob("HCG_NO_SMALL") != nullptr;  // A/B: locate + union + gather for every batch
+    const uint32_t wave = uint32_t(dev_info(device).sms) * (a.k <= 64 ? 2u : 1u);
     return !off && dims16 && (la.m == 8 || la.m == 16) && a.dtype == HCG_U8 && la.dtype == HCG_U8 && a.nq >= 1 &&
-           a.nq <= kSmallBatch && a.pitch <= 128 && uint64_t(a.C) * a.take <= kSmallMaxWalk && wsmax <= 4 &&
-           a.C <= kSmallMaxCurves && a.C * 16 <= kSmallMaxAssign && a.mode != kOutCandidates;
+           a.nq <= std::min(kSmallBatch, wave) && a.pitch <= 128 && uint64_t(a.C) * a.take <= kSmallMaxWalk &&
+           wsmax <= 4 && a.C <= kSmallMaxCurves && a.C * 16 <= kSmallMaxAssign && a.mode != kOutCandidates;
 }
 
 hcg_status launch_search_small(const LocateArgs& la, const RefineArgs& a, int wsmax, int device, cudaStream_t st) {
@@ -1412,21 +1434,6 @@ __global__ void __launch_bounds__(kRefineThreads) k_union_cas(RefineArgs a, uint
 
 namespace {
 int r_bucket(uint32_t k) { return k <= 32 ? 1 : k <= 64 ? 2 : k <= 128 ? 4 : 8; }
-
-// Device attributes of the refine launches, queried once per device.
-struct DevInfo {
-    int sms = 0;
-};
-const DevInfo& dev_info(int device) {
-    static DevInfo info[64];
-    DevInfo& d = info[device & 63];
-    if (d.sms == 0) {
-        int sms = 148;
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-        d.sms = sms;
-    }
-    return d;
-}
 
 template <class K>
 hcg_status opt_in_smem(K kern, int device, bool* configured) {
