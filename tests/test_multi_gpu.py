@@ -28,14 +28,17 @@ def _ngpus():
 needs2 = [pytest.mark.gpu, pytest.mark.skipif(not gpu_available() or _ngpus() < 2, reason="needs >= 2 GPUs")]
 
 
-@pytest.mark.parametrize("view", ["lifted", "raw"])
+@pytest.mark.parametrize("view,queries", [("lifted", 64), ("raw", 64), ("lifted", 3)])
 @pytest.mark.gpu
 @pytest.mark.skipif(not gpu_available() or _ngpus() < 2, reason="needs >= 2 GPUs")
-def test_sharded_search_per_rank_processes(view):
+def test_sharded_search_per_rank_processes(view, queries):
+    """Per-rank shard groups vs the sharded oracle and the reference TUs; the
+    routed aggregate's blocks (3 queries: some ranks aggregate none) vs the
+    all-gathered result."""
     g = min(_ngpus(), 4)
     out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={g}",
                           "--master-addr", "127.0.0.1", "--master-port", "29533",
-                          os.path.join(ROOT, "tools", "sharded_check.py"), "--view", view],
+                          os.path.join(ROOT, "tools", "sharded_check.py"), "--view", view, "--queries", str(queries)],
                          capture_output=True, text=True, timeout=900, cwd=ROOT)
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
     assert "sharded ok" in out.stdout
