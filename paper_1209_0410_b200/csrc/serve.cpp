@@ -50,6 +50,11 @@ namespace {
 
 using Clock = std::chrono::steady_clock;
 
+// Batches up to this size may run side by side (launch): the one-CTA-per-query
+// search path's range (search.cu kSmallBatch).
+constexpr uint32_t kServeSmallBatch = 512;
+constexpr uint32_t kSideSlots = 8;  // slots beyond pol.slots for side batches
+
 double seconds_since(Clock::time_point t0) {
     return std::chrono::duration<double>(Clock::now() - t0).count();
 }
@@ -60,6 +65,9 @@ struct Slot {
     uint32_t* dsq = nullptr;
     uint32_t* dlen = nullptr;
     cudaEvent_t loaded = nullptr, searched = nullptr, copied = nullptr;  // copied: timing event
+    cudaStream_t own = nullptr;  // the whole batch when it runs beside others (see launch)
+    bool side = false;           // launched on `own`
+    uint32_t cap = 0;            // queries it holds
     bool busy = false;
     uint64_t first = 0;  // sequence number of the batch's first query
     uint32_t count = 0;
@@ -75,6 +83,7 @@ struct hcg_server {
     hcg_shard_group* group = nullptr;
     int device = 0;
     uint32_t d_full = 0, k = 0, depth = 0;
+    uint32_t sms = 0;  // SM count: the budget for batches that run side by side
     hcg_server_policy pol{};
     cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
     std::vector<Slot> slots;
@@ -103,13 +112,19 @@ namespace {
 
 hcg_status engine_init(hcg_server* s) {
     SV_CUDA(cudaSetDevice(s->device));
+    int sms = 0;
+    SV_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device));
+    s->sms = uint32_t(sms);
     SV_CUDA(cudaStreamCreateWithFlags(&s->h2d, cudaStreamNonBlocking));
     SV_CUDA(cudaStreamCreateWithFlags(&s->comp, cudaStreamNonBlocking));
     SV_CUDA(cudaStreamCreateWithFlags(&s->d2h, cudaStreamNonBlocking));
     SV_CUDA(cudaEventCreate(&s->start));
-    s->slots.resize(s->pol.slots);
-    const size_t B = s->pol.max_batch;
-    for (auto& sl : s->slots) {
+    s->slots.resize(s->pol.slots + (s->pol.slots >= 2 ? kSideSlots : 0));
+    for (size_t i = 0; i < s->slots.size(); ++i) {
+        Slot& sl = s->slots[i];
+        // the pipeline's slots hold max_batch queries, the extra ones a side batch
+        sl.cap = i < s->pol.slots ? s->pol.max_batch : std::min(s->pol.max_batch, kServeSmallBatch);
+        const size_t B = sl.cap;
         SV_CUDA(cudaMalloc(&sl.dq, B * s->d_full));
         SV_CUDA(cudaMalloc(&sl.dids, B * s->k * 8));
         SV_CUDA(cudaMalloc(&sl.dsq, B * s->k * 4));
@@ -117,6 +132,7 @@ hcg_status engine_init(hcg_server* s) {
         SV_CUDA(cudaEventCreateWithFlags(&sl.loaded, cudaEventDisableTiming));
         SV_CUDA(cudaEventCreateWithFlags(&sl.searched, cudaEventDisableTiming));
         SV_CUDA(cudaEventCreate(&sl.copied));
+        SV_CUDA(cudaStreamCreateWithFlags(&sl.own, cudaStreamNonBlocking));
     }
     return HCG_OK;
 }
@@ -133,6 +149,10 @@ void engine_free(hcg_server* s) {
         if (sl.loaded) cudaEventDestroy(sl.loaded);
         if (sl.searched) cudaEventDestroy(sl.searched);
         if (sl.copied) cudaEventDestroy(sl.copied);
+        if (sl.own) {
+            cudaStreamSynchronize(sl.own);
+            cudaStreamDestroy(sl.own);
+        }
     }
     if (s->start) cudaEventDestroy(s->start);
     for (cudaStream_t st : {s->h2d, s->comp, s->d2h})
@@ -155,30 +175,38 @@ hcg_status clock_sync(hcg_server* s) {
 }
 
 // Enqueue one batch: `count` queries from host memory q (pinned or registered)
-// into slot `si`; results to host memory (ids / sq / len, count rows).
-hcg_status launch(hcg_server* s, uint32_t si, const uint8_t* q, uint32_t count, uint64_t* ids, uint32_t* sq,
-                  uint32_t* len) {
+// into slot `si`; results to host memory (ids / sq / len, count rows).  A side
+// batch (pick) runs H2D -> search -> D2H on the slot's own stream; any other
+// runs on s->comp after the side batches in flight, its copies overlapped on
+// s->h2d / s->d2h.  The slot's events order its reuse either way.
+hcg_status launch(hcg_server* s, uint32_t si, bool side, const uint8_t* q, uint32_t count, uint64_t* ids,
+                  uint32_t* sq, uint32_t* len) {
     Slot& sl = s->slots[si];
     const size_t k = s->k;
+    cudaStream_t up = side ? sl.own : s->h2d, cs = side ? sl.own : s->comp, down = side ? sl.own : s->d2h;
+    if (!side)
+        for (const auto& o : s->slots)
+            if (o.busy && o.side) SV_CUDA(cudaStreamWaitEvent(cs, o.searched, 0));
     // upload (after this slot's previous search read its queries)
-    SV_CUDA(cudaStreamWaitEvent(s->h2d, sl.searched, 0));
-    SV_CUDA(cudaMemcpyAsync(sl.dq, q, size_t(count) * s->d_full, cudaMemcpyHostToDevice, s->h2d));
-    SV_CUDA(cudaEventRecord(sl.loaded, s->h2d));
+    SV_CUDA(cudaStreamWaitEvent(up, sl.searched, 0));
+    SV_CUDA(cudaMemcpyAsync(sl.dq, q, size_t(count) * s->d_full, cudaMemcpyHostToDevice, up));
+    SV_CUDA(cudaEventRecord(sl.loaded, up));
     // search (after the upload, and after this slot's previous results left)
-    SV_CUDA(cudaStreamWaitEvent(s->comp, sl.loaded, 0));
-    SV_CUDA(cudaStreamWaitEvent(s->comp, sl.copied, 0));
+    if (cs != up) SV_CUDA(cudaStreamWaitEvent(cs, sl.loaded, 0));
+    SV_CUDA(cudaStreamWaitEvent(cs, sl.copied, 0));
     if (s->group)
-        HCG_RET_IF(hcg_shard_group_search(s->group, sl.dq, count, s->k, s->depth, sl.dids, sl.dsq, sl.dlen, s->comp));
+        HCG_RET_IF(hcg_shard_group_search(s->group, sl.dq, count, s->k, s->depth, sl.dids, sl.dsq, sl.dlen, cs));
     else
-        HCG_RET_IF(hcg_search(s->ix, sl.dq, count, s->k, s->depth, sl.dids, sl.dsq, sl.dlen, s->comp));
-    SV_CUDA(cudaEventRecord(sl.searched, s->comp));
+        HCG_RET_IF(hcg_search(s->ix, sl.dq, count, s->k, s->depth, sl.dids, sl.dsq, sl.dlen, cs));
+    SV_CUDA(cudaEventRecord(sl.searched, cs));
     // download; the copy event is the batch's completion
-    SV_CUDA(cudaStreamWaitEvent(s->d2h, sl.searched, 0));
-    SV_CUDA(cudaMemcpyAsync(ids, sl.dids, count * k * 8, cudaMemcpyDeviceToHost, s->d2h));
-    SV_CUDA(cudaMemcpyAsync(sq, sl.dsq, count * k * 4, cudaMemcpyDeviceToHost, s->d2h));
-    SV_CUDA(cudaMemcpyAsync(len, sl.dlen, size_t(count) * 4, cudaMemcpyDeviceToHost, s->d2h));
-    SV_CUDA(cudaEventRecord(sl.copied, s->d2h));
+    if (down != cs) SV_CUDA(cudaStreamWaitEvent(down, sl.searched, 0));
+    SV_CUDA(cudaMemcpyAsync(ids, sl.dids, count * k * 8, cudaMemcpyDeviceToHost, down));
+    SV_CUDA(cudaMemcpyAsync(sq, sl.dsq, count * k * 4, cudaMemcpyDeviceToHost, down));
+    SV_CUDA(cudaMemcpyAsync(len, sl.dlen, size_t(count) * 4, cudaMemcpyDeviceToHost, down));
+    SV_CUDA(cudaEventRecord(sl.copied, down));
     sl.busy = true;
+    sl.side = side;
     sl.count = count;
     return HCG_OK;
 }
@@ -198,16 +226,37 @@ hcg_status poll(hcg_server* s, uint32_t si, bool* done, double* t) {
     return HCG_OK;
 }
 
-int free_slot(const hcg_server* s) {
-    for (size_t i = 0; i < s->slots.size(); ++i)
-        if (!s->slots[i].busy) return int(i);
-    return -1;
-}
-
 bool any_busy(const hcg_server* s) {
     for (const auto& sl : s->slots)
         if (sl.busy) return true;
     return false;
+}
+
+// Slot for a batch of `count` queries, or -1 (keep buffering).  The paper's
+// pipeline keeps pol.slots batches in flight, one after another on the device.
+// At light load a batch is small and its search takes one SM per query: such
+// a batch runs beside the other small ones in flight (*side) while their
+// queries fit one CTA per SM and no large batch is in flight; the side
+// batches together count as one stage of the pipeline.
+int pick(const hcg_server* s, uint32_t count, bool* side) {
+    uint32_t side_q = 0, stages = 0;
+    bool any_side = false;
+    int free_full = -1, free_side = -1;  // a free pipeline slot / a free extra slot
+    for (size_t i = 0; i < s->slots.size(); ++i) {
+        const Slot& o = s->slots[i];
+        if (!o.busy) {
+            int& f = i < s->pol.slots ? free_full : free_side;
+            if (f < 0) f = int(i);
+        } else if (o.side) {
+            side_q += o.count;
+            any_side = true;
+        } else {
+            ++stages;
+        }
+    }
+    *side = !s->group && s->pol.slots >= 2 && stages == 0 && count <= kServeSmallBatch && side_q + count <= s->sms;
+    if (*side) return free_side >= 0 ? free_side : free_full;
+    return stages + (any_side ? 1 : 0) < s->pol.slots ? free_full : -1;
 }
 
 // The dispatch rule (Alg. 3 lines 9-10 with CC = 0, plus max_wait).
@@ -262,15 +311,16 @@ void worker_loop(hcg_server* s) {
         const uint64_t waiting = s->submitted - head;
         const double now = seconds_since(s->t0);
         const double oldest = waiting ? now - s->arrive[head % s->capacity] : 0.0;
-        const int si = free_slot(s);
-        if (si >= 0 && should_launch(s, waiting, oldest)) {
-            // a batch never wraps the ring: it ends at the ring's end at the latest
-            const uint64_t ring_off = head % s->capacity;
-            const uint32_t count = uint32_t(std::min<uint64_t>({waiting, s->pol.max_batch, s->capacity - ring_off}));
+        // a batch never wraps the ring: it ends at the ring's end at the latest
+        const uint64_t ring_off = head % s->capacity;
+        const uint32_t count = uint32_t(std::min<uint64_t>({waiting, s->pol.max_batch, s->capacity - ring_off}));
+        bool side = false;
+        const int si = should_launch(s, waiting, oldest) ? pick(s, count, &side) : -1;
+        if (si >= 0) {
             lk.unlock();
             Slot& sl = s->slots[si];
             sl.first = head;
-            const hcg_status rc = launch(s, uint32_t(si), s->in_ring + ring_off * s->d_full, count,
+            const hcg_status rc = launch(s, uint32_t(si), side, s->in_ring + ring_off * s->d_full, count,
                                          s->out_ids + ring_off * s->k, s->out_sq + ring_off * s->k,
                                          s->out_len + ring_off);
             if (rc != HCG_OK) {
@@ -388,11 +438,12 @@ hcg_status hcg_server_replay(hcg_server* s, const uint8_t* queries, uint32_t nq,
             }
         }
         const uint64_t waiting = arrived - head;
-        const int si = free_slot(s);
-        if (si >= 0 && should_launch(s, waiting, waiting ? now - arrival_s[head] : 0.0)) {
-            const uint32_t count = uint32_t(std::min<uint64_t>(waiting, s->pol.max_batch));
+        const uint32_t count = uint32_t(std::min<uint64_t>(waiting, s->pol.max_batch));
+        bool side = false;
+        const int si = should_launch(s, waiting, waiting ? now - arrival_s[head] : 0.0) ? pick(s, count, &side) : -1;
+        if (si >= 0) {
             s->slots[si].first = head;
-            HCG_RET_IF(launch(s, uint32_t(si), queries + head * s->d_full, count, out_ids + head * k,
+            HCG_RET_IF(launch(s, uint32_t(si), side, queries + head * s->d_full, count, out_ids + head * k,
                               out_sqdist + head * k, out_len + head));
             sizes.push_back(count);
             head += count;

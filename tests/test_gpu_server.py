@@ -64,6 +64,22 @@ def test_light_load_gives_small_batches(index, queries):
     srv.close()
 
 
+@pytest.mark.parametrize("slots,rate", [(2, 1e6), (4, 3e6), (8, 6e6)])
+def test_side_by_side_batches_match_search(index, queries, slots, rate):
+    """Light-to-middle load: small batches run side by side on their slots'
+    own streams, larger ones through the pipeline after them (serve.cpp pick);
+    every query is answered once with hcg_search's exact results."""
+    srv = Server(index, K, D, max_batch=8192, slots=slots)
+    q = queries[:6000]
+    ids, sq, ln, lat, sizes = srv.replay(q, poisson_arrivals(rate, len(q), seed=slots))
+    ri, rs, rl = _direct(index, q)
+    np.testing.assert_array_equal(ids, ri)
+    np.testing.assert_array_equal(sq, rs)
+    np.testing.assert_array_equal(ln, rl)
+    assert sizes.sum() == len(q) and (lat > 0).all()
+    srv.close()
+
+
 def test_min_batch_and_max_wait_buffer_queries(index, queries):
     """min_batch=64 with max_wait 2 ms: while a batch is in flight, arrivals
     are held until 64 wait or the oldest waited 2 ms."""
