@@ -287,6 +287,7 @@ constexpr int kTopkBatchMin = HCG_TOPK_BATCH_MIN;
 // (vecio.cpp:102-105) a plain integer order.
 template <int R>
 struct WarpTopK {
+    static constexpr int kR = R;
     uint64_t a[R];
     uint64_t thr;  // current k-th smallest (kNone until k elements seen)
     int thr_lane, thr_reg;
@@ -411,6 +412,52 @@ struct WarpTopK {
             m &= ~(1u << src);
             m &= __ballot_sync(kFull, cand < thr);
         }
+    }
+
+    // offer_unique for long walks at k > 32: offers that may beat the
+    // threshold are appended to the warp's shared queue wq (qcap <= 32 slots,
+    // qn entries, warp-uniform) and a full queue is sorted, merged and
+    // deduplicated in one go, so a pass with a few passing offers costs a
+    // ballot and a store instead of a merge or one insertion each.  Offers
+    // carry the physical row in the low word; the queue translates it through
+    // idtab (row -> id) when it flushes, one load latency per flush instead of
+    // one per pass, so the filter compares distances only (ties pass and the
+    // merge sorts them out).  A merge of qcap values pushes out at most qcap
+    // repeats: exact while 32 * R - qcap >= k.  The threshold only falls, so
+    // nothing the queue holds is lost; flush_queue() after the last offer.
+    __device__ __forceinline__ void offer_queued(uint64_t cand, int lane, uint64_t* wsm, uint64_t* wq, uint32_t& qn,
+                                                 uint32_t qcap, const uint32_t* idtab) {
+        const bool pass = cand != kNone && uint32_t(cand >> 32) <= uint32_t(thr >> 32);
+        unsigned m = __ballot_sync(kFull, pass);
+        while (m) {
+            const uint32_t take = min(uint32_t(__popc(m)), qcap - qn);
+            const bool mine = (m >> lane) & 1u;
+            const uint32_t rank = __popc(m & ((1u << lane) - 1u));
+            const bool store = mine && rank < take;
+            if (store) wq[qn + rank] = cand;
+            m &= ~__ballot_sync(kFull, store);
+            qn += take;
+            if (qn == qcap) {
+                flush_queue(lane, wsm, wq, qn, idtab);
+                m &= __ballot_sync(kFull, uint32_t(cand >> 32) <= uint32_t(thr >> 32));
+            }
+        }
+    }
+
+    __device__ __forceinline__ void flush_queue(int lane, uint64_t* wsm, const uint64_t* wq, uint32_t& qn,
+                                                const uint32_t* idtab) {
+        if (qn == 0) return;
+        __syncwarp();
+        uint64_t c = kNone;
+        if (uint32_t(lane) < qn) {
+            c = wq[lane];
+            c = (c & 0xFFFFFFFF00000000ull) | __ldg(idtab + uint32_t(c));
+        }
+        merge_sorted32<R>(a, warp_sort_asc(c, lane), lane);
+        dedup_sorted(lane, wsm);
+        update_thr();
+        __syncwarp();  // every lane read its entry before the queue refills
+        qn = 0;
     }
 };
 

@@ -546,10 +546,11 @@ __device__ __forceinline__ void gather_list(const RefineArgs& a, const uint32_t*
     }
 }
 
-// K3c without the union (k <= 32, rows in curve-0 order): the warp walks the
-// query's C windows directly -- entry e is position e % take of curve
-// e / take -- and offers every row; a row reached through two curves gives
-// the same (distance, id) key twice and offer_unique keeps one.  Costs the
+// K3c without the union (rows in curve-0 order): the warp walks the query's C
+// windows directly -- entry e is position e % take of curve e / take -- and
+// offers every row; a row reached through two curves gives the same
+// (distance, id) key twice and the queued merge keeps one
+// (WarpTopK::offer_queued: a queue of min(32, 32 R - k) offers).  Costs the
 // duplicate rows (~16 % of the windows, partly L2 hits) instead of the union
 // kernel and the lists' round trip.
 // SMALLC (C <= 32): lane c holds curve c's window start pointer (slots[c] +
@@ -583,6 +584,9 @@ __device__ __forceinline__ void gather_windows(const RefineArgs& a, const uint32
     uint32_t nx[8];
 #pragma unroll
     for (int r = 0; r < 8; ++r) nx[r] = entry(r);
+    // the offer queue (WarpTopK::offer_queued) behind the dedup scratch
+    uint32_t qn = 0;
+    const uint32_t qcap = min(32u, 32u * TK::kR - a.k);
     for (uint32_t base = 0; base < n; base += 32) {
         uint4 v[8][CR];
 #pragma unroll
@@ -630,13 +634,11 @@ __device__ __forceinline__ void gather_windows(const RefineArgs& a, const uint32
             s2[i] = keep + __shfl_xor_sync(kFull, send, 2);
         }
         const uint32_t S = (b0 ? s2[1] : s2[0]) + __shfl_xor_sync(kFull, b0 ? s2[0] : s2[1], 1);
-        uint32_t sl = me;
-        if (a.idtab) {
-            const bool pre = me != kEmpty && S <= uint32_t(tk.thr >> 32);
-            if (__any_sync(kFull, pre) && pre) sl = __ldg(a.idtab + me);
-        }
-        tk.offer_unique(me != kEmpty ? ((uint64_t(S) << 32) | sl) : kNone, lane, wsm);
+        // the queue translates rows to ids when it flushes
+        tk.offer_queued(me != kEmpty ? ((uint64_t(S) << 32) | me) : kNone, lane, wsm, wsm + 32 * TK::kR, qn, qcap,
+                        a.idtab);
     }
+    tk.flush_queue(lane, wsm, wsm + 32 * TK::kR, qn, a.idtab);
 }
 
 template <int CR>
@@ -673,10 +675,10 @@ __global__ void __launch_bounds__(kRefineThreads, MINB) k_gather(RefineArgs a, c
 // K3c without the union: one warp per query over the raw windows.
 template <int R, int CR, int MINB, bool SMALLC, int NT = kRefineThreads>
 __global__ void __launch_bounds__(NT, MINB) k_gather_nu(RefineArgs a) {
-    // per-warp scratch of the batched dedup (R >= 2 only)
-    __shared__ uint64_t dsm[R >= 2 ? NT / 32 : 1][R >= 2 ? 32 * R : 1];
+    // per-warp scratch of the batched dedup + the offer queue
+    __shared__ uint64_t dsm[NT / 32][32 * R + 32];
     const int lane = threadIdx.x & 31;
-    uint64_t* wsm = R >= 2 ? dsm[threadIdx.x >> 5] : nullptr;
+    uint64_t* wsm = dsm[threadIdx.x >> 5];
     const uint32_t qstep = gridDim.x * (NT / 32);
     for (uint32_t q = (blockIdx.x * NT + threadIdx.x) >> 5; q < a.nq; q += qstep) {
         const uint32_t qq = a.qorder ? __ldg(a.qorder + q) : q;
@@ -1513,27 +1515,39 @@ constexpr uint64_t kMaxWalk = uint64_t(1) << 27;
 // The union-less K3c (k_gather_nu) serves k <= 128, u8 rows in curve-0
 // order and batches of >= 16K queries; everything else runs the separate
 // union (K3b) + K3c.  One predicate for the scratch query and the launch.
-// k > 32 pays for the merge + dedup of repeats (and wider lists) in the walk;
-// that beats the union's hash rounds only for long walks: measured at 10M,
-// C = 8, 100K queries (profiles/r02_unionless_k_ab.jsonl), k = 64 / 100 union-less vs
-// union + gather: D = 350 8.1 / 10.2 vs 6.7 / 7.5 ms, D = 1024 18.3 / 21.9 vs
-// 23.1 / 23.6 ms; k <= 32 is faster union-less at every depth.
-constexpr uint32_t kUnionlessWideWalk = 8192;  // C x take from which k > 32 walks union-less
+// k <= 16 is faster union-less at every depth; wider lists pay for their
+// merges in the walk, which beats the union's hash rounds from moderate walks
+// on.  Measured at 10M, C = 8, 100K queries (profiles/r02_unionless_wq.jsonl,
+// M q/s, union-less vs union + gather): C x take = 1024 (D = 128) k = 17 / 32
+// / 48 / 100 / 128: 34.7 / 33.2 / 32.0 / 28.1 / 22.5 vs 38.5 / 37.4 / 34.8 /
+// 27.6 / 26.6; C x take = 2800 (D = 350): 15.9 / 16.5 / 15.4 / 14.2 / 12.0
+// vs 15.6 / 15.5 / 15.1 / 13.4 / 12.9; C x take = 8192: union-less ahead by
+// 25-45 % at every k.
+constexpr uint32_t kUnionlessWalk = 2048;    // C x take from which 16 < k <= 112 walks union-less
+constexpr uint32_t kUnionlessWalkR8 = 8192;  // ... 112 < k <= 128
+// The union-less walk's list widths R = 1 / 2 / 4 / 8 by k (launch_gather_nu).
+constexpr uint32_t kNuR1MaxK = 16, kNuR2MaxK = 48, kNuR4MaxK = 112;
 
 template <int R>
 bool unionless_path(const RefineArgs& a) {
     static const bool off = knob("HCG_NO_UNIONLESS") != nullptr;  // A/B: separate union for every k
     static const bool wide = knob("HCG_UNIONLESS_WIDE") != nullptr;  // A/B: union-less for every k <= 128
     if (R > 4 || a.k > 128 || off) return false;
-    if (a.k > 32 && !wide && uint64_t(a.C) * a.take < kUnionlessWideWalk) return false;
+    const uint64_t walk = uint64_t(a.C) * a.take;
+    const uint64_t need = a.k <= kNuR1MaxK ? 0 : a.k <= kNuR4MaxK ? kUnionlessWalk : kUnionlessWalkR8;
+    if (!wide && walk < need) return false;
     return a.mode != kOutCandidates && a.dtype == HCG_U8 && a.nq >= 16384 && a.idtab != nullptr;
 }
 
-// The union-less walk's list width: k <= 32 inserts one offer at a time
-// (R = 1); larger k merge batches of offers and dedup after the merge, which
-// needs 32 spare slots: k <= 32 * (R - 1).
+// The union-less walk's list width: offers are queued and a full queue of
+// min(32, 32 R - k) is merged + deduplicated at a time
+// (WarpTopK::offer_queued); each width serves the k that leave a queue of
+// >= 16.
 #ifndef HCG_NU_MINB1
 #define HCG_NU_MINB1 3
+#endif
+#ifndef HCG_NU_MINB2
+#define HCG_NU_MINB2 3
 #endif
 #ifndef HCG_NU_MINB4
 #define HCG_NU_MINB4 2
@@ -1543,11 +1557,12 @@ bool unionless_path(const RefineArgs& a) {
 #endif
 template <int CR, bool SMALLC>
 hcg_status launch_gather_nu(const RefineArgs& a, int device, int sms, cudaStream_t st) {
-    auto nk = a.k <= 32 ? k_gather_nu<1, CR, HCG_NU_MINB1, SMALLC>
-              : a.k <= 96 ? k_gather_nu<4, CR, HCG_NU_MINB4, SMALLC>
-                          : k_gather_nu<8, CR, HCG_NU_MINB8, SMALLC>;
-    const int kb = a.k <= 32 ? 0 : a.k <= 96 ? 1 : 2;
-    static int per_sm_cache[64][3] = {};
+    auto nk = a.k <= kNuR1MaxK   ? k_gather_nu<1, CR, HCG_NU_MINB1, SMALLC>
+              : a.k <= kNuR2MaxK ? k_gather_nu<2, CR, HCG_NU_MINB2, SMALLC>
+              : a.k <= kNuR4MaxK ? k_gather_nu<4, CR, HCG_NU_MINB4, SMALLC>
+                                 : k_gather_nu<8, CR, HCG_NU_MINB8, SMALLC>;
+    const int kb = a.k <= kNuR1MaxK ? 0 : a.k <= kNuR2MaxK ? 1 : a.k <= kNuR4MaxK ? 2 : 3;
+    static int per_sm_cache[64][4] = {};
     int& per_sm = per_sm_cache[device & 63][kb];
     if (per_sm == 0) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nk, kRefineThreads, 0);
