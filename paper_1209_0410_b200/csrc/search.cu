@@ -1526,7 +1526,10 @@ constexpr uint64_t kMaxWalk = uint64_t(1) << 27;
 constexpr uint32_t kUnionlessWalk = 2048;    // C x take from which 16 < k <= 112 walks union-less
 constexpr uint32_t kUnionlessWalkR8 = 8192;  // ... 112 < k <= 128
 // The union-less walk's list widths R = 1 / 2 / 4 / 8 by k (launch_gather_nu).
-constexpr uint32_t kNuR1MaxK = 16, kNuR2MaxK = 48, kNuR4MaxK = 112;
+#ifndef HCG_NU_R1_MAXK
+#define HCG_NU_R1_MAXK 16
+#endif
+constexpr uint32_t kNuR1MaxK = HCG_NU_R1_MAXK, kNuR2MaxK = 48, kNuR4MaxK = 112;
 
 template <int R>
 bool unionless_path(const RefineArgs& a) {

@@ -94,8 +94,8 @@ def test_random_configurations_f32(seed):
 @pytest.mark.parametrize("seed", range(16))
 def test_random_configurations_large_batch(seed):
     """>= 16K queries with k <= 128: the union-less gather (k_gather_nu walks the
-    C windows and drops repeated candidates in the top-k; k > 32 merges
-    batches of offers and dedups after the merge) over random schemes,
+    C windows, queues its offers and merges + dedups a full queue; list
+    widths R = 1 / 2 / 4 / 8 switch at k = 16 / 48 / 112) over random schemes,
     row widths, depths (windows past both ends included) and views."""
     rng = np.random.default_rng(9000 + seed)
     d_full = int(rng.choice([16, 24, 64, 100, 128]))
@@ -109,7 +109,7 @@ def test_random_configurations_large_batch(seed):
     n = int(rng.integers(1, 12_000))
     nq = int(rng.choice([16_384, 17_001]))
     depth = int(rng.choice([1, 3, 50, 350, 2000]))
-    k = int(rng.choice([1, 10, 32, 33, 64, 96, 100, 128]))
+    k = int(rng.choice([1, 10, 16, 17, 32, 33, 48, 49, 64, 96, 100, 112, 113, 128]))
     rows = rng.integers(0, 256, (n, d_full), dtype=np.uint8)
     if n > 50:
         rows[n // 2:n // 2 + 20] = rows[0]  # ties and repeats across curves
@@ -131,18 +131,40 @@ def test_random_configurations_large_batch(seed):
         assert (ids[q, L:] == np.uint64(2**64 - 1)).all()
 
 
-@pytest.mark.parametrize("k", [33, 64, 100, 128])
-def test_unionless_wide_k_long_walks(k):
-    """k > 32 with C x depth >= 8192 (and >= 16K queries): the union-less walk
-    with batched merges and the dedup of repeats after each merge."""
+@pytest.mark.parametrize("k,depth", [(16, 1100), (17, 300), (33, 1100), (48, 300), (64, 1100), (100, 300),
+                                     (112, 1100), (113, 1100), (128, 1100)])
+def test_unionless_wide_k_long_walks(k, depth):
+    """k > 16 on walks of C x depth >= 2048 (>= 8192 for k > 112) and >= 16K
+    queries: the union-less walk with queued offers, merged and deduplicated
+    per full queue, at every list width and both sides of each switch."""
     n = 12_000
     rows = P.gen_rows(0, n)
     qs = P.gen_queries(0, 16_384, n)
     gi = H.MulticurvesIndex(rows, H.default_scheme(128, 8, 16), H.LIFTED)
-    assert gi.unionless(16_384, k, 1100)
+    assert gi.unionless(16_384, k, depth)
     oi = P.Oracle(H.LIFTED.floats(rows), 8, 16)
-    ids, sq, ln = gi.search_batch(qs, k, 1100)
-    oids, odist, oln = oi.search(H.LIFTED.floats(qs), k, 1100)
+    ids, sq, ln = gi.search_batch(qs, k, depth)
+    oids, odist, oln = oi.search(H.LIFTED.floats(qs), k, depth)
+    np.testing.assert_array_equal(ln, oln)
+    np.testing.assert_array_equal(ids, oids)
+    assert gi.rooted(sq).tobytes() == odist.tobytes()
+
+
+@pytest.mark.parametrize("k", [10, 40, 100])
+def test_unionless_many_ties(k):
+    """Rows of 0 / 1 bytes: most distances tie, so many offers sit exactly at
+    the k-th distance -- they pass the queue's distance-only filter and the
+    merge orders them by id (vecio.cpp:102-105)."""
+    rng = np.random.default_rng(77 + k)
+    n = 6000
+    rows = rng.integers(0, 2, (n, 128), dtype=np.uint8)
+    rows[100:400] = rows[0]  # exact repeats as well
+    qs = rng.integers(0, 2, (16_384, 128), dtype=np.uint8)
+    gi = H.MulticurvesIndex(rows, H.default_scheme(128, 8, 16), H.LIFTED)
+    assert gi.unionless(16_384, k, 700)
+    oi = P.Oracle(H.LIFTED.floats(rows), 8, 16)
+    ids, sq, ln = gi.search_batch(qs, k, 700)
+    oids, odist, oln = oi.search(H.LIFTED.floats(qs), k, 700)
     np.testing.assert_array_equal(ln, oln)
     np.testing.assert_array_equal(ids, oids)
     assert gi.rooted(sq).tobytes() == odist.tobytes()
