@@ -3,14 +3,16 @@
 
 One "step" = one batched search of a fresh batch of synthetic queries through
 the whole hot path (per-curve keys -> lower_bound -> windows -> dedup ->
-gather -> exact L2 -> top-k; at N>1 also the NCCL all-gather + merge).
+gather -> exact L2 -> top-k; at N>1 also the routed exchange + merge).
 
   N=1 : configs[1] -- 10M x 128-d uint8 (synthetic SIFT-like),
         100K queries per step, k=10, 8 Hilbert curves, probe depth 350,
         lifted view (1 + b/256, m=16; recall@10 ~0.99).
   N>1 : configs[2] -- 100M x 128-d sharded id mod N over N ranks (one process
         per GPU, torchrun), per-shard depth from the equivalence planner
-        (miss < 2%), NCCL all-gather of packed top-k + K4.
+        (miss < 2%); the packed top-k lists are routed to
+        their aggregator rank (route_to_aggregator: NCCL
+        send / recv of 1/N query blocks inside libhcg) and merged by K4.
 
 value   : queries/s with queries already resident in HBM (device timed,
           CUDA events, max over ranks).
@@ -179,8 +181,8 @@ def cpu_reference_qps(rows_u8, queries_u8, curves, m, kind, view, k, depth, thre
 def workload_name(n_total: int, Q: int, k: int, C: int, D: int, world: int) -> str:
     base = f"{n_total / 1e6:g}M x 128-d, {Q} queries/step, k={k}, {C} curves, probe depth {D}"
     if n_total >= 100_000_000:
-        tag = ("configs[2]: 100M sharded id mod N over N GPUs (hcg_shard_group: per-shard search, NCCL all-gather, "
-               "K4 merge)" if world > 1 else "configs[2] at N=1: 100M on one B200 (same-workload anchor)")
+        tag = ("configs[2]: 100M sharded id mod N over N GPUs (hcg_shard_group: per-shard search, routed NCCL "
+               "exchange of 1/N query blocks, K4 merge)" if world > 1 else "configs[2] at N=1: 100M on one B200 (same-workload anchor)")
     elif n_total == 10_000_000 and world == 1:
         tag = "configs[1]"
     elif n_total == 1_000_000:
@@ -479,7 +481,7 @@ def run_ours(a):
                 "launch_ms": round(gather_ms, 4),
                 # device time of the step's kernels (locate + batch order / union + refine), CUDA
                 # events on the launching stream; ms_per_step minus this is launch gaps + (N>1) the
-                # all-gather and merge
+                # exchange and merge
                 "kernel_ms_sum": round(statistics.median(tl) + union_ms + gather_ms, 4),
                 "other_kernels_ms": ({"k_locate": round(statistics.median(tl), 4),
                                       "batch_order_sort": round(union_ms, 4)} if unionless else
