@@ -312,7 +312,11 @@ uint32_t hcg_shard_group_dims(const hcg_shard_group* group);
  * SPEC.md:436), the server launches min(waiting, max_batch) queries when the
  * device is idle ("GPU idle"), when >= min_batch queries wait ("buffer
  * full"), or when the oldest waiting query has waited max_wait_s; otherwise
- * it keeps buffering.  FIFO, every query answered exactly once.
+ * it keeps buffering.  FIFO dispatch, every query answered exactly once
+ * (SPEC.md:491-493).  Serving one index, small batches (<= 512 queries: one
+ * SM per query) run side by side on their slots' own streams while their
+ * queries fit one CTA per SM and no large batch is in flight; together they
+ * count as one of the `slots` stages, and a large batch runs after them.
  * A batch is H2D (host queries -> device) -> search (one index, or a shard
  * group) -> D2H (results -> host), with uploads and downloads overlapping the
  * neighbouring batches' searches; a query's response time runs from its
@@ -321,7 +325,7 @@ typedef struct hcg_server_policy {
     uint32_t max_batch;  /* buffer capacity B                      */
     uint32_t min_batch;  /* launch when this many queries wait      */
     double max_wait_s;   /* launch when the oldest waited this long */
-    uint32_t slots;      /* batches in flight (1..8)                */
+    uint32_t slots;      /* pipeline stages in flight (1..8)         */
 } hcg_server_policy;
 typedef struct hcg_server hcg_server;
 
