@@ -451,7 +451,7 @@ struct WarpTopK {
         uint64_t c = kNone;
         if (uint32_t(lane) < qn) {
             c = wq[lane];
-            c = (c & 0xFFFFFFFF00000000ull) | __ldg(idtab + uint32_t(c));
+            if (idtab) c = (c & 0xFFFFFFFF00000000ull) | __ldg(idtab + uint32_t(c));
         }
         merge_sorted32<R>(a, warp_sort_asc(c, lane), lane);
         dedup_sorted(lane, wsm);

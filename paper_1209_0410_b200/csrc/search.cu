@@ -473,9 +473,14 @@ __global__ void __launch_bounds__(kRefineThreads) k_union(RefineArgs a, uint32_t
 // (8*grp + l8)'s squared distance in lane l8 of group grp, which offers
 // (sqdist << 32 | slot).  Lists are read with ld.global.cg: they were written
 // by the preceding union launch.
-template <int R, int CR, bool SMEMLIST = false>
+// QUEUED (one warp per list): offers go through the warp's queue
+// (WarpTopK::offer_queued; wsm: 32 R + 32 slots) -- the list holds no
+// repeats, so the queue takes 32 and a pass waits for no id.
+template <int R, int CR, bool SMEMLIST = false, bool QUEUED = false>
 __device__ __forceinline__ void gather_list(const RefineArgs& a, const uint32_t* list, uint32_t n, uint32_t start,
-                                            uint32_t step, const uint4 (&qv)[CR], int lane, WarpTopK<R>& tk) {
+                                            uint32_t step, const uint4 (&qv)[CR], int lane, WarpTopK<R>& tk,
+                                            uint64_t* wsm = nullptr) {
+    uint32_t qn = 0;
     const int l8 = lane & 7, grp = lane >> 3;
     const uint32_t chunks = a.pitch >> 4;
     auto ld = [&](uint32_t e) -> uint32_t { return SMEMLIST ? list[e] : __ldcg(list + e); };
@@ -535,6 +540,11 @@ __device__ __forceinline__ void gather_list(const RefineArgs& a, const uint32_t*
             s2[i] = keep + __shfl_xor_sync(kFull, send, 2);
         }
         const uint32_t S = (b0 ? s2[1] : s2[0]) + __shfl_xor_sync(kFull, b0 ? s2[0] : s2[1], 1);
+        if constexpr (QUEUED) {
+            tk.offer_queued(me != kEmpty ? ((uint64_t(S) << 32) | me) : kNone, lane, wsm, wsm + 32 * R, qn, 32u,
+                            a.idtab);
+            continue;
+        }
         uint32_t sl = me;
         if (SMEMLIST) {
             sl = idpre;
@@ -544,6 +554,7 @@ __device__ __forceinline__ void gather_list(const RefineArgs& a, const uint32_t*
         }
         tk.template offer<SMEMLIST>(me != kEmpty ? ((uint64_t(S) << 32) | sl) : kNone, lane);
     }
+    if constexpr (QUEUED) tk.flush_queue(lane, wsm, wsm + 32 * R, qn, a.idtab);
 }
 
 // K3c without the union (rows in curve-0 order): the warp walks the query's C
@@ -653,11 +664,22 @@ __device__ __forceinline__ void load_query(const RefineArgs& a, uint32_t q, int 
 }
 
 // K3c for large batches: one WARP per query (persistent grid-stride), no
-// shared memory and no barriers.
+// barriers.  Lists of 32 and 128 / 256 take their offers through a per-warp
+// queue in shared memory (WarpTopK::offer_queued); the 64-entry list keeps
+// per-pass offers, 3-4 % faster there (profiles/r02_gather_queue_ab.jsonl:
+// k = 100 at D = 350 6.66 vs 7.50 ms, k = 32 2.55 vs 2.68 ms at D = 128, k =
+// 64 7.04 vs 6.76 ms at D = 350).
+#ifndef HCG_GATHER_QUEUE
+#define HCG_GATHER_QUEUE 1
+#endif
+template <int R>
+constexpr bool kGatherQueued = HCG_GATHER_QUEUE && R != 2;
+
 template <int R, int CR, int MINB>
 __global__ void __launch_bounds__(kRefineThreads, MINB) k_gather(RefineArgs a, const uint32_t* __restrict__ lists,
                                                                  const uint32_t* __restrict__ counts,
                                                                  uint32_t lstride) {
+    __shared__ uint64_t dsm[kGatherQueued<R> ? kRefineThreads / 32 : 1][kGatherQueued<R> ? 32 * R + 32 : 1];
     const int lane = threadIdx.x & 31;
     const uint32_t qstep = gridDim.x * (kRefineThreads / 32);
     for (uint32_t q = (blockIdx.x * kRefineThreads + threadIdx.x) >> 5; q < a.nq; q += qstep) {
@@ -667,7 +689,8 @@ __global__ void __launch_bounds__(kRefineThreads, MINB) k_gather(RefineArgs a, c
         load_query<CR>(a, qq, lane, qv);
         WarpTopK<R> tk;
         tk.init(int(a.k));
-        gather_list<R, CR>(a, lists + uint64_t(q) * lstride, n, 0, 32, qv, lane, tk);
+        gather_list<R, CR, false, kGatherQueued<R>>(a, lists + uint64_t(q) * lstride, n, 0, 32, qv, lane, tk,
+                                                    dsm[kGatherQueued<R> ? threadIdx.x >> 5 : 0]);
         write_result<R>(a, qq, tk, lane, n);
     }
 }
@@ -1516,15 +1539,18 @@ constexpr uint64_t kMaxWalk = uint64_t(1) << 27;
 // order and batches of >= 16K queries; everything else runs the separate
 // union (K3b) + K3c.  One predicate for the scratch query and the launch.
 // k <= 16 is faster union-less at every depth; wider lists pay for their
-// merges in the walk, which beats the union's hash rounds from moderate walks
-// on.  Measured at 10M, C = 8, 100K queries (profiles/r02_unionless_wq.jsonl,
-// M q/s, union-less vs union + gather): C x take = 1024 (D = 128) k = 17 / 32
-// / 48 / 100 / 128: 34.7 / 33.2 / 32.0 / 28.1 / 22.5 vs 38.5 / 37.4 / 34.8 /
-// 27.6 / 26.6; C x take = 2800 (D = 350): 15.9 / 16.5 / 15.4 / 14.2 / 12.0
-// vs 15.6 / 15.5 / 15.1 / 13.4 / 12.9; C x take = 8192: union-less ahead by
-// 25-45 % at every k.
-constexpr uint32_t kUnionlessWalk = 2048;    // C x take from which 16 < k <= 112 walks union-less
-constexpr uint32_t kUnionlessWalkR8 = 8192;  // ... 112 < k <= 128
+// merges in the walk, which beats the union + gather from moderate walks on;
+// the union gather's 64-entry list (k <= 64) takes per-pass offers, the
+// others a queue (k_gather), so the crossover moves up at k = 64.  Measured at
+// 10M, C = 8, 100K queries, same box interleaved
+// (profiles/r02_gather_queue4.jsonl, ms): C x take = 2800 (D = 350) k = 64:
+// union-less 6.39 vs union 6.79; k = 100: 6.89 vs 6.66; k = 128: 7.72 (the
+// previous union gather) vs 6.72; C x take = 1024 (D = 128): the union at
+// every k > 16 (r02_gather_queue2.jsonl: 2.54-3.00 vs 2.70-4.41 ms); C x take
+// = 8192 (D = 1024): union-less 15.9-19.2 vs 23.4-23.7 at every k.
+constexpr uint32_t kUnionlessWalk = 2048;     // C x take from which 16 < k <= 64 walks union-less
+constexpr uint32_t kUnionlessWalkWide = 4096; // ... 64 < k <= 112
+constexpr uint32_t kUnionlessWalkR8 = 6144;   // ... 112 < k <= 128
 // The union-less walk's list widths R = 1 / 2 / 4 / 8 by k (launch_gather_nu).
 #ifndef HCG_NU_R1_MAXK
 #define HCG_NU_R1_MAXK 16
@@ -1537,7 +1563,8 @@ bool unionless_path(const RefineArgs& a) {
     static const bool wide = knob("HCG_UNIONLESS_WIDE") != nullptr;  // A/B: union-less for every k <= 128
     if (R > 4 || a.k > 128 || off) return false;
     const uint64_t walk = uint64_t(a.C) * a.take;
-    const uint64_t need = a.k <= kNuR1MaxK ? 0 : a.k <= kNuR4MaxK ? kUnionlessWalk : kUnionlessWalkR8;
+    const uint64_t need = a.k <= kNuR1MaxK ? 0 : a.k <= 64 ? kUnionlessWalk
+                          : a.k <= kNuR4MaxK ? kUnionlessWalkWide : kUnionlessWalkR8;
     if (!wide && walk < need) return false;
     return a.mode != kOutCandidates && a.dtype == HCG_U8 && a.nq >= 16384 && a.idtab != nullptr;
 }

@@ -131,10 +131,10 @@ def test_random_configurations_large_batch(seed):
         assert (ids[q, L:] == np.uint64(2**64 - 1)).all()
 
 
-@pytest.mark.parametrize("k,depth", [(16, 1100), (17, 300), (33, 1100), (48, 300), (64, 1100), (100, 300),
-                                     (112, 1100), (113, 1100), (128, 1100)])
+@pytest.mark.parametrize("k,depth", [(16, 1100), (17, 300), (32, 260), (33, 1100), (48, 300), (49, 300), (64, 260), (65, 520), (100, 600),
+                                     (112, 1100), (113, 800), (128, 1100)])
 def test_unionless_wide_k_long_walks(k, depth):
-    """k > 16 on walks of C x depth >= 2048 (>= 8192 for k > 112) and >= 16K
+    """k > 16 on walks of C x depth >= 2048 (4096 for k > 64, 6144 for k > 112) and >= 16K
     queries: the union-less walk with queued offers, merged and deduplicated
     per full queue, at every list width and both sides of each switch."""
     n = 12_000
