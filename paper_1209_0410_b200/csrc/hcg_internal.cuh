@@ -389,32 +389,7 @@ struct WarpTopK {
     }
 
     // offer() for candidate streams that may repeat a value (the same row
-    // reached through two curves): a value already held is not inserted again.
-    // Many passing offers (R >= 2, wsm given) are sorted, merged and then
-    // deduplicated in one go; a merge can push out up to 32 values that later
-    // turn out to be repeats, so the list keeps >= 32 * (R - 1) distinct
-    // values: k <= 32 * (R - 1) stays exact (the caller picks R that way).
-    __device__ __forceinline__ void offer_unique(uint64_t cand, int lane, uint64_t* wsm = nullptr) {
-        unsigned m = __ballot_sync(kFull, cand < thr);
-        if (R >= 2 && wsm && __popc(m) >= kTopkBatchMin) {
-            merge_sorted32<R>(a, warp_sort_asc(cand < thr ? cand : kNone, lane), lane);
-            dedup_sorted(lane, wsm);
-            update_thr();
-            return;
-        }
-        while (m) {
-            const int src = __ffs(m) - 1;
-            const uint64_t x = __shfl_sync(kFull, cand, src);
-            bool held = false;
-#pragma unroll
-            for (int r = 0; r < R; ++r) held |= a[r] == x;
-            if (!__any_sync(kFull, held)) insert(x, lane);
-            m &= ~(1u << src);
-            m &= __ballot_sync(kFull, cand < thr);
-        }
-    }
-
-    // offer_unique for long walks at k > 32: offers that may beat the
+    // reached through two curves) and for long lists: offers that may beat the
     // threshold are appended to the warp's shared queue wq (qcap <= 32 slots,
     // qn entries, warp-uniform) and a full queue is sorted, merged and
     // deduplicated in one go, so a pass with a few passing offers costs a
